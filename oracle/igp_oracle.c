@@ -1,0 +1,308 @@
+/*
+ * igp_oracle.c — fp64 CPU ORACLE for InfraredGP's feed-forward propagation (FFP).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2508_19737_b200/, include/igp.h, libigp.so) never links, imports or
+ * calls anything in oracle/, and this file shares no code, header, table or
+ * constant generator with the CUDA path.
+ *
+ * It is deliberately plain and slow: every step follows PAPER.md (arXiv
+ * 2508.19737, the paper's LaTeX source) in the paper's order and notation,
+ * in double precision, with no blocking, fusion or algebraic reordering.
+ *   - Problem statement / adjacency:   PAPER.md:126-127 (§II)
+ *   - Eq. (1) negative correction:     PAPER.md:101-105 (§I)
+ *   - D_tau = D + tau I for tau >= 0:  PAPER.md:91 (§I)
+ *   - Eq. (2)/(3) filter + spatial conv: PAPER.md:143-157 (§III-A)
+ *   - random input N(0, 1/d):          PAPER.md:161 (§III-A), Alg. 1 l.2 PAPER.md:186
+ *   - Eq. (4) layer, ZNorm, sigmoid:   PAPER.md:163-166 (§III-A), Alg. 1 l.3-6 PAPER.md:187-192
+ * Readings where the paper is silent (population std, the 1e-8 std floor,
+ * isolated nodes, the Philox counter layout, ...) are listed in DESIGN.md §3.
+ *
+ * Parity pins: every exported function here is pinned by tests/test_oracle_*.py
+ * against closed forms, brute force, numpy eigh spectral forms, cuRAND's
+ * Philox (host-compiled library header), and invariants.  No function is
+ * "parity unpinned".
+ *
+ * Threads: an optional OpenMP loop over *rows* in oracle_propagate only; each
+ * row's neighbour sum stays sequential in ascending neighbour id and all column
+ * statistics stay serial, so the result is bitwise independent of the thread
+ * count.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_ERR_INPUT (-2)
+#define ORACLE_ERR_RANGE (-1)
+
+/* ------------------------------------------------------------------------ */
+/* Graph: A in {0,1}^{N x N}, A_ij = A_ji = 1 iff (v_i, v_j) in E            */
+/* (PAPER.md:127).  No self loops (A is built from E only, no I + A).        */
+/* Canonical CSR: rows ascending, columns strictly ascending within a row.   */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int32_t a;
+    int32_t b;
+} oracle_pair;
+
+static int cmp_pair(const void* x, const void* y) {
+    const oracle_pair* p = (const oracle_pair*)x;
+    const oracle_pair* q = (const oracle_pair*)y;
+    if (p->a != q->a) return p->a < q->a ? -1 : 1;
+    if (p->b != q->b) return p->b < q->b ? -1 : 1;
+    return 0;
+}
+
+/* Returns nnz = 2M (>= 0), ORACLE_ERR_RANGE if an index is outside [0, N),
+ * ORACLE_ERR_INPUT if N <= 0 or E < 0.  row_ptr has N+1 entries; col_idx must
+ * hold 2*E entries (upper bound of 2M).  *m_out receives M. */
+int64_t oracle_build_csr(const int32_t* edges, int64_t E, int32_t N,
+                         int32_t* row_ptr, int32_t* col_idx, int64_t* m_out) {
+    if (N <= 0 || E < 0) return ORACLE_ERR_INPUT;
+    oracle_pair* und = (oracle_pair*)malloc((size_t)(E > 0 ? E : 1) * sizeof(oracle_pair));
+    if (!und) return ORACLE_ERR_INPUT;
+    int64_t n_und = 0;
+    for (int64_t e = 0; e < E; ++e) {
+        int32_t u = edges[2 * e], v = edges[2 * e + 1];
+        if (u < 0 || u >= N || v < 0 || v >= N) {
+            free(und);
+            return ORACLE_ERR_RANGE;
+        }
+        if (u == v) continue; /* no self loops */
+        und[n_und].a = u < v ? u : v; /* unordered pair {u, v} */
+        und[n_und].b = u < v ? v : u;
+        ++n_und;
+    }
+    qsort(und, (size_t)n_und, sizeof(oracle_pair), cmp_pair);
+    int64_t M = 0; /* unique unordered pairs */
+    for (int64_t e = 0; e < n_und; ++e)
+        if (M == 0 || cmp_pair(&und[e], &und[M - 1]) != 0) und[M++] = und[e];
+    /* both orientations (A symmetric), sorted by (row, col) */
+    oracle_pair* dir = (oracle_pair*)malloc((size_t)(2 * M > 0 ? 2 * M : 1) * sizeof(oracle_pair));
+    if (!dir) {
+        free(und);
+        return ORACLE_ERR_INPUT;
+    }
+    for (int64_t e = 0; e < M; ++e) {
+        dir[2 * e].a = und[e].a;
+        dir[2 * e].b = und[e].b;
+        dir[2 * e + 1].a = und[e].b;
+        dir[2 * e + 1].b = und[e].a;
+    }
+    free(und);
+    qsort(dir, (size_t)(2 * M), sizeof(oracle_pair), cmp_pair);
+    for (int32_t i = 0; i <= N; ++i) row_ptr[i] = 0;
+    for (int64_t e = 0; e < 2 * M; ++e) row_ptr[dir[e].a + 1] += 1;
+    for (int32_t i = 0; i < N; ++i) row_ptr[i + 1] += row_ptr[i];
+    for (int64_t e = 0; e < 2 * M; ++e) col_idx[e] = dir[e].b;
+    free(dir);
+    if (m_out) *m_out = M;
+    return 2 * M;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Eq. (1):  (D_tau)_ii = deg_i - min{|tau|, deg_i - eps}  for  */
+/* tau < 0;  PAPER.md:91:  D_tau = D + tau I  otherwise.                     */
+/* ------------------------------------------------------------------------ */
+double oracle_corrected_degree(int32_t deg, double tau, double eps) {
+    if (tau < 0.0) {
+        double a = fabs(tau);
+        double b = (double)deg - eps;
+        double m = a < b ? a : b;
+        return (double)deg - m;
+    }
+    return (double)deg + tau;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon et al., SC'11) — the counter-based generator this   */
+/* build fixes for "random noise Theta ~ N(0, 1/d)" (the */
+/* paper names no generator, reading A11 in DESIGN.md).                      */
+/* ------------------------------------------------------------------------ */
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0;
+        c1 = n1;
+        c2 = n2;
+        c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+/* Raw 32-bit draws r[k], k in [0, count): block b = k / 4 uses counter
+ * (lo32 b, hi32 b, lo32 sub, hi32 sub) and key (lo32 seed, hi32 seed); r[k]
+ * is word k % 4 of that block. */
+void oracle_philox_bits(uint64_t seed, uint64_t sub, int64_t count, uint32_t* out) {
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int64_t b = 0; 4 * b < count; ++b) {
+        uint32_t ctr[4] = {(uint32_t)b, (uint32_t)((uint64_t)b >> 32), (uint32_t)sub,
+                           (uint32_t)(sub >> 32)};
+        uint32_t w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        for (int q = 0; q < 4 && 4 * b + q < count; ++q) out[4 * b + q] = w[q];
+    }
+}
+
+/* X ~ N(0,1) by Box-Muller on consecutive pairs (r0,r1), (r2,r3) of each
+ * block:  u = (r_even + 1/2) 2^-32,  v = (r_odd + 1/2) 2^-32,
+ * n_even = sqrt(-2 ln u) sin(2 pi v),  n_odd = sqrt(-2 ln u) cos(2 pi v).
+ * count must be a multiple of 4 (d % 4 == 0 in this build). */
+void oracle_box_muller(uint32_t r_even, uint32_t r_odd, double out[2]) {
+    const double two32inv = 1.0 / 4294967296.0;
+    const double two_pi = 6.283185307179586476925286766559;
+    double u = ((double)r_even + 0.5) * two32inv;
+    double v = ((double)r_odd + 0.5) * two32inv;
+    double R = sqrt(-2.0 * log(u));
+    out[0] = R * sin(two_pi * v);
+    out[1] = R * cos(two_pi * v);
+}
+
+void oracle_normal(uint64_t seed, uint64_t sub, int64_t count, double* out) {
+    uint32_t* r = (uint32_t*)malloc((size_t)(count > 0 ? count : 1) * sizeof(uint32_t));
+    oracle_philox_bits(seed, sub, count, r);
+    for (int64_t k = 0; k + 1 < count; k += 2) oracle_box_muller(r[k], r[k + 1], &out[k]);
+    free(r);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Eq. (3), PAPER.md:155 (general Eq. (2) form with (alpha, theta)):          */
+/*   phi * Z = theta Z + alpha D_tau^{-1/2} A D_tau^{-1/2} Z                  */
+/* i.e.  P_i = theta Z_i + alpha s_i sum_{j in N(i)} s_j Z_j,  s = D^{-1/2}.  */
+/* Dtau[i] is the corrected degree; an isolated row's neighbour term is the  */
+/* empty sum (0), so its s is never used (reading A5).                        */
+/* ------------------------------------------------------------------------ */
+void oracle_propagate(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int32_t d,
+                      const double* Dtau, const double* Z, double theta, double alpha,
+                      int32_t nthreads, double* P) {
+    (void)nthreads;
+    /* s = D_tau^{-1/2} (the diagonal of D_tau^{-1/2}); only non-isolated rows use it */
+    double* s = (double*)malloc((size_t)N * sizeof(double));
+    for (int32_t i = 0; i < N; ++i) s[i] = 1.0 / sqrt(Dtau[i]);
+#ifdef _OPENMP
+    int nt = nthreads > 0 ? nthreads : 1;
+#pragma omp parallel num_threads(nt)
+#endif
+    {
+        double* nb = (double*)malloc((size_t)d * sizeof(double));
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 256)
+#endif
+        for (int32_t i = 0; i < N; ++i) {
+            double* Pi = P + (int64_t)i * d;
+            const double* Zi = Z + (int64_t)i * d;
+            int32_t beg = row_ptr[i], end = row_ptr[i + 1];
+            /* nb_c = sum_{j in N(i)} s_j Z_jc, each column summed in ascending j */
+            for (int32_t c = 0; c < d; ++c) nb[c] = 0.0;
+            for (int32_t e = beg; e < end; ++e) {
+                int32_t j = col_idx[e];
+                const double* Zj = Z + (int64_t)j * d;
+                for (int32_t c = 0; c < d; ++c) nb[c] += s[j] * Zj[c];
+            }
+            for (int32_t c = 0; c < d; ++c) {
+                double term = (end > beg) ? alpha * s[i] * nb[c] : 0.0;
+                Pi[c] = theta * Zi[c] + term;
+            }
+        }
+        free(nb);
+    }
+    free(s);
+}
+
+/* ZNorm(x) := (x - mu(x)) / s(x), column-wise, population
+ * standard deviation (reading A2); a column with s < 1e-8 becomes 0 (A3).
+ * In place on T (N x d, row-major).  Two passes, serial, ascending rows. */
+void oracle_zscore_columns(double* T, int32_t N, int32_t d) {
+    for (int32_t c = 0; c < d; ++c) {
+        double sum = 0.0;
+        for (int32_t i = 0; i < N; ++i) sum += T[(int64_t)i * d + c];
+        double mu = sum / (double)N;
+        double ss = 0.0;
+        for (int32_t i = 0; i < N; ++i) {
+            double x = T[(int64_t)i * d + c] - mu;
+            ss += x * x;
+        }
+        double s = sqrt(ss / (double)N);
+        for (int32_t i = 0; i < N; ++i) {
+            double* x = &T[(int64_t)i * d + c];
+            *x = (s < 1e-8) ? 0.0 : (*x - mu) / s;
+        }
+    }
+}
+
+/* modes for oracle_embed */
+#define ORACLE_MODE_FULL 0        /* Z~ = sigmoid(Z^(L))                        */
+#define ORACLE_MODE_PRE_SIGMOID 1 /* Z^(L)                                      */
+#define ORACLE_MODE_LINEAR 2      /* Z^(l) = phi * Z^(l-1), no tanh/ZNorm/sigmoid */
+
+/* Alg. 1 lines 1-6, one FFP:
+ *   1: D_tau via Eq. (1)
+ *   2: Theta ~ N(0, 1/d)          (Theta = X / sqrt(d), X from oracle_normal;
+ *                                   element (i, c) is draw k = i*d + c; A1, A11)
+ *   3: Z^(0) <- Theta             (or the caller's Z0 when Z0 != NULL)
+ *   4-5: Z^(l) <- ZNorm(tanh(phi * Z^(l-1)))   for l = 1..L
+ *   6: Z~ <- sigmoid(Z^(L))
+ * Returns 0, or ORACLE_ERR_INPUT on invalid arguments. */
+int oracle_embed(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int32_t d, int32_t L,
+                 double tau, double theta, double alpha, double eps, const double* Z0,
+                 uint64_t seed, uint64_t sub, int32_t mode, int32_t nthreads, double* out) {
+    if (N <= 0 || d <= 0 || L < 0 || (Z0 == NULL && d % 4 != 0)) return ORACLE_ERR_INPUT;
+    int64_t nd = (int64_t)N * d;
+    double* Dtau = (double*)malloc((size_t)N * sizeof(double));
+    double* Z = (double*)malloc((size_t)nd * sizeof(double));
+    double* P = (double*)malloc((size_t)nd * sizeof(double));
+    if (!Dtau || !Z || !P) {
+        free(Dtau);
+        free(Z);
+        free(P);
+        return ORACLE_ERR_INPUT;
+    }
+    /* line 1 */
+    for (int32_t i = 0; i < N; ++i)
+        Dtau[i] = oracle_corrected_degree(row_ptr[i + 1] - row_ptr[i], tau, eps);
+    /* lines 2-3 */
+    if (Z0) {
+        memcpy(Z, Z0, (size_t)nd * sizeof(double));
+    } else {
+        oracle_normal(seed, sub, nd, Z);
+        double sq = sqrt((double)d);
+        for (int64_t k = 0; k < nd; ++k) Z[k] = Z[k] / sq; /* Theta = X / sqrt(d) */
+    }
+    /* lines 4-5 */
+    for (int32_t l = 1; l <= L; ++l) {
+        oracle_propagate(row_ptr, col_idx, N, d, Dtau, Z, theta, alpha, nthreads, P);
+        if (mode == ORACLE_MODE_LINEAR) {
+            memcpy(Z, P, (size_t)nd * sizeof(double));
+            continue;
+        }
+        for (int64_t k = 0; k < nd; ++k) P[k] = tanh(P[k]);
+        oracle_zscore_columns(P, N, d);
+        memcpy(Z, P, (size_t)nd * sizeof(double));
+    }
+    /* line 6 */
+    for (int64_t k = 0; k < nd; ++k)
+        out[k] = (mode == ORACLE_MODE_FULL) ? 1.0 / (1.0 + exp(-Z[k])) : Z[k];
+    free(Dtau);
+    free(Z);
+    free(P);
+    return 0;
+}
