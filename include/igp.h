@@ -1,0 +1,176 @@
+/*
+ * igp.h — C ABI of the B200-native InfraredGP feed-forward-propagation (FFP) library.
+ *
+ * InfraredGP (arXiv 2508.19737) embeds the nodes of an undirected, unweighted
+ * graph by pushing random Gaussian noise through L layers of a low-pass
+ * spectral-GNN filter on the negatively corrected graph Laplacian, with no
+ * training (§III).  This library implements Alg. 1 lines
+ * 1-6 on one GPU:
+ *
+ *   igp_build_graph   the problem statement's graph G = (V, E), A symmetric
+ *                     binary with no self loops, as a
+ *                     canonical device CSR;
+ *   igp_embed         Alg. 1 l.1-6: D_tau by Eq. (1) or
+ *                     D + tau I; Theta ~ N(0, 1/d) (PAPER.md:161,
+ *                     :186); L layers Z <- ZNorm(tanh(phi * Z)) with
+ *                     phi * Z = theta Z + alpha D^-1/2 A D^-1/2 Z (Eq. (2)/(3),
+ *                     PAPER.md:143-157; Eq. (4)); output
+ *                     Z~ = sigmoid(Z^(L)).
+ *
+ * Conventions (all functions):
+ *   - extern "C", no exceptions cross the ABI; every call returns igp_status.
+ *   - Pointers named d_* are DEVICE pointers (CUDA global memory of the current
+ *     device); h_* are HOST pointers (pageable or pinned).
+ *   - `stream` is a cudaStream_t (a CUstream handle) passed as void*; NULL means
+ *     the legacy default stream.  Work is enqueued on it; unless stated
+ *     otherwise the call returns before the work completes (asynchronous, like a
+ *     kernel launch) and device faults surface at the caller's next sync.
+ *   - On any non-OK status no output is written and no handle is created;
+ *     igp_last_error_message() gives a thread-local detail string.
+ *   - The library never falls back to the CPU: with no usable CUDA device every
+ *     call returns IGP_ERR_CUDA.
+ */
+#ifndef IGP_H_
+#define IGP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define IGP_API __attribute__((visibility("default")))
+#else
+#define IGP_API
+#endif
+
+typedef struct igp_graph_s* igp_graph_t;
+typedef void* igp_stream_t; /* cudaStream_t */
+
+typedef enum {
+    IGP_OK = 0,
+    IGP_ERR_INPUT = 2,       /* invalid argument or edge index out of range */
+    IGP_ERR_NUMERICAL = 4,   /* reserved */
+    IGP_ERR_CUDA = 5,        /* CUDA runtime/launch error (detail in igp_last_error_message) */
+    IGP_ERR_OOM = 6,         /* device allocation failed */
+    IGP_ERR_UNSUPPORTED = 7  /* valid request outside this build's envelope (e.g. d not in {16,32,64,128}) */
+} igp_status;
+
+/* ---------------------------------------------------------------------------
+ * Graph construction  (§II: A_ij = A_ji = 1 iff (v_i,v_j) in E)
+ * ------------------------------------------------------------------------- */
+
+/* Build the canonical CSR of the undirected simple graph on num_nodes nodes.
+ *   d_edges    device, int32 [num_edges][2] row-major (u, v) pairs; borrowed for
+ *              the duration of the call only.  Duplicates, both orientations and
+ *              self loops are allowed: self loops are dropped, each unordered
+ *              pair {u, v}, u != v, becomes A_uv = A_vu = 1 once.
+ *   num_edges  >= 0 (0 is valid: M = 0, all degrees 0); 2*num_edges must be
+ *              <= INT32_MAX (else IGP_ERR_UNSUPPORTED).
+ *   num_nodes  N >= 1 (else IGP_ERR_INPUT).
+ *   out        receives a new handle owning device row_ptr int32[N+1] and
+ *              col_idx int32[2M] (rows ascending, columns strictly ascending).
+ * Errors: any index outside [0, N) -> IGP_ERR_INPUT (detected on the device and
+ * read back at the build's single host synchronisation).
+ * Synchronisation: exactly one stream sync (to read nnz and the error flag);
+ * the remaining compaction is enqueued on `stream` when the call returns. */
+IGP_API igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes,
+                           igp_stream_t stream, igp_graph_t* out);
+
+/* Query a graph: N, nnz = 2M (directed CSR entries) and M.  Any output pointer may be NULL. */
+IGP_API igp_status igp_graph_info(igp_graph_t g, int32_t* num_nodes, int64_t* nnz, int64_t* num_undirected_edges);
+
+/* Copy the canonical CSR (original node ids) into caller-owned device buffers
+ * d_row_ptr int32[N+1] and d_col_idx int32[nnz]; asynchronous on `stream`. */
+IGP_API igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t* d_col_idx, igp_stream_t stream);
+
+/* Release a graph (synchronises the device before freeing).  NULL is a no-op. */
+IGP_API igp_status igp_destroy_graph(igp_graph_t g);
+
+/* ---------------------------------------------------------------------------
+ * Embedding  (Alg. 1 lines 1-6)
+ * ------------------------------------------------------------------------- */
+
+#define IGP_MODE_FULL 0        /* Z~ = sigmoid(Z^(L))                      (Eq. (4)) */
+#define IGP_MODE_PRE_SIGMOID 1 /* Z^(L) (column z-scored), debug/test      */
+#define IGP_MODE_LINEAR 2      /* Z^(l) = phi * Z^(l-1): no tanh/ZNorm/sigmoid, debug/test */
+
+#define IGP_FLAG_TIME_LAYERS 1u /* record CUDA events around the L filter-step launches
+                                   (igp_last_layer_time_ms); makes the call mutate the handle */
+
+typedef struct {
+    float tau;            /* degree correction tau (Eq. (1) for tau < 0; D + tau I otherwise); finite */
+    int32_t d;            /* embedding dimensionality, one of 16, 32, 64, 128 */
+    int32_t steps;        /* L >= 0 filter steps (layers) */
+    uint64_t seed;        /* Philox key for Theta */
+    uint64_t subsequence; /* Philox subsequence (e.g. streaming stage t, Alg. 2 l.3) */
+    float theta;          /* Eq. (2) theta, default 0.1 */
+    float alpha;          /* Eq. (2) alpha, default 1.0 */
+    float eps;            /* Eq. (1) epsilon > 0, default 0.001 */
+    int32_t mode;         /* IGP_MODE_* */
+    uint32_t flags;       /* IGP_FLAG_* */
+} igp_embed_opts;
+
+/* Fill opts with the paper's defaults: theta 0.1, alpha 1, eps 1e-3, subsequence 0,
+ * mode FULL, flags 0 (tau/d/steps/seed left at 0 for the caller to set). */
+IGP_API void igp_embed_opts_default(igp_embed_opts* opts);
+
+/* Z~ for graph g written to d_out, device fp32 [N][d] row-major, caller-owned,
+ * row i = node id i, values in (0, 1).  Input Theta = X / sqrt(d) with X the
+ * Philox4x32-10/Box-Muller stream (seed, subsequence 0) of element k = i*d + c
+ * (readings A1, A11).  Fully asynchronous on `stream`; workspace is
+ * allocated stream-ordered (cudaMallocAsync) and released before return, so the
+ * handle is read-only and concurrent embeds on different streams are safe.
+ * Errors (host-validated, nothing enqueued): NULL g/d_out or non-finite tau ->
+ * IGP_ERR_INPUT; d not in {16,32,64,128} -> IGP_ERR_UNSUPPORTED; steps < 0 ->
+ * IGP_ERR_INPUT.  Deterministic: identical arguments give bitwise-identical output. */
+IGP_API igp_status igp_embed(igp_graph_t g, float tau, int32_t d, int32_t steps, uint64_t seed,
+                     float* d_out, igp_stream_t stream);
+
+/* As igp_embed with all options (theta, alpha, eps, subsequence, debug modes, timing). */
+IGP_API igp_status igp_embed_ex(igp_graph_t g, const igp_embed_opts* opts, float* d_out, igp_stream_t stream);
+
+/* End-to-end convenience on HOST buffers: copies h_edges (int32 [num_edges][2])
+ * to the device, builds the graph, embeds, copies Z~ back into h_out (fp32 [N][d])
+ * and synchronises `stream` before returning.  Same argument rules as above. */
+IGP_API igp_status igp_embed_host(const int32_t* h_edges, int64_t num_edges, int32_t num_nodes,
+                          const igp_embed_opts* opts, float* h_out, igp_stream_t stream);
+
+/* After an igp_embed_ex with IGP_FLAG_TIME_LAYERS has completed (caller synced):
+ * total device time of the L filter-step launches and the launch count. */
+IGP_API igp_status igp_last_layer_time_ms(igp_graph_t g, float* total_ms, int32_t* launches);
+
+/* ---------------------------------------------------------------------------
+ * Random input (test / inspection entry points)
+ * ------------------------------------------------------------------------- */
+
+/* Raw Philox4x32-10 words r[k], k < count: block b = k/4, counter
+ * (lo32 b, hi32 b, lo32 subsequence, hi32 subsequence), key (lo32 seed, hi32 seed),
+ * word k%4 (identical to cuRAND curand_init(seed, subsequence, 4b) + curand4).
+ * d_out device uint32[count]. */
+IGP_API igp_status igp_philox_bits(uint64_t seed, uint64_t subsequence, int64_t count, uint32_t* d_out,
+                           igp_stream_t stream);
+
+/* X ~ N(0,1) fp32 (unscaled): Box-Muller on word pairs (r0,r1), (r2,r3):
+ * u = (r_even + 1/2) 2^-32, v = (r_odd + 1/2) 2^-32, X_even = sqrt(-2 ln u) sin(2 pi v),
+ * X_odd = sqrt(-2 ln u) cos(2 pi v), evaluated in fp64 and rounded.
+ * count must be a multiple of 4.  d_out device float[count]. */
+IGP_API igp_status igp_philox_normal(uint64_t seed, uint64_t subsequence, int64_t count, float* d_out,
+                             igp_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics
+ * ------------------------------------------------------------------------- */
+IGP_API const char* igp_status_string(igp_status s);
+IGP_API const char* igp_last_error_message(void);
+/* Number of kernels this library has launched in this process (all threads). */
+IGP_API uint64_t igp_kernel_launch_count(void);
+/* Library version string. */
+IGP_API const char* igp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IGP_H_ */

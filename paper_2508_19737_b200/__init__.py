@@ -1,0 +1,220 @@
+"""B200-native InfraredGP feed-forward propagation (arXiv 2508.19737), Python binding.
+
+A thin ctypes layer over ``libigp.so`` (the C ABI in ``include/igp.h``): argument
+marshalling only — every step of the method runs in the library's sm_100a
+kernels.  PyTorch supplies device memory and streams.  There is no CPU
+fallback: importing this package without the built library, or calling it
+without a CUDA device, raises.
+
+    import torch, paper_2508_19737_b200 as igp
+    g = igp.build_graph(edges_cuda_int32_Ex2, num_nodes)
+    Z = igp.embed(g, tau=-1.0, d=64, steps=60, seed=0)     # torch.float32 [N, 64] on cuda
+
+Method: Alg. 1 lines 1-6: D_tau by Eq. (1),
+Theta ~ N(0, 1/d), L layers Z <- ZNorm(tanh(phi * Z)) with Eq. (3)
+ and Eq. (4), output sigmoid(Z^(L)).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libigp.so")
+
+MODES = {"full": 0, "pre_sigmoid": 1, "linear": 2}
+FLAG_TIME_LAYERS = 1
+
+IGP_OK = 0
+_STATUS = {0: "IGP_OK", 2: "IGP_ERR_INPUT", 4: "IGP_ERR_NUMERICAL", 5: "IGP_ERR_CUDA", 6: "IGP_ERR_OOM",
+           7: "IGP_ERR_UNSUPPORTED"}
+
+
+class IGPError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class EmbedOpts(ctypes.Structure):
+    _fields_ = [("tau", ctypes.c_float), ("d", ctypes.c_int32), ("steps", ctypes.c_int32),
+                ("seed", ctypes.c_uint64), ("subsequence", ctypes.c_uint64), ("theta", ctypes.c_float),
+                ("alpha", ctypes.c_float), ("eps", ctypes.c_float), ("mode", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+# name -> (restype, argtypes); mirrors include/igp.h
+_P, _i32, _i64, _u64, _f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
+SIGNATURES = {
+    "igp_build_graph": (ctypes.c_int, [_P, _i64, _i32, _P, ctypes.POINTER(_P)]),
+    "igp_graph_info": (ctypes.c_int, [_P, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "igp_graph_copy_csr": (ctypes.c_int, [_P, _P, _P, _P]),
+    "igp_destroy_graph": (ctypes.c_int, [_P]),
+    "igp_embed_opts_default": (None, [ctypes.POINTER(EmbedOpts)]),
+    "igp_embed": (ctypes.c_int, [_P, _f32, _i32, _i32, _u64, _P, _P]),
+    "igp_embed_ex": (ctypes.c_int, [_P, ctypes.POINTER(EmbedOpts), _P, _P]),
+    "igp_embed_host": (ctypes.c_int, [_P, _i64, _i32, ctypes.POINTER(EmbedOpts), _P, _P]),
+    "igp_last_layer_time_ms": (ctypes.c_int, [_P, ctypes.POINTER(_f32), ctypes.POINTER(_i32)]),
+    "igp_philox_bits": (ctypes.c_int, [_u64, _u64, _i64, _P, _P]),
+    "igp_philox_normal": (ctypes.c_int, [_u64, _u64, _i64, _P, _P]),
+    "igp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "igp_last_error_message": (ctypes.c_char_p, []),
+    "igp_kernel_launch_count": (_u64, []),
+    "igp_version": (ctypes.c_char_p, []),
+}
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2508_19737_b200._build` "
+                      "(there is no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+for _name, (_res, _args) in SIGNATURES.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def _check(status: int):
+    if status != IGP_OK:
+        raise IGPError(status, _lib.igp_last_error_message().decode())
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _require_cuda(t: torch.Tensor, dtype, name: str):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous {dtype} tensor")
+
+
+class Graph:
+    """Device CSR handle (igp_graph_t).  Owns row_ptr / col_idx on the device."""
+
+    def __init__(self, handle: ctypes.c_void_p, device: torch.device):
+        self._h = handle
+        self.device = device
+        n, nnz, m = _i32(), _i64(), _i64()
+        _check(_lib.igp_graph_info(handle, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(m)))
+        self.num_nodes, self.nnz, self.num_edges = n.value, nnz.value, m.value
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("graph was destroyed")
+        return self._h
+
+    def csr(self, stream=None):
+        """(row_ptr int32[N+1], col_idx int32[nnz]) copies on the graph's device."""
+        rp = torch.empty(self.num_nodes + 1, dtype=torch.int32, device=self.device)
+        ci = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=self.device)
+        _check(_lib.igp_graph_copy_csr(self.handle, ctypes.c_void_p(rp.data_ptr()), ctypes.c_void_p(ci.data_ptr()),
+                                       _stream_ptr(stream)))
+        return rp, ci[: self.nnz]
+
+    def last_layer_time_ms(self):
+        ms, n = _f32(), _i32()
+        _check(_lib.igp_last_layer_time_ms(self.handle, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    def close(self):
+        if self._h is not None:
+            _lib.igp_destroy_graph(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def build_graph(edges: torch.Tensor, num_nodes: int, stream=None) -> Graph:
+    """igp_build_graph: canonical CSR of the undirected simple graph.
+
+    ``edges``: CUDA int32 tensor [E, 2] (duplicates / both orientations / self loops allowed)."""
+    _require_cuda(edges, torch.int32, "edges")
+    if edges.dim() != 2 or edges.shape[1] != 2:
+        raise ValueError("edges must have shape [E, 2]")
+    h = _P()
+    with torch.cuda.device(edges.device):
+        _check(_lib.igp_build_graph(ctypes.c_void_p(edges.data_ptr()), edges.shape[0], int(num_nodes),
+                                    _stream_ptr(stream), ctypes.byref(h)))
+    return Graph(h, edges.device)
+
+
+def make_opts(tau: float, d: int, steps: int, seed: int = 0, *, subsequence: int = 0, theta: float = 0.1,
+              alpha: float = 1.0, eps: float = 1e-3, mode: str = "full", time_layers: bool = False) -> EmbedOpts:
+    o = EmbedOpts()
+    _lib.igp_embed_opts_default(ctypes.byref(o))
+    o.tau, o.d, o.steps, o.seed, o.subsequence = float(tau), int(d), int(steps), int(seed), int(subsequence)
+    o.theta, o.alpha, o.eps, o.mode = float(theta), float(alpha), float(eps), MODES[mode]
+    o.flags = FLAG_TIME_LAYERS if time_layers else 0
+    return o
+
+
+def embed(graph: Graph, tau: float, d: int, steps: int, seed: int = 0, *, out: torch.Tensor | None = None,
+          stream=None, **kw) -> torch.Tensor:
+    """igp_embed_ex: Alg. 1 l.1-6; returns Z~ as CUDA float32 [N, d] (asynchronous on ``stream``)."""
+    o = make_opts(tau, d, steps, seed, **kw)
+    if out is None:
+        out = torch.empty((graph.num_nodes, int(d)), dtype=torch.float32, device=graph.device)
+    _require_cuda(out, torch.float32, "out")
+    if tuple(out.shape) != (graph.num_nodes, int(d)):
+        raise ValueError("out must have shape [N, d]")
+    with torch.cuda.device(graph.device):
+        _check(_lib.igp_embed_ex(graph.handle, ctypes.byref(o), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+    return out
+
+
+def embed_host(edges, num_nodes: int, tau: float, d: int, steps: int, seed: int = 0, *, out=None, stream=None,
+               **kw) -> torch.Tensor:
+    """igp_embed_host: end to end from HOST edges (int32 [E, 2], pinned recommended) to a HOST
+    float32 [N, d] result; copies, build, embed and the stream sync happen inside the call."""
+    e = edges if isinstance(edges, torch.Tensor) else torch.from_numpy(edges)
+    if e.is_cuda or e.dtype != torch.int32 or not e.is_contiguous():
+        raise TypeError("edges must be a contiguous host int32 tensor/array")
+    if out is None:
+        out = torch.empty((int(num_nodes), int(d)), dtype=torch.float32, pin_memory=True)
+    if out.is_cuda or out.dtype != torch.float32 or not out.is_contiguous():
+        raise TypeError("out must be a contiguous host float32 tensor")
+    o = make_opts(tau, d, steps, seed, **kw)
+    _check(_lib.igp_embed_host(ctypes.c_void_p(e.data_ptr()), e.shape[0] if e.dim() == 2 else 0, int(num_nodes),
+                               ctypes.byref(o), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+    return out
+
+
+def philox_bits(seed: int, subsequence: int, count: int, device="cuda", stream=None) -> torch.Tensor:
+    """Raw Philox4x32-10 words as int32 (bit pattern of the uint32 draws)."""
+    out = torch.empty(max(count, 1), dtype=torch.int32, device=device)
+    _check(_lib.igp_philox_bits(seed, subsequence, count, ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+    return out[:count]
+
+
+def philox_normal(seed: int, subsequence: int, count: int, device="cuda", stream=None) -> torch.Tensor:
+    out = torch.empty(max(count, 4), dtype=torch.float32, device=device)
+    _check(_lib.igp_philox_normal(seed, subsequence, count, ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+    return out[:count]
+
+
+def kernel_launch_count() -> int:
+    return int(_lib.igp_kernel_launch_count())
+
+
+def version() -> str:
+    return _lib.igp_version().decode()

@@ -1,0 +1,463 @@
+// csr_build.cu — device CSR builder (igp_build_graph), SURVEY.md §8(a) rows a1-a3.
+//
+// Problem statement (§II): G = (V, E) undirected, unweighted,
+// A_ij = A_ji = 1 iff (v_i, v_j) in E — so the builder symmetrises, drops self
+// loops and removes duplicates.  The result is the unique canonical CSR (rows
+// ascending, columns strictly ascending), bit-exact by construction: no step's
+// output depends on thread timing once the per-row sort has run.
+//
+// Pipeline (one radix-N counting-sort pass on the row digit + a per-row sort):
+//   B1 count      validate 0 <= u,v < N (device error flag), skip u == v,
+//                 histogram both orientations per row            (atomics, grid over edges)
+//   B2 scan       exclusive scan of row counts -> bucket offsets (3-phase scan)
+//   B3 scatter    both orientations into their row bucket        (order within a row arbitrary)
+//   B4 row sort   per-row sort + in-row dedup -> unique counts:
+//                   len <= 1024:          one warp per row, bitonic sort in shared memory
+//                   1024 < len <= 16384:  one block per row, bitonic sort in shared memory
+//                   len > 16384:          one block per row, N-bit bitmap in global scratch
+//   B5 scan+compact  row_ptr = scan(unique counts); col_idx = compacted rows
+// The only host synchronisation reads nnz = row_ptr[N] and the error flag.
+#include <climits>
+#include <cstdio>
+
+#include "igp_internal.cuh"
+
+namespace igp {
+namespace {
+
+constexpr int kWarpSortCap = 1024;
+constexpr int kBlockSortCap = 16384;
+constexpr int kGiantBlocks = 16;
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ---------------------------------------------------------------- B1 / B3
+__global__ void count_kernel(const int32_t* __restrict__ edges, int64_t E, int32_t n,
+                             int32_t* __restrict__ cnt, int32_t* __restrict__ err) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += stride) {
+        const int32_t u = __ldg(edges + 2 * e), v = __ldg(edges + 2 * e + 1);
+        if ((unsigned)u >= (unsigned)n || (unsigned)v >= (unsigned)n) {
+            atomicOr(err, 1);
+            continue;
+        }
+        if (u == v) continue;
+        atomicAdd(cnt + u, 1);
+        atomicAdd(cnt + v, 1);
+    }
+}
+
+__global__ void scatter_kernel(const int32_t* __restrict__ edges, int64_t E, int32_t n,
+                               const int32_t* __restrict__ off, int32_t* __restrict__ fill,
+                               int32_t* __restrict__ tmp) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += stride) {
+        const int32_t u = __ldg(edges + 2 * e), v = __ldg(edges + 2 * e + 1);
+        if ((unsigned)u >= (unsigned)n || (unsigned)v >= (unsigned)n || u == v) continue;
+        tmp[off[u] + atomicAdd(fill + u, 1)] = v;
+        tmp[off[v] + atomicAdd(fill + v, 1)] = u;
+    }
+}
+
+// ---------------------------------------------------------------- B2 scan
+__device__ __forceinline__ int32_t block_exclusive_scan(int32_t x, int32_t* warp_tot, int32_t* total) {
+    // blockDim.x <= 1024, multiple of 32; returns exclusive prefix of x, *total = block sum
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t w = lane < nw ? warp_tot[lane] : 0;
+        int32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < nw) warp_tot[lane] = wi - w;  // exclusive warp offsets
+        if (lane == nw - 1) *total = wi;
+    }
+    __syncthreads();
+    int32_t r = warp_tot[warp] + inc - x;
+    __syncthreads();  // warp_tot reusable by the caller afterwards
+    return r;
+}
+
+__global__ void scan_reduce_kernel(const int32_t* __restrict__ in, int32_t n, int32_t* __restrict__ bsum) {
+    __shared__ int32_t red[kScanThreads / 32];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    int32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int64_t i = base + k * kScanThreads + threadIdx.x;
+        if (i < n) s += in[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t t = 0;
+        for (int w = 0; w < kScanThreads / 32; ++w) t += red[w];
+        bsum[blockIdx.x] = t;
+    }
+}
+
+// single block: exclusive scan of nb block sums in place; out_total <- sum
+__global__ void scan_blocksums_kernel(int32_t* __restrict__ bsum, int32_t nb, int32_t* __restrict__ out_total) {
+    __shared__ int32_t wt[32];
+    __shared__ int32_t tot;
+    int32_t carry = 0;
+    for (int32_t b0 = 0; b0 < nb; b0 += blockDim.x) {
+        int32_t i = b0 + threadIdx.x;
+        int32_t x = i < nb ? bsum[i] : 0;
+        int32_t ex = block_exclusive_scan(x, wt, &tot);
+        if (i < nb) bsum[i] = carry + ex;
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out_total = carry;
+}
+
+__global__ void scan_apply_kernel(const int32_t* __restrict__ in, int32_t n, const int32_t* __restrict__ bsum,
+                                  int32_t* __restrict__ out) {
+    __shared__ int32_t tile[kScanTile];
+    __shared__ int32_t wt[32];
+    __shared__ int32_t tot;
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int64_t i = base + k * kScanThreads + threadIdx.x;
+        tile[k * kScanThreads + threadIdx.x] = i < n ? in[i] : 0;
+    }
+    __syncthreads();
+    int32_t loc[kScanItems];
+    int32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        loc[k] = s;
+        s += tile[threadIdx.x * kScanItems + k];
+    }
+    int32_t ex = block_exclusive_scan(s, wt, &tot) + bsum[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) tile[threadIdx.x * kScanItems + k] = ex + loc[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int64_t i = base + k * kScanThreads + threadIdx.x;
+        if (i < n) out[i] = tile[k * kScanThreads + threadIdx.x];
+    }
+}
+
+// ---------------------------------------------------------------- B4 row sort + dedup
+__device__ __forceinline__ int next_pow2(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// warp-cooperative bitonic sort of buf[0..P) (P power of two) in shared memory
+__device__ __forceinline__ void warp_bitonic(int32_t* buf, int P, int lane) {
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    int32_t a = buf[i], b = buf[ixj];
+                    bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        buf[i] = b;
+                        buf[ixj] = a;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) sort_rows_warp_kernel(const int32_t* __restrict__ off, int32_t* __restrict__ tmp,
+                                                             int32_t* __restrict__ ucnt, int32_t n,
+                                                             int32_t* __restrict__ big_list, int32_t* __restrict__ big_count,
+                                                             int32_t* __restrict__ giant_list,
+                                                             int32_t* __restrict__ giant_count) {
+    __shared__ int32_t sbuf[8][kWarpSortCap];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t* buf = sbuf[warp];
+    const int32_t nwarps = gridDim.x * 8;
+    for (int32_t r = blockIdx.x * 8 + warp; r < n; r += nwarps) {
+        const int32_t o = off[r];
+        const int len = off[r + 1] - o;
+        if (len > kWarpSortCap) {
+            if (lane == 0) {
+                if (len <= kBlockSortCap) big_list[atomicAdd(big_count, 1)] = r;
+                else giant_list[atomicAdd(giant_count, 1)] = r;
+            }
+            continue;
+        }
+        if (len <= 1) {
+            if (lane == 0) ucnt[r] = len;
+            continue;
+        }
+        const int P = next_pow2(len);
+        for (int i = lane; i < P; i += 32) buf[i] = i < len ? tmp[o + i] : INT_MAX;
+        __syncwarp();
+        warp_bitonic(buf, P, lane);
+        int base = 0;
+        for (int i0 = 0; i0 < len; i0 += 32) {
+            const int i = i0 + lane;
+            bool keep = false;
+            int32_t v = 0;
+            if (i < len) {
+                v = buf[i];
+                keep = (i == 0) || (v != buf[i - 1]);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) tmp[o + base + __popc(m & lanemask_lt())] = v;
+            base += __popc(m);
+        }
+        if (lane == 0) ucnt[r] = base;
+        __syncwarp();
+    }
+}
+
+// one block (1024 threads) per row with kWarpSortCap < len <= kBlockSortCap
+__global__ void __launch_bounds__(1024) sort_rows_block_kernel(const int32_t* __restrict__ off, int32_t* __restrict__ tmp,
+                                                               int32_t* __restrict__ ucnt,
+                                                               const int32_t* __restrict__ big_list,
+                                                               const int32_t* __restrict__ big_count) {
+    extern __shared__ int32_t buf[];  // kBlockSortCap
+    __shared__ int32_t wt[32];
+    __shared__ int32_t tot;
+    const int32_t cnt = *big_count;
+    for (int32_t b = blockIdx.x; b < cnt; b += gridDim.x) {
+        const int32_t r = big_list[b];
+        const int32_t o = off[r];
+        const int len = off[r + 1] - o;
+        const int P = next_pow2(len);
+        for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = i < len ? tmp[o + i] : INT_MAX;
+        __syncthreads();
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                    int ixj = i ^ j;
+                    if (ixj > i) {
+                        int32_t a = buf[i], c = buf[ixj];
+                        bool up = (i & k) == 0;
+                        if ((a > c) == up) {
+                            buf[i] = c;
+                            buf[ixj] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        int32_t base = 0;
+        for (int i0 = 0; i0 < len; i0 += blockDim.x) {
+            const int i = i0 + threadIdx.x;
+            int32_t v = 0, keep = 0;
+            if (i < len) {
+                v = buf[i];
+                keep = (i == 0) || (v != buf[i - 1]);
+            }
+            int32_t pos = block_exclusive_scan(keep, wt, &tot);
+            if (keep) tmp[o + base + pos] = v;
+            base += tot;
+        }
+        if (threadIdx.x == 0) ucnt[r] = base;
+        __syncthreads();
+    }
+}
+
+// one block (1024 threads) per row with len > kBlockSortCap: N-bit bitmap (sorted + unique by construction)
+__global__ void __launch_bounds__(1024) sort_rows_giant_kernel(const int32_t* __restrict__ off, int32_t* __restrict__ tmp,
+                                                               int32_t* __restrict__ ucnt,
+                                                               const int32_t* __restrict__ giant_list,
+                                                               const int32_t* __restrict__ giant_count,
+                                                               uint32_t* __restrict__ bitmap, int32_t n) {
+    __shared__ int32_t wt[32];
+    __shared__ int32_t tot;
+    const int32_t words = (n + 31) >> 5;
+    uint32_t* bm = bitmap + (int64_t)blockIdx.x * words;
+    const int32_t cnt = *giant_count;
+    const int32_t per = (words + blockDim.x - 1) / blockDim.x;
+    for (int32_t b = blockIdx.x; b < cnt; b += gridDim.x) {
+        const int32_t r = giant_list[b];
+        const int32_t o = off[r];
+        const int32_t len = off[r + 1] - o;
+        for (int32_t w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0u;
+        __syncthreads();
+        for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
+            const int32_t v = tmp[o + i];
+            atomicOr(bm + (v >> 5), 1u << (v & 31));
+        }
+        __syncthreads();
+        const int32_t w0 = threadIdx.x * per, w1 = min(words, w0 + per);
+        int32_t c = 0;
+        for (int32_t w = w0; w < w1; ++w) c += __popc(bm[w]);
+        int32_t pos = block_exclusive_scan(c, wt, &tot);
+        for (int32_t w = w0; w < w1; ++w) {
+            uint32_t bits = bm[w];
+            while (bits) {
+                const int t = __ffs(bits) - 1;
+                tmp[o + pos++] = (w << 5) + t;
+                bits &= bits - 1;
+            }
+        }
+        if (threadIdx.x == 0) ucnt[r] = tot;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- B5 compact
+__global__ void compact_kernel(const int32_t* __restrict__ off, const int32_t* __restrict__ tmp,
+                               const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx, int32_t n) {
+    const int lane = threadIdx.x & 31;
+    const int32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nwarps) {
+        const int32_t src = off[r], dst = row_ptr[r], len = row_ptr[r + 1] - dst;
+        for (int32_t i = lane; i < len; i += 32) col_idx[dst + i] = tmp[src + i];
+    }
+}
+
+int grid_for(int64_t work, int threads, int num_sms, int per_sm) {
+    int64_t g = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)num_sms * per_sm;
+    if (g > cap) g = cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+igp_status scan_exclusive(const int32_t* in, int32_t* out, int32_t n, cudaStream_t s) {
+    const int32_t nb = (n + kScanTile - 1) / kScanTile;
+    int32_t* bsum = nullptr;
+    IGP_CUDA(alloc_async((void**)&bsum, sizeof(int32_t) * (size_t)(nb > 0 ? nb : 1), s), "scan alloc");
+    if (nb > 0) {
+        scan_reduce_kernel<<<nb, kScanThreads, 0, s>>>(in, n, bsum);
+        IGP_TRY(launch_status("scan_reduce_kernel"));
+    }
+    scan_blocksums_kernel<<<1, 1024, 0, s>>>(bsum, nb, out + n);
+    IGP_TRY(launch_status("scan_blocksums_kernel"));
+    if (nb > 0) {
+        scan_apply_kernel<<<nb, kScanThreads, 0, s>>>(in, n, bsum, out);
+        IGP_TRY(launch_status("scan_apply_kernel"));
+    }
+    free_async(bsum, s);
+    return IGP_OK;
+}
+
+igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, cudaStream_t s, CsrDevice* out) {
+    DeviceInfo di;
+    if (!device_info(&di)) return IGP_ERR_CUDA;
+    const int64_t raw = 2 * E;  // both orientations, before dedup / self-loop removal
+    const int32_t words = (n + 31) >> 5;
+    // temporaries in one stream-ordered block
+    size_t o_cnt = 0;
+    size_t o_off = o_cnt + sizeof(int32_t) * (size_t)n;
+    size_t o_ucnt = o_off + sizeof(int32_t) * ((size_t)n + 1);
+    size_t o_big = o_ucnt + sizeof(int32_t) * (size_t)n;
+    size_t o_giant = o_big + sizeof(int32_t) * (size_t)n;
+    size_t o_flags = o_giant + sizeof(int32_t) * (size_t)n;  // err, big_count, giant_count, pad
+    size_t o_bitmap = o_flags + 4 * sizeof(int32_t);
+    size_t o_tmp = o_bitmap + sizeof(uint32_t) * (size_t)words * kGiantBlocks;
+    o_tmp = (o_tmp + 255) & ~(size_t)255;
+    size_t total = o_tmp + sizeof(int32_t) * (size_t)(raw > 0 ? raw : 1);
+    char* ws = nullptr;
+    IGP_CUDA(alloc_async((void**)&ws, total, s), "build workspace alloc");
+    int32_t* cnt = (int32_t*)(ws + o_cnt);
+    int32_t* off = (int32_t*)(ws + o_off);
+    int32_t* ucnt = (int32_t*)(ws + o_ucnt);
+    int32_t* big_list = (int32_t*)(ws + o_big);
+    int32_t* giant_list = (int32_t*)(ws + o_giant);
+    int32_t* flags = (int32_t*)(ws + o_flags);
+    uint32_t* bitmap = (uint32_t*)(ws + o_bitmap);
+    int32_t* tmp = (int32_t*)(ws + o_tmp);
+
+    int32_t* row_ptr = nullptr;
+    igp_status st = cuda_status(alloc_async((void**)&row_ptr, sizeof(int32_t) * ((size_t)n + 1), s), "row_ptr alloc");
+    if (st != IGP_OK) {
+        free_async(ws, s);
+        return st;
+    }
+    auto fail = [&](igp_status e) {
+        free_async(ws, s);
+        free_async(row_ptr, s);
+        return e;
+    };
+    if ((st = cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset")) != IGP_OK) return fail(st);
+    if ((st = cuda_status(cudaMemsetAsync(flags, 0, 4 * sizeof(int32_t), s), "memset")) != IGP_OK) return fail(st);
+    const int eg = grid_for(E, 256, di.num_sms, 16);
+    if (E > 0) {
+        count_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, cnt, flags);
+        if ((st = launch_status("count_kernel")) != IGP_OK) return fail(st);
+    }
+    if ((st = scan_exclusive(cnt, off, n, s)) != IGP_OK) return fail(st);
+    if (E > 0) {
+        if ((st = cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset")) != IGP_OK)
+            return fail(st);
+        scatter_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, off, cnt, tmp);
+        if ((st = launch_status("scatter_kernel")) != IGP_OK) return fail(st);
+    }
+    const int rg = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
+    sort_rows_warp_kernel<<<rg, 256, 0, s>>>(off, tmp, ucnt, n, big_list, flags + 1, giant_list, flags + 2);
+    if ((st = launch_status("sort_rows_warp_kernel")) != IGP_OK) return fail(st);
+    if (E > kWarpSortCap) {  // a raw row longer than kWarpSortCap needs > kWarpSortCap edges
+        cudaFuncSetAttribute(sort_rows_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kBlockSortCap * (int)sizeof(int32_t));
+        sort_rows_block_kernel<<<di.num_sms, 1024, kBlockSortCap * sizeof(int32_t), s>>>(off, tmp, ucnt, big_list,
+                                                                                         flags + 1);
+        if ((st = launch_status("sort_rows_block_kernel")) != IGP_OK) return fail(st);
+        if (E > kBlockSortCap) {
+            sort_rows_giant_kernel<<<kGiantBlocks, 1024, 0, s>>>(off, tmp, ucnt, giant_list, flags + 2, bitmap, n);
+            if ((st = launch_status("sort_rows_giant_kernel")) != IGP_OK) return fail(st);
+        }
+    }
+    if ((st = scan_exclusive(ucnt, row_ptr, n, s)) != IGP_OK) return fail(st);
+    // the build's single host synchronisation: nnz and the error flag
+    int32_t host_vals[2] = {0, 0};
+    if ((st = cuda_status(cudaMemcpyAsync(&host_vals[0], row_ptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+                          "nnz readback")) != IGP_OK)
+        return fail(st);
+    if ((st = cuda_status(cudaMemcpyAsync(&host_vals[1], flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+                          "flag readback")) != IGP_OK)
+        return fail(st);
+    if ((st = cuda_status(cudaStreamSynchronize(s), "build sync")) != IGP_OK) return fail(st);
+    if (host_vals[1] != 0) {
+        set_error("igp_build_graph: edge index outside [0, num_nodes)");
+        return fail(IGP_ERR_INPUT);
+    }
+    const int64_t nnz = host_vals[0];
+    int32_t* col_idx = nullptr;
+    if ((st = cuda_status(alloc_async((void**)&col_idx, sizeof(int32_t) * (size_t)(nnz > 0 ? nnz : 1), s),
+                          "col_idx alloc")) != IGP_OK)
+        return fail(st);
+    if (nnz > 0) {
+        compact_kernel<<<rg, 256, 0, s>>>(off, tmp, row_ptr, col_idx, n);
+        if ((st = launch_status("compact_kernel")) != IGP_OK) {
+            free_async(col_idx, s);
+            return fail(st);
+        }
+    }
+    free_async(ws, s);
+    out->row_ptr = row_ptr;
+    out->col_idx = col_idx;
+    out->n = n;
+    out->nnz = nnz;
+    return IGP_OK;
+}
+
+}  // namespace igp

@@ -1,0 +1,291 @@
+// igp_api.cu — the C ABI declared in include/igp.h: argument validation, handle
+// ownership, status codes, stream-ordered workspace, and the host-buffer
+// end-to-end entry point.  All compute is in csr_build.cu / philox.cu / embed.cu.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "igp_internal.cuh"
+
+namespace igp {
+
+std::atomic<uint64_t> g_launches{0};
+
+std::string& error_slot() {
+    thread_local std::string msg;
+    return msg;
+}
+
+void set_error(const std::string& msg) { error_slot() = msg; }
+
+bool device_info(DeviceInfo* out) {
+    static std::mutex mu;
+    static DeviceInfo cache[64];
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess || dev < 0) {
+        set_error(std::string("no usable CUDA device: ") + cudaGetErrorString(e));
+        return false;
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    DeviceInfo& di = cache[dev & 63];
+    if (di.device != dev) {
+        DeviceInfo n;
+        n.device = dev;
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+            set_error("cudaDeviceGetAttribute(MultiProcessorCount) failed");
+            return false;
+        }
+        n.num_sms = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        n.max_smem_optin = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+        n.l2_bytes = (size_t)v;
+        // keep freed stream-ordered memory in the default pool (repeated embeds reuse it)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        di = n;
+    }
+    *out = di;
+    return true;
+}
+
+cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s) {
+    return cudaMallocAsync(p, bytes > 0 ? bytes : 16, s);
+}
+
+void free_async(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+}  // namespace igp
+
+using namespace igp;
+
+static igp_status check_opts(const igp_embed_opts* o) {
+    if (!o) {
+        set_error("opts is NULL");
+        return IGP_ERR_INPUT;
+    }
+    if (!std::isfinite(o->tau) || !std::isfinite(o->theta) || !std::isfinite(o->alpha)) {
+        set_error("tau, theta and alpha must be finite");
+        return IGP_ERR_INPUT;
+    }
+    if (!(o->eps > 0.0f) || !std::isfinite(o->eps)) {
+        set_error("eps must be positive (Eq. (1))");
+        return IGP_ERR_INPUT;
+    }
+    if (o->steps < 0) {
+        set_error("steps must be >= 0");
+        return IGP_ERR_INPUT;
+    }
+    if (o->mode != IGP_MODE_FULL && o->mode != IGP_MODE_PRE_SIGMOID && o->mode != IGP_MODE_LINEAR) {
+        set_error("unknown mode");
+        return IGP_ERR_INPUT;
+    }
+    if (o->d != 16 && o->d != 32 && o->d != 64 && o->d != 128) {
+        set_error("d must be one of 16, 32, 64, 128");
+        return IGP_ERR_UNSUPPORTED;
+    }
+    return IGP_OK;
+}
+
+extern "C" {
+
+const char* igp_version(void) { return "igp 0.1 (sm_100a)"; }
+
+const char* igp_status_string(igp_status s) {
+    switch (s) {
+        case IGP_OK: return "IGP_OK";
+        case IGP_ERR_INPUT: return "IGP_ERR_INPUT";
+        case IGP_ERR_NUMERICAL: return "IGP_ERR_NUMERICAL";
+        case IGP_ERR_CUDA: return "IGP_ERR_CUDA";
+        case IGP_ERR_OOM: return "IGP_ERR_OOM";
+        case IGP_ERR_UNSUPPORTED: return "IGP_ERR_UNSUPPORTED";
+        default: return "IGP_ERR_UNKNOWN";
+    }
+}
+
+const char* igp_last_error_message(void) { return error_slot().c_str(); }
+
+uint64_t igp_kernel_launch_count(void) { return g_launches.load(); }
+
+igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes, igp_stream_t stream,
+                           igp_graph_t* out) {
+    set_error("");
+    if (!out) {
+        set_error("out handle pointer is NULL");
+        return IGP_ERR_INPUT;
+    }
+    *out = nullptr;
+    if (num_nodes <= 0) {
+        set_error("num_nodes must be >= 1");
+        return IGP_ERR_INPUT;
+    }
+    if (num_edges < 0 || (num_edges > 0 && !d_edges)) {
+        set_error("num_edges must be >= 0 and d_edges non-NULL when num_edges > 0");
+        return IGP_ERR_INPUT;
+    }
+    if (2 * num_edges > (int64_t)INT32_MAX) {
+        set_error("2*num_edges exceeds the int32 CSR index range");
+        return IGP_ERR_UNSUPPORTED;
+    }
+    igp_graph_s* g = new (std::nothrow) igp_graph_s();
+    if (!g) return IGP_ERR_OOM;
+    igp_status st = build_csr(d_edges, num_edges, num_nodes, (cudaStream_t)stream, &g->csr);
+    if (st != IGP_OK) {
+        delete g;
+        return st;
+    }
+    g->m = g->csr.nnz / 2;
+    *out = g;
+    return IGP_OK;
+}
+
+igp_status igp_graph_info(igp_graph_t g, int32_t* num_nodes, int64_t* nnz, int64_t* m) {
+    if (!g) {
+        set_error("graph is NULL");
+        return IGP_ERR_INPUT;
+    }
+    if (num_nodes) *num_nodes = g->csr.n;
+    if (nnz) *nnz = g->csr.nnz;
+    if (m) *m = g->m;
+    return IGP_OK;
+}
+
+igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t* d_col_idx, igp_stream_t stream) {
+    if (!g || !d_row_ptr || (g->csr.nnz > 0 && !d_col_idx)) {
+        set_error("graph or output pointer is NULL");
+        return IGP_ERR_INPUT;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    IGP_CUDA(cudaMemcpyAsync(d_row_ptr, g->csr.row_ptr, sizeof(int32_t) * ((size_t)g->csr.n + 1),
+                             cudaMemcpyDeviceToDevice, s),
+             "copy row_ptr");
+    if (g->csr.nnz > 0)
+        IGP_CUDA(cudaMemcpyAsync(d_col_idx, g->csr.col_idx, sizeof(int32_t) * (size_t)g->csr.nnz,
+                                 cudaMemcpyDeviceToDevice, s),
+                 "copy col_idx");
+    return IGP_OK;
+}
+
+static void release_graph(igp_graph_t g) {
+    // the CSR lives in the stream-ordered pool; callers have drained all work on it
+    free_async(g->csr.row_ptr, (cudaStream_t)0);
+    free_async(g->csr.col_idx, (cudaStream_t)0);
+    if (g->timing.ev0) cudaEventDestroy(g->timing.ev0);
+    if (g->timing.ev1) cudaEventDestroy(g->timing.ev1);
+    delete g;
+}
+
+igp_status igp_destroy_graph(igp_graph_t g) {
+    if (!g) return IGP_OK;
+    cudaDeviceSynchronize();  // no stream may still read the CSR
+    release_graph(g);
+    return IGP_OK;
+}
+
+void igp_embed_opts_default(igp_embed_opts* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->theta = 0.1f;
+    o->alpha = 1.0f;
+    o->eps = 1e-3f;
+    o->mode = IGP_MODE_FULL;
+}
+
+igp_status igp_embed_ex(igp_graph_t g, const igp_embed_opts* opts, float* d_out, igp_stream_t stream) {
+    set_error("");
+    if (!g || !d_out) {
+        set_error("graph or d_out is NULL");
+        return IGP_ERR_INPUT;
+    }
+    IGP_TRY(check_opts(opts));
+    return run_embed(g->csr, *opts, d_out, (cudaStream_t)stream, &g->timing);
+}
+
+igp_status igp_embed(igp_graph_t g, float tau, int32_t d, int32_t steps, uint64_t seed, float* d_out,
+                     igp_stream_t stream) {
+    igp_embed_opts o;
+    igp_embed_opts_default(&o);
+    o.tau = tau;
+    o.d = d;
+    o.steps = steps;
+    o.seed = seed;
+    return igp_embed_ex(g, &o, d_out, stream);
+}
+
+igp_status igp_last_layer_time_ms(igp_graph_t g, float* total_ms, int32_t* launches) {
+    if (!g || !g->timing.valid) {
+        set_error("no timed embed recorded on this graph");
+        return IGP_ERR_INPUT;
+    }
+    float ms = 0.0f;
+    IGP_CUDA(cudaEventElapsedTime(&ms, g->timing.ev0, g->timing.ev1), "cudaEventElapsedTime");
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = g->timing.launches;
+    return IGP_OK;
+}
+
+igp_status igp_embed_host(const int32_t* h_edges, int64_t num_edges, int32_t num_nodes, const igp_embed_opts* opts,
+                          float* h_out, igp_stream_t stream) {
+    set_error("");
+    if (!h_out || (num_edges > 0 && !h_edges) || num_edges < 0 || num_nodes <= 0) {
+        set_error("invalid host buffers or sizes");
+        return IGP_ERR_INPUT;
+    }
+    IGP_TRY(check_opts(opts));
+    cudaStream_t s = (cudaStream_t)stream;
+    int32_t* d_edges = nullptr;
+    float* d_out = nullptr;
+    const size_t eb = sizeof(int32_t) * 2 * (size_t)num_edges;
+    const size_t ob = sizeof(float) * (size_t)num_nodes * (size_t)opts->d;
+    IGP_CUDA(alloc_async((void**)&d_edges, eb, s), "edges alloc");
+    if (eb) IGP_CUDA(cudaMemcpyAsync(d_edges, h_edges, eb, cudaMemcpyHostToDevice, s), "edges H2D");
+    igp_graph_t g = nullptr;
+    igp_status st = igp_build_graph(d_edges, num_edges, num_nodes, stream, &g);
+    free_async(d_edges, s);
+    if (st != IGP_OK) return st;
+    st = cuda_status(alloc_async((void**)&d_out, ob, s), "out alloc");
+    if (st == IGP_OK) st = igp_embed_ex(g, opts, d_out, stream);
+    if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(h_out, d_out, ob, cudaMemcpyDeviceToHost, s), "out D2H");
+    free_async(d_out, s);
+    igp_status st2 = cuda_status(cudaStreamSynchronize(s), "stream sync");
+    // release the graph without a device-wide sync (its only user, `s`, is drained)
+    free_async(g->csr.row_ptr, s);
+    free_async(g->csr.col_idx, s);
+    if (g->timing.ev0) cudaEventDestroy(g->timing.ev0);
+    if (g->timing.ev1) cudaEventDestroy(g->timing.ev1);
+    delete g;
+    return st != IGP_OK ? st : st2;
+}
+
+igp_status igp_philox_bits(uint64_t seed, uint64_t sub, int64_t count, uint32_t* d_out, igp_stream_t stream) {
+    set_error("");
+    if (count < 0 || (count > 0 && !d_out)) {
+        set_error("invalid count or NULL output");
+        return IGP_ERR_INPUT;
+    }
+    DeviceInfo di;
+    if (!device_info(&di)) return IGP_ERR_CUDA;
+    return launch_philox_bits(seed, sub, count, d_out, (cudaStream_t)stream);
+}
+
+igp_status igp_philox_normal(uint64_t seed, uint64_t sub, int64_t count, float* d_out, igp_stream_t stream) {
+    set_error("");
+    if (count < 0 || count % 4 != 0 || (count > 0 && !d_out)) {
+        set_error("count must be a non-negative multiple of 4 and d_out non-NULL");
+        return IGP_ERR_INPUT;
+    }
+    DeviceInfo di;
+    if (!device_info(&di)) return IGP_ERR_CUDA;
+    return launch_philox_normal(seed, sub, count, d_out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

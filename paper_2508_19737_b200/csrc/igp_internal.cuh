@@ -1,0 +1,94 @@
+// igp_internal.cuh — host-side plumbing shared by the library's translation units.
+// (Product code only; shares nothing with oracle/.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/igp.h"
+
+namespace igp {
+
+// error detail string, thread-local
+void set_error(const std::string& msg);
+std::string& error_slot();
+
+// kernel launch accounting (igp_kernel_launch_count)
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+struct DeviceInfo {
+    int device = -1;
+    int num_sms = 0;
+    int max_smem_optin = 0;
+    size_t l2_bytes = 0;
+};
+// cached per current device; returns false (and sets the error) if no device
+bool device_info(DeviceInfo* out);
+
+// stream-ordered allocation helpers (default pool, release threshold raised once)
+cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s);
+void free_async(void* p, cudaStream_t s);
+
+inline igp_status cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return IGP_OK;
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? IGP_ERR_OOM : IGP_ERR_CUDA;
+}
+
+// check the launch that was just enqueued
+inline igp_status launch_status(const char* what) {
+    count_launch();
+    return cuda_status(cudaGetLastError(), what);
+}
+
+#define IGP_TRY(expr)                                   \
+    do {                                                \
+        igp_status _st = (expr);                        \
+        if (_st != IGP_OK) return _st;                  \
+    } while (0)
+
+#define IGP_CUDA(expr, what) IGP_TRY(::igp::cuda_status((expr), (what)))
+
+// ---------------------------------------------------------------------------
+// csr_build.cu
+// ---------------------------------------------------------------------------
+struct CsrDevice {
+    int32_t* row_ptr = nullptr;  // [N+1]
+    int32_t* col_idx = nullptr;  // [nnz]
+    int32_t n = 0;
+    int64_t nnz = 0;
+};
+igp_status build_csr(const int32_t* d_edges, int64_t num_edges, int32_t n, cudaStream_t s,
+                     CsrDevice* out);
+
+// exclusive scan of n int32 counts: out[0..n], out[n] = total (int32 range checked by caller)
+igp_status scan_exclusive(const int32_t* in, int32_t* out, int32_t n, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// philox.cu
+// ---------------------------------------------------------------------------
+igp_status launch_philox_bits(uint64_t seed, uint64_t sub, int64_t count, uint32_t* out, cudaStream_t s);
+igp_status launch_philox_normal(uint64_t seed, uint64_t sub, int64_t count, float* out, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// embed.cu
+// ---------------------------------------------------------------------------
+struct EmbedTiming {
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int32_t launches = 0;
+    bool valid = false;
+};
+igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s,
+                     EmbedTiming* timing);
+
+}  // namespace igp
+
+struct igp_graph_s {
+    igp::CsrDevice csr;
+    int64_t m = 0;
+    igp::EmbedTiming timing;
+};

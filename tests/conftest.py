@@ -57,3 +57,19 @@ def row_rel_err(a, b):
     nrm = np.linalg.norm(b, axis=1, keepdims=True)
     nrm = np.where(nrm > 0, nrm, 1.0)
     return float(np.max(np.abs(a - b) / nrm)) if a.size else 0.0
+
+
+_RECORDS = {}
+
+
+def record(name, value):
+    """Collect parity numbers; written to $IGP_PARITY_LOG at session end (if set)."""
+    _RECORDS[name] = value
+
+
+def pytest_sessionfinish(session, exitstatus):
+    path = os.environ.get("IGP_PARITY_LOG")
+    if path and _RECORDS:
+        os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+        with open(path, "w") as f:
+            json.dump(_RECORDS, f, indent=1, sort_keys=True)

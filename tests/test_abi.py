@@ -1,0 +1,66 @@
+"""The C-ABI library loads and exports every symbol include/igp.h declares (no GPU needed).
+
+Only calls that return before touching the device are made here (status strings,
+version, host-side argument validation); compute calls are in the -m gpu tests.
+"""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "igp.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"IGP_API\s+[\w\s\*]+?\b(igp_\w+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def igp():
+    from paper_2508_19737_b200 import _build
+    _build.build()
+    import paper_2508_19737_b200 as m
+    return m
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ["igp_build_graph", "igp_embed", "igp_embed_ex", "igp_embed_host", "igp_destroy_graph",
+              "igp_graph_info", "igp_graph_copy_csr", "igp_philox_bits", "igp_philox_normal"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(igp):
+    lib = ctypes.CDLL(igp.LIB_PATH)
+    for s in declared_symbols():
+        assert hasattr(lib, s), f"{s} declared in igp.h but not exported"
+    # the binding wraps exactly the declared surface
+    assert set(igp.SIGNATURES) == set(declared_symbols())
+
+
+def test_only_the_abi_is_exported(igp):
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", igp.LIB_PATH], capture_output=True, text=True).stdout
+    names = [ln.split()[-1] for ln in out.splitlines() if ln.strip()]
+    text_syms = [n for n in names if not n.startswith("_") and n not in ("_init", "_fini")]
+    assert all(n.startswith("igp_") for n in text_syms), text_syms
+
+
+def test_host_side_calls_without_device(igp):
+    lib = igp.lib()
+    assert lib.igp_status_string(0) == b"IGP_OK"
+    assert lib.igp_status_string(7) == b"IGP_ERR_UNSUPPORTED"
+    assert b"sm_100a" in lib.igp_version()
+    assert lib.igp_kernel_launch_count() == 0
+    # host-validated input errors return before any device work
+    h = ctypes.c_void_p()
+    assert lib.igp_build_graph(None, 0, 0, None, ctypes.byref(h)) == 2
+    assert lib.igp_build_graph(None, -1, 5, None, ctypes.byref(h)) == 2
+    assert lib.igp_build_graph(ctypes.c_void_p(0x1000), 2**31, 5, None, ctypes.byref(h)) == 7  # not dereferenced
+    o = igp.make_opts(-1.0, 48, 10)
+    assert lib.igp_embed_ex(None, ctypes.byref(o), None, None) == 2
+    assert lib.igp_destroy_graph(None) == 0
+    assert lib.igp_kernel_launch_count() == 0

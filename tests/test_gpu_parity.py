@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bars (north star):
+  - CSR: bit-exact (row_ptr, col_idx) on adversarial lists and the DC-SBM configs;
+  - Philox raw words: bit-exact; normals: within 1 fp32 ulp of the fp64 value;
+  - embeddings: max_i max_c |gpu - oracle| / ||oracle_i||_2 <= 1e-4 (fp32 vs fp64).
+All inputs are seeded and synthetic (synth/dcsbm.py).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import record, row_rel_err
+from synth.dcsbm import CONFIGS, generate
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # north-star row-relative tolerance
+NTHREADS = max(1, len(os.sched_getaffinity(0)))
+
+
+@pytest.fixture(scope="module")
+def igp():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test requires CUDA (no CPU fallback)")
+    import paper_2508_19737_b200 as m
+    return m
+
+
+def gpu_graph(igp, edges, n):
+    e = torch.from_numpy(np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))).cuda()
+    return igp.build_graph(e, n)
+
+
+def check_csr(igp, edges, n):
+    g = gpu_graph(igp, edges, n)
+    rp, ci = g.csr()
+    torch.cuda.synchronize()
+    rp_o, ci_o, m_o = oracle.build_csr(edges, n)
+    assert g.num_edges == m_o and g.nnz == 2 * m_o
+    assert np.array_equal(rp.cpu().numpy(), rp_o), "row_ptr differs"
+    assert np.array_equal(ci.cpu().numpy(), ci_o), "col_idx differs"
+    return g, rp_o, ci_o
+
+
+# ------------------------------------------------------------------ CSR
+def adversarial_edge_lists():
+    rng = np.random.default_rng(0)
+    cases = {
+        "empty": (np.zeros((0, 2), np.int32), 3),
+        "single_node": (np.zeros((0, 2), np.int32), 1),
+        "self_loops_only": (np.array([[0, 0], [1, 1], [2, 2]], np.int32), 3),
+        "dups_both_orient": (np.array([[0, 1], [1, 0], [0, 1], [1, 1], [2, 0], [0, 2]], np.int32), 4),
+        "random_small": (rng.integers(0, 50, (400, 2)).astype(np.int32), 50),
+        "ragged_tail": (rng.integers(0, 2049, (30000, 2)).astype(np.int32), 2049),
+    }
+    # stars: hub rows that take the block-sort (1024 < len <= 16384) and bitmap (> 16384) paths
+    for name, leaves in [("star_1500", 1500), ("star_20000", 20000)]:
+        n = leaves + 1
+        e = np.stack([np.zeros(leaves, np.int32), np.arange(1, n, dtype=np.int32)], 1)
+        e = np.concatenate([e, e[::3, ::-1], rng.integers(0, n, (2000, 2)).astype(np.int32)])
+        cases[name] = (e[rng.permutation(e.shape[0])], n)
+    # a dense core: many rows with raw length > 1024 (duplicates included)
+    n = 3000
+    core = rng.integers(0, 64, (80000, 2)).astype(np.int32)
+    cases["dense_core"] = (np.concatenate([core, rng.integers(0, n, (5000, 2)).astype(np.int32)]), n)
+    return cases
+
+
+@pytest.mark.parametrize("name", list(adversarial_edge_lists()))
+def test_csr_bit_exact_adversarial(igp, name):
+    edges, n = adversarial_edge_lists()[name]
+    check_csr(igp, edges, n)
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "medium", "streaming"])
+def test_csr_bit_exact_configs(igp, cfg):
+    c = CONFIGS[cfg]
+    edges, _ = generate(c)
+    check_csr(igp, edges, c.num_nodes)
+
+
+def test_csr_out_of_range_is_input_error(igp):
+    with pytest.raises(igp.IGPError) as ei:
+        gpu_graph(igp, np.array([[0, 1], [2, 5]], np.int32), 5)
+    assert ei.value.status == 2
+    with pytest.raises(igp.IGPError):
+        gpu_graph(igp, np.array([[0, -1]], np.int32), 5)
+
+
+# ------------------------------------------------------------------ Philox
+@pytest.mark.parametrize("seed,sub", [(0, 0), (1234, 5), (2**40 + 17, 3)])
+def test_philox_bits_bit_exact(igp, seed, sub):
+    count = 4 * 100_003
+    got = igp.philox_bits(seed, sub, count).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, oracle.philox_bits(seed, sub, count))
+
+
+def test_philox_normal_within_one_ulp(igp):
+    count = 1 << 20
+    got = igp.philox_normal(7, 2, count).cpu().numpy()
+    ref = oracle.normal(7, 2, count)
+    ulp = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+    assert np.all(np.abs(got.astype(np.float64) - ref) <= ulp)
+
+
+# ------------------------------------------------------------------ embeddings
+def run_parity(igp, edges, n, d, L, tau, seed=0, mode="full", sub=0, **kw):
+    g = gpu_graph(igp, edges, n)
+    z = igp.embed(g, tau, d, L, seed, mode=mode, subsequence=sub, **kw).cpu().numpy()
+    rp, ci, _ = oracle.build_csr(edges, n)
+    omode = {"full": oracle.MODE_FULL, "pre_sigmoid": oracle.MODE_PRE_SIGMOID, "linear": oracle.MODE_LINEAR}[mode]
+    ref = oracle.embed(rp, ci, n, d, L, tau, seed=seed, sub=sub, mode=omode, nthreads=NTHREADS, **kw)
+    return z, ref
+
+
+def test_embed_tiny_config(igp):
+    c = CONFIGS["tiny"]
+    edges, _ = generate(c)
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, c.steps, c.tau)
+    err = row_rel_err(z, ref)
+    record("tiny", err)
+    assert err <= TOL
+    assert z.min() > 0 and z.max() < 1
+
+
+@pytest.mark.parametrize("tau", [-1.5, -1.0, 0.0])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_embed_medium_config(igp, tau, seed):
+    c = CONFIGS["medium"]
+    edges, _ = generate(c, seed=seed)
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, c.steps, tau, seed=seed)
+    err = row_rel_err(z, ref)
+    record(f"medium_tau{tau}_seed{seed}", err)
+    assert err <= TOL
+
+
+@pytest.mark.parametrize("d", [16, 32, 64, 128])
+@pytest.mark.parametrize("n", [1, 7, 777, 4099])
+def test_embed_dims_and_ragged_sizes(igp, d, n):
+    rng = np.random.default_rng(n + d)
+    edges = rng.integers(0, n, (6 * n, 2)).astype(np.int32)
+    for mode in ["full", "pre_sigmoid"]:
+        z, ref = run_parity(igp, edges, n, d, 6, -1.0, seed=3, mode=mode)
+        err = row_rel_err(z, ref)
+        record(f"ragged_n{n}_d{d}_{mode}", err)
+        assert err <= TOL, (mode, d, n)
+
+
+def test_embed_linear_mode(igp):
+    rng = np.random.default_rng(9)
+    n = 500
+    edges = rng.integers(0, n, (3000, 2)).astype(np.int32)
+    z, ref = run_parity(igp, edges, n, 32, 3, -0.5, seed=1, mode="linear")
+    assert row_rel_err(z, ref) <= TOL
+
+
+@pytest.mark.parametrize("tau", [-1.0, 0.0, 2.0])
+def test_embed_isolated_nodes_and_empty_graph(igp, tau):
+    rng = np.random.default_rng(4)
+    n = 1000
+    edges = rng.integers(0, 600, (2000, 2)).astype(np.int32)  # nodes 600..999 isolated
+    z, ref = run_parity(igp, edges, n, 64, 8, tau, seed=2)
+    assert row_rel_err(z, ref) <= TOL
+    z, ref = run_parity(igp, np.zeros((0, 2), np.int32), 300, 16, 5, tau, seed=2)
+    assert row_rel_err(z, ref) <= TOL
+
+
+def test_embed_single_node_is_one_half(igp):
+    z, _ = run_parity(igp, np.zeros((0, 2), np.int32), 1, 64, 4, -1.0)
+    assert np.all(z == 0.5)
+
+
+def test_embed_star_hub_and_theta_alpha_subsequence(igp):
+    n = 5000
+    e = np.stack([np.zeros(n - 1, np.int32), np.arange(1, n, dtype=np.int32)], 1)
+    z, ref = run_parity(igp, e, n, 64, 10, -1.0, seed=5, sub=3, theta=0.3, alpha=0.7, eps=1e-2)
+    err = row_rel_err(z, ref)
+    record("star_hub_theta0.3_alpha0.7", err)
+    assert err <= TOL
+
+
+def test_embed_deterministic_and_stream_safe(igp):
+    c = CONFIGS["tiny"]
+    edges, _ = generate(c)
+    g = gpu_graph(igp, edges, c.num_nodes)
+    a = igp.embed(g, -1.0, 64, 10, 0).clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        b = igp.embed(g, -1.0, 64, 10, 0, stream=s1)
+    with torch.cuda.stream(s2):
+        c2 = igp.embed(g, -1.0, 64, 10, 0, stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(a, c2)
+
+
+def test_embed_host_matches_device_path(igp):
+    c = CONFIGS["tiny"]
+    edges, _ = generate(c)
+    g = gpu_graph(igp, edges, c.num_nodes)
+    dev = igp.embed(g, -1.0, 64, 10, 0).cpu()
+    host = igp.embed_host(torch.from_numpy(edges).pin_memory(), c.num_nodes, -1.0, 64, 10, 0)
+    assert torch.equal(dev, host)
+
+
+def test_embed_argument_errors(igp):
+    g = gpu_graph(igp, np.array([[0, 1]], np.int32), 2)
+    with pytest.raises(igp.IGPError) as ei:
+        igp.embed(g, -1.0, 48, 3, 0)
+    assert ei.value.status == 7
+    with pytest.raises(igp.IGPError):
+        igp.embed(g, float("nan"), 64, 3, 0)
+    with pytest.raises(igp.IGPError):
+        igp.embed(g, -1.0, 64, -1, 0)
+
+
+# ------------------------------------------------------------------ full size (bench launch configuration)
+@pytest.fixture(scope="module")
+def headline(igp):
+    c = CONFIGS["headline"]
+    edges, _ = generate(c)
+    return c, edges
+
+
+def test_headline_csr_bit_exact(igp, headline):
+    c, edges = headline
+    check_csr(igp, edges, c.num_nodes)
+
+
+def test_headline_parity_reduced_steps(igp, headline):
+    """Full N / nnz / d, the same kernels and grid as bench.py; L reduced so the
+    fp64 oracle finishes in the test budget (IGP_FULL_PARITY=1 runs L = 60)."""
+    c, edges = headline
+    L = c.steps if os.environ.get("IGP_FULL_PARITY") == "1" else 3
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, L, c.tau)
+    err = row_rel_err(z, ref)
+    record(f"headline_L{L}", err)
+    assert err <= TOL
+
+
+def test_headline_full_steps_properties(igp, headline):
+    """L = 60 at full size: properties that hold at any size (range, determinism,
+    standardised pre-sigmoid columns)."""
+    c, edges = headline
+    g = gpu_graph(igp, edges, c.num_nodes)
+    z1 = igp.embed(g, c.tau, c.d, c.steps, 0)
+    z2 = igp.embed(g, c.tau, c.d, c.steps, 0)
+    assert torch.equal(z1, z2)
+    assert float(z1.min()) > 0 and float(z1.max()) < 1
+    pre = igp.embed(g, c.tau, c.d, c.steps, 0, mode="pre_sigmoid").double()
+    assert torch.allclose(pre.mean(0), torch.zeros(c.d, dtype=torch.float64, device=pre.device), atol=1e-4)
+    assert torch.allclose(pre.std(0, unbiased=False), torch.ones(c.d, dtype=torch.float64, device=pre.device),
+                          atol=1e-4)

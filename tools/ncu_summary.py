@@ -1,0 +1,64 @@
+"""Summarise ncu outputs for profiles/ (tooling, not product).
+
+  python tools/ncu_summary.py launches gpurun_out/launches.csv      # per-kernel share of a launch list
+  python tools/ncu_summary.py full gpurun_out/prof_layer.ncu-rep    # key counters of a --set full capture
+"""
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "launch__occupancy_limit_registers", "smsp__inst_executed.sum",
+        "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum",
+        "lts__t_sectors_srcunit_tex_op_read_lookup_miss.sum", "sm__cycles_elapsed.avg.per_second",
+        "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
+        "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct",
+        "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h, data = rows[hi], rows[hi + 1:]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3}
+    for r in data:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").replace("igp::(anonymous namespace)::", "")
+        agg[name][0] += 1
+        agg[name][1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+    tot = sum(a[1] for a in agg.values())
+    out = []
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.append(f"{k:44s} n={n:4d} total={t / 1e3:9.2f} ms  avg={t / n:9.1f} us  share={t / tot * 100:5.1f}%")
+    return "\n".join(out)
+
+
+def full(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+        d = {"kernel": name[:80]}
+        for k in KEYS:
+            if k in h:
+                i = h.index(k)
+                d[k] = f"{r[i]} {units[i]}".strip()
+        res.append(d)
+    return json.dumps(res, indent=1)
+
+
+if __name__ == "__main__":
+    print(launches(sys.argv[2]) if sys.argv[1] == "launches" else full(sys.argv[2]))
