@@ -333,6 +333,54 @@ __global__ void compact_kernel(const int32_t* __restrict__ off, const int32_t* _
     }
 }
 
+// ---------------------------------------------------------------- row schedule (degree-descending order)
+// Bucket key = kDegBuckets-1-min(deg, kDegBuckets-1); a block-aggregated counting sort.
+// The order within a bucket is arbitrary: each row's result is independent of where it
+// is scheduled, and the layer statistics are exact sums (embed.cu), so outputs do not
+// depend on this order.
+constexpr int kDegBuckets = 1024;
+constexpr int kSchedTile = 2048;
+
+__device__ __forceinline__ int deg_key(const int32_t* rp, int32_t i) {
+    const int32_t deg = rp[i + 1] - rp[i];
+    return kDegBuckets - 1 - (deg < kDegBuckets - 1 ? deg : kDegBuckets - 1);
+}
+
+__global__ void __launch_bounds__(256) degree_hist_kernel(const int32_t* __restrict__ rp, int32_t n,
+                                                          int32_t* __restrict__ hist) {
+    __shared__ int32_t sh[kDegBuckets];
+    for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        atomicAdd(&sh[deg_key(rp, (int32_t)i)], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x)
+        if (sh[b]) atomicAdd(hist + b, sh[b]);
+}
+
+__global__ void __launch_bounds__(256) degree_scatter_kernel(const int32_t* __restrict__ rp, int32_t n,
+                                                             int32_t* __restrict__ fill, int32_t* __restrict__ order) {
+    __shared__ int32_t cnt[kDegBuckets];
+    __shared__ int32_t base[kDegBuckets];
+    for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    const int32_t i0 = blockIdx.x * kSchedTile;
+    int key[kSchedTile / 256], rank[kSchedTile / 256];
+#pragma unroll
+    for (int k = 0; k < kSchedTile / 256; ++k) {
+        const int32_t i = i0 + k * 256 + threadIdx.x;
+        key[k] = i < n ? deg_key(rp, i) : -1;
+        rank[k] = key[k] >= 0 ? atomicAdd(&cnt[key[k]], 1) : 0;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x) base[b] = cnt[b] ? atomicAdd(fill + b, cnt[b]) : 0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSchedTile / 256; ++k)
+        if (key[k] >= 0) order[base[key[k]] + rank[k]] = i0 + k * 256 + threadIdx.x;
+}
+
 int grid_for(int64_t work, int threads, int num_sms, int per_sm) {
     int64_t g = (work + threads - 1) / threads;
     int64_t cap = (int64_t)num_sms * per_sm;
@@ -360,103 +408,183 @@ igp_status scan_exclusive(const int32_t* in, int32_t* out, int32_t n, cudaStream
     return IGP_OK;
 }
 
+namespace {
+
+// ---------------------------------------------------------------- B6 degree-sorted relabelling
+// order[r] = original id of new row r (descending degree, ascending id within a degree
+// bucket after the segmented sort: deterministic); inv[order[r]] = r.
+__global__ void inverse_perm_kernel(const int32_t* __restrict__ order, int32_t n, int32_t* __restrict__ inv,
+                                    const int32_t* __restrict__ rp, int32_t* __restrict__ degp) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += stride) {
+        const int32_t o = order[r];
+        inv[o] = (int32_t)r;
+        degp[r] = rp[o + 1] - rp[o];
+    }
+}
+
+// new row r takes original row order[r] with every neighbour id mapped through inv
+__global__ void perm_scatter_kernel(const int32_t* __restrict__ order, const int32_t* __restrict__ inv,
+                                    const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                    const int32_t* __restrict__ rpp, int32_t* __restrict__ cip, int32_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
+        const int32_t o = order[r];
+        const int32_t src = rp[o], len = rp[o + 1] - src, dst = rpp[r];
+        for (int32_t k = lane; k < len; k += 32) cip[dst + k] = inv[ci[src + k]];
+    }
+}
+
+struct SortScratch {
+    int32_t* big_list;     // capacity >= number of segments
+    int32_t* giant_list;   // capacity >= number of segments
+    int32_t* counters;     // [2]
+    uint32_t* bitmap;      // kGiantBlocks x ceil(value_range / 32) words
+};
+
+// sort (and dedup) every segment data[off[k] .. off[k+1]) ascending; ucnt[k] = unique count
+igp_status segmented_sort(const int32_t* off, int32_t* data, int32_t* ucnt, int32_t nseg, int64_t max_len,
+                          int32_t value_range, const SortScratch& sc, cudaStream_t s, const DeviceInfo& di) {
+    IGP_CUDA(cudaMemsetAsync(sc.counters, 0, 2 * sizeof(int32_t), s), "memset");
+    const int rg = grid_for((int64_t)nseg * 32, 256, di.num_sms, 8);
+    sort_rows_warp_kernel<<<rg, 256, 0, s>>>(off, data, ucnt, nseg, sc.big_list, sc.counters, sc.giant_list,
+                                             sc.counters + 1);
+    IGP_TRY(launch_status("sort_rows_warp_kernel"));
+    if (max_len > kWarpSortCap) {
+        cudaFuncSetAttribute(sort_rows_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kBlockSortCap * (int)sizeof(int32_t));
+        sort_rows_block_kernel<<<di.num_sms, 1024, kBlockSortCap * sizeof(int32_t), s>>>(off, data, ucnt, sc.big_list,
+                                                                                         sc.counters);
+        IGP_TRY(launch_status("sort_rows_block_kernel"));
+        if (max_len > kBlockSortCap) {
+            sort_rows_giant_kernel<<<kGiantBlocks, 1024, 0, s>>>(off, data, ucnt, sc.giant_list, sc.counters + 1,
+                                                                 sc.bitmap, value_range);
+            IGP_TRY(launch_status("sort_rows_giant_kernel"));
+        }
+    }
+    return IGP_OK;
+}
+
+}  // namespace
+
 igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, cudaStream_t s, CsrDevice* out) {
     DeviceInfo di;
     if (!device_info(&di)) return IGP_ERR_CUDA;
     const int64_t raw = 2 * E;  // both orientations, before dedup / self-loop removal
     const int32_t words = (n + 31) >> 5;
+    const int32_t lists = n > kDegBuckets ? n : kDegBuckets;
     // temporaries in one stream-ordered block
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     size_t o_cnt = 0;
-    size_t o_off = o_cnt + sizeof(int32_t) * (size_t)n;
-    size_t o_ucnt = o_off + sizeof(int32_t) * ((size_t)n + 1);
-    size_t o_big = o_ucnt + sizeof(int32_t) * (size_t)n;
-    size_t o_giant = o_big + sizeof(int32_t) * (size_t)n;
-    size_t o_flags = o_giant + sizeof(int32_t) * (size_t)n;  // err, big_count, giant_count, pad
-    size_t o_bitmap = o_flags + 4 * sizeof(int32_t);
-    size_t o_tmp = o_bitmap + sizeof(uint32_t) * (size_t)words * kGiantBlocks;
-    o_tmp = (o_tmp + 255) & ~(size_t)255;
+    size_t o_off = al(o_cnt + sizeof(int32_t) * (size_t)n);
+    size_t o_ucnt = al(o_off + sizeof(int32_t) * ((size_t)n + 1));
+    size_t o_big = al(o_ucnt + sizeof(int32_t) * (size_t)lists);
+    size_t o_giant = al(o_big + sizeof(int32_t) * (size_t)lists);
+    size_t o_flags = al(o_giant + sizeof(int32_t) * (size_t)lists);  // err, sort counters
+    size_t o_hist = al(o_flags + 4 * sizeof(int32_t));                // kDegBuckets
+    size_t o_boff = al(o_hist + sizeof(int32_t) * kDegBuckets);       // kDegBuckets + 1
+    size_t o_fill = al(o_boff + sizeof(int32_t) * (kDegBuckets + 1));  // kDegBuckets + 1
+    size_t o_inv = al(o_fill + sizeof(int32_t) * (kDegBuckets + 1));
+    size_t o_degp = al(o_inv + sizeof(int32_t) * (size_t)n);
+    size_t o_bitmap = al(o_degp + sizeof(int32_t) * (size_t)n);
+    size_t o_tmp = al(o_bitmap + sizeof(uint32_t) * (size_t)words * kGiantBlocks);
     size_t total = o_tmp + sizeof(int32_t) * (size_t)(raw > 0 ? raw : 1);
     char* ws = nullptr;
     IGP_CUDA(alloc_async((void**)&ws, total, s), "build workspace alloc");
     int32_t* cnt = (int32_t*)(ws + o_cnt);
     int32_t* off = (int32_t*)(ws + o_off);
     int32_t* ucnt = (int32_t*)(ws + o_ucnt);
-    int32_t* big_list = (int32_t*)(ws + o_big);
-    int32_t* giant_list = (int32_t*)(ws + o_giant);
     int32_t* flags = (int32_t*)(ws + o_flags);
-    uint32_t* bitmap = (uint32_t*)(ws + o_bitmap);
+    int32_t* hist = (int32_t*)(ws + o_hist);
+    int32_t* boff = (int32_t*)(ws + o_boff);
+    int32_t* fill = (int32_t*)(ws + o_fill);
+    int32_t* inv = (int32_t*)(ws + o_inv);
+    int32_t* degp = (int32_t*)(ws + o_degp);
     int32_t* tmp = (int32_t*)(ws + o_tmp);
+    SortScratch sc{(int32_t*)(ws + o_big), (int32_t*)(ws + o_giant), flags + 1, (uint32_t*)(ws + o_bitmap)};
 
-    int32_t* row_ptr = nullptr;
-    igp_status st = cuda_status(alloc_async((void**)&row_ptr, sizeof(int32_t) * ((size_t)n + 1), s), "row_ptr alloc");
-    if (st != IGP_OK) {
-        free_async(ws, s);
-        return st;
-    }
+    CsrDevice c;
+    c.n = n;
+    igp_status st = cuda_status(alloc_async((void**)&c.row_ptr, sizeof(int32_t) * ((size_t)n + 1), s), "alloc");
+    if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.order, sizeof(int32_t) * (size_t)n, s), "alloc");
+    if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 1), s), "alloc");
     auto fail = [&](igp_status e) {
         free_async(ws, s);
-        free_async(row_ptr, s);
+        free_async(c.row_ptr, s);
+        free_async(c.order, s);
+        free_async(c.rp_perm, s);
+        free_async(c.col_idx, s);
+        free_async(c.col_perm, s);
         return e;
     };
-    if ((st = cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset")) != IGP_OK) return fail(st);
-    if ((st = cuda_status(cudaMemsetAsync(flags, 0, 4 * sizeof(int32_t), s), "memset")) != IGP_OK) return fail(st);
+    if (st != IGP_OK) return fail(st);
+#define IGP_STEP(expr)                                  \
+    do {                                                \
+        igp_status _s = (expr);                         \
+        if (_s != IGP_OK) return fail(_s);              \
+    } while (0)
+    IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
+    IGP_STEP(cuda_status(cudaMemsetAsync(flags, 0, 4 * sizeof(int32_t), s), "memset"));
+    // B1-B3: count, scan, scatter both orientations into row buckets
     const int eg = grid_for(E, 256, di.num_sms, 16);
     if (E > 0) {
         count_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, cnt, flags);
-        if ((st = launch_status("count_kernel")) != IGP_OK) return fail(st);
+        IGP_STEP(launch_status("count_kernel"));
     }
-    if ((st = scan_exclusive(cnt, off, n, s)) != IGP_OK) return fail(st);
+    IGP_STEP(scan_exclusive(cnt, off, n, s));
     if (E > 0) {
-        if ((st = cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset")) != IGP_OK)
-            return fail(st);
+        IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
         scatter_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, off, cnt, tmp);
-        if ((st = launch_status("scatter_kernel")) != IGP_OK) return fail(st);
+        IGP_STEP(launch_status("scatter_kernel"));
     }
-    const int rg = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
-    sort_rows_warp_kernel<<<rg, 256, 0, s>>>(off, tmp, ucnt, n, big_list, flags + 1, giant_list, flags + 2);
-    if ((st = launch_status("sort_rows_warp_kernel")) != IGP_OK) return fail(st);
-    if (E > kWarpSortCap) {  // a raw row longer than kWarpSortCap needs > kWarpSortCap edges
-        cudaFuncSetAttribute(sort_rows_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kBlockSortCap * (int)sizeof(int32_t));
-        sort_rows_block_kernel<<<di.num_sms, 1024, kBlockSortCap * sizeof(int32_t), s>>>(off, tmp, ucnt, big_list,
-                                                                                         flags + 1);
-        if ((st = launch_status("sort_rows_block_kernel")) != IGP_OK) return fail(st);
-        if (E > kBlockSortCap) {
-            sort_rows_giant_kernel<<<kGiantBlocks, 1024, 0, s>>>(off, tmp, ucnt, giant_list, flags + 2, bitmap, n);
-            if ((st = launch_status("sort_rows_giant_kernel")) != IGP_OK) return fail(st);
-        }
-    }
-    if ((st = scan_exclusive(ucnt, row_ptr, n, s)) != IGP_OK) return fail(st);
+    // B4-B5: per-row sort + dedup, row pointers
+    IGP_STEP(segmented_sort(off, tmp, ucnt, n, E, n, sc, s, di));
+    IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
+    // B6a: degree-descending order (counting sort by degree, then ascending id per bucket)
+    IGP_STEP(cuda_status(cudaMemsetAsync(hist, 0, sizeof(int32_t) * kDegBuckets, s), "memset"));
+    degree_hist_kernel<<<grid_for(n, 256, di.num_sms, 4), 256, 0, s>>>(c.row_ptr, n, hist);
+    IGP_STEP(launch_status("degree_hist_kernel"));
+    IGP_STEP(scan_exclusive(hist, boff, kDegBuckets, s));
+    IGP_STEP(cuda_status(cudaMemcpyAsync(fill, boff, sizeof(int32_t) * (kDegBuckets + 1), cudaMemcpyDeviceToDevice, s),
+                         "copy"));
+    degree_scatter_kernel<<<(n + kSchedTile - 1) / kSchedTile, 256, 0, s>>>(c.row_ptr, n, fill, c.order);
+    IGP_STEP(launch_status("degree_scatter_kernel"));
+    IGP_STEP(segmented_sort(boff, c.order, hist, kDegBuckets, n, n, sc, s, di));
     // the build's single host synchronisation: nnz and the error flag
     int32_t host_vals[2] = {0, 0};
-    if ((st = cuda_status(cudaMemcpyAsync(&host_vals[0], row_ptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
-                          "nnz readback")) != IGP_OK)
-        return fail(st);
-    if ((st = cuda_status(cudaMemcpyAsync(&host_vals[1], flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
-                          "flag readback")) != IGP_OK)
-        return fail(st);
-    if ((st = cuda_status(cudaStreamSynchronize(s), "build sync")) != IGP_OK) return fail(st);
+    IGP_STEP(cuda_status(cudaMemcpyAsync(&host_vals[0], c.row_ptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+                         "nnz readback"));
+    IGP_STEP(cuda_status(cudaMemcpyAsync(&host_vals[1], flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+                         "flag readback"));
+    IGP_STEP(cuda_status(cudaStreamSynchronize(s), "build sync"));
     if (host_vals[1] != 0) {
         set_error("igp_build_graph: edge index outside [0, num_nodes)");
         return fail(IGP_ERR_INPUT);
     }
-    const int64_t nnz = host_vals[0];
-    int32_t* col_idx = nullptr;
-    if ((st = cuda_status(alloc_async((void**)&col_idx, sizeof(int32_t) * (size_t)(nnz > 0 ? nnz : 1), s),
-                          "col_idx alloc")) != IGP_OK)
-        return fail(st);
-    if (nnz > 0) {
-        compact_kernel<<<rg, 256, 0, s>>>(off, tmp, row_ptr, col_idx, n);
-        if ((st = launch_status("compact_kernel")) != IGP_OK) {
-            free_async(col_idx, s);
-            return fail(st);
-        }
+    c.nnz = host_vals[0];
+    const size_t cbytes = sizeof(int32_t) * (size_t)(c.nnz + kColPad);
+    IGP_STEP(cuda_status(alloc_async((void**)&c.col_idx, cbytes, s), "col_idx alloc"));
+    IGP_STEP(cuda_status(alloc_async((void**)&c.col_perm, cbytes, s), "col_perm alloc"));
+    IGP_STEP(cuda_status(cudaMemsetAsync(c.col_idx + c.nnz, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
+    IGP_STEP(cuda_status(cudaMemsetAsync(c.col_perm + c.nnz, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
+    const int rg = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
+    if (c.nnz > 0) {
+        compact_kernel<<<rg, 256, 0, s>>>(off, tmp, c.row_ptr, c.col_idx, n);
+        IGP_STEP(launch_status("compact_kernel"));
     }
+    // B6b: the relabelled CSR the filter steps run on (rows by descending degree)
+    inverse_perm_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n, inv, c.row_ptr, degp);
+    IGP_STEP(launch_status("inverse_perm_kernel"));
+    IGP_STEP(scan_exclusive(degp, c.rp_perm, n, s));
+    if (c.nnz > 0) {
+        perm_scatter_kernel<<<rg, 256, 0, s>>>(c.order, inv, c.row_ptr, c.col_idx, c.rp_perm, c.col_perm, n);
+        IGP_STEP(launch_status("perm_scatter_kernel"));
+        IGP_STEP(segmented_sort(c.rp_perm, c.col_perm, ucnt, n, E, n, sc, s, di));
+    }
+#undef IGP_STEP
     free_async(ws, s);
-    out->row_ptr = row_ptr;
-    out->col_idx = col_idx;
-    out->n = n;
-    out->nnz = nnz;
+    *out = c;
     return IGP_OK;
 }
 

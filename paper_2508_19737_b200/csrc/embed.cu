@@ -1,24 +1,35 @@
 // embed.cu — igp_embed: Alg. 1 lines 1-6 on one GPU.
 //
 // Kernels:
-//   E1a scale_kernel     D_tau by Eq. (1) / D + tau I in fp64;
-//                        per node {s = D^-1/2, r = D^1/2} as fp32
-//   E1b affine_kernel    c_i = theta + alpha s_i sum_{j in N(i)} s_j   ( = (phi * 1)_i )
-//   E2  input_kernel     Theta = X / sqrt(d), X ~ Philox/Box-Muller N(0,1);  y0 = s * Theta
-//   E3  layer_kernel<D>  one filter step, L launches:  gather y_j = s_j t_j rows
-//                        (float4, one warp per row, 32/(D/4) neighbour groups),
-//                        Eq. (3) with the deferred column z-score, tanh (Eq. (4)),
-//                        store y' = s t', per-column fp64 sum / sum-of-squares;
-//                        the last block to finish reduces the block partials in a
-//                        fixed order and publishes (mu, 1/sigma) for the next step
-//   E4  output_kernel    Z~ = sigmoid((t - mu)/sigma)  (Eq. (4))
+//   E1a scale_kernel       D_tau by Eq. (1) / D + tau I in fp64;
+//                          per node {s = D^-1/2, r = D^1/2} as fp32
+//   E1b affine_kernel      c_i = theta + alpha s_i sum_{j in N(i)} s_j  ( = (phi * 1)_i ), kept as hi+lo fp32
+//   E2  input_kernel<W>    Theta = X / sqrt(d), X ~ Philox/Box-Muller N(0,1); y0 = s * Theta
+//   E3  layer_kernel<W>    one filter step on a W-column slice (L launches per slice):
+//                          gather y_j = s_j t_j (float4), Eq. (3) with the deferred column
+//                          z-score, tanh (Eq. (4)), store y' = s t', exact column sums
+//   E4  output_kernel<W>   Z~ = sigmoid((t - mu)/sigma)  (Eq. (4))
+//
+// Column slicing.  Every step of the FFP acts on each column independently:
+// phi* mixes rows only, tanh/sigmoid are element-wise and ZNorm is per column
+// (PAPER.md:155, :164-166).  So the d columns are processed as d/W slices of W
+// columns, each pushed through all L steps before the next: the gathered slice
+// (N x W fp32) is sized to stay resident in L2 (DESIGN.md §5 derives W from the
+// measured gather bandwidth table).
 //
 // Deferred ZNorm.  ZNorm is a per-column affine map and phi* is linear, so with
 // t = tanh(P) of the previous step and Z = (t - mu)/sigma:
 //   phi * Z = [theta t_i + alpha s_i sum_j s_j t_j - mu c_i] / sigma,  c_i = (phi * 1)_i.
-// Hence the normalised matrix is never written: each step stores y = s t once
-// and the next step applies (mu, 1/sigma) while it gathers.
+// Each step stores y = s t once; the next step applies (mu, 1/sigma) while it gathers.
+//
+// Exact column statistics.  Each t (and t^2) is rounded to a fixed grid 2^-g
+// (g chosen from N so that |sum| < 2^53 grid units) before it is accumulated in
+// fp64; every partial sum is then an exact integer multiple of 2^-g, so the sums
+// are independent of summation order: blocks combine them with plain atomics,
+// the row schedule is free, and the output is still bitwise deterministic.  The
+// rounding perturbs mu and sigma by < 2^-g (~1e-9), far below fp32 resolution.
 #include <cmath>
+#include <cstdlib>
 
 #include "igp_internal.cuh"
 #include "philox.cuh"
@@ -26,12 +37,15 @@
 namespace igp {
 namespace {
 
-constexpr int kLayerThreads = 256;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 16;      // neighbours per index chunk
+constexpr int kFoldChunks = 4;  // fp32 partial sums span at most 64 neighbours
 constexpr unsigned kFull = 0xffffffffu;
+constexpr bool kDefaultOcc4 = true;
 
 __global__ void scale_kernel(const int32_t* __restrict__ rp, int32_t n, double tau, double eps,
-                             float4* __restrict__ node, double2* __restrict__ st0, int d,
-                             unsigned* __restrict__ counter) {
+                             float4* __restrict__ node) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
         const int32_t deg = rp[i + 1] - rp[i];
@@ -49,10 +63,6 @@ __global__ void scale_kernel(const int32_t* __restrict__ rp, int32_t n, double t
             r = (float)sq;
         }
         node[i] = make_float4(s, r, 0.0f, 0.0f);
-    }
-    if (blockIdx.x == 0) {
-        for (int c = threadIdx.x; c < d; c += blockDim.x) st0[c] = make_double2(0.0, 1.0);  // Z^(0) = Theta
-        if (threadIdx.x == 0) *counter = 0u;
     }
 }
 
@@ -77,185 +87,305 @@ __global__ void affine_kernel(const int32_t* __restrict__ rp, const int32_t* __r
     }
 }
 
-// y0 = s_i * Theta_i,  Theta = X / sqrt(d); element (i, c) is draw k = i*d + c (block k/4)
-__global__ void input_kernel(uint64_t seed, uint64_t sub, int32_t n, int d, const float4* __restrict__ node,
+// slice k of y0 = s_i * Theta_i, Theta = X / sqrt(d); element (i, c) of original node i is
+// draw k = i*d + c; relabelled row r holds original node order[r]
+template <int W>
+__global__ void input_kernel(uint64_t seed, uint64_t sub, int32_t n, int d, int col0,
+                             const int32_t* __restrict__ order, const float4* __restrict__ node,
                              float4* __restrict__ y0) {
-    const int64_t nb = (int64_t)n * d / 4;
+    constexpr int LPR = W / 4;
+    const int64_t total = (int64_t)n * LPR;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const double sqd = sqrt((double)d);
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += stride) {
-        const U4 r = philox_block(seed, sub, (uint64_t)b);
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
+        const int64_t i = idx / LPR;
+        const int q = (int)(idx % LPR);
+        const uint64_t b = (uint64_t)(((int64_t)order[i] * d + col0) / 4 + q);  // draws of the ORIGINAL id
+        const U4 r = philox_block(seed, sub, b);
         double x0, x1, x2, x3;
         box_muller64(r.x, r.y, x0, x1);
         box_muller64(r.z, r.w, x2, x3);
-        const double s = (double)node[(4 * b) / d].x;
-        y0[b] = make_float4((float)(s * (x0 / sqd)), (float)(s * (x1 / sqd)), (float)(s * (x2 / sqd)),
-                            (float)(s * (x3 / sqd)));
+        const double s = (double)node[i].x;
+        y0[idx] = make_float4((float)(s * (x0 / sqd)), (float)(s * (x1 / sqd)), (float)(s * (x2 / sqd)),
+                              (float)(s * (x3 / sqd)));
     }
 }
 
-struct LayerParams {
+struct LayerArgs {
     const int32_t* rp;
     const int32_t* ci;
-    const float4* node;
-    const float4* yin;
-    float4* yout;
-    const double2* st_in;  // [D] (mu, 1/sigma) of the previous step
-    double2* st_out;       // [D] (mu, 1/sigma) of this step
-    double* st64_out;      // [2D] (mu, sigma) record
-    double* partials;     // [gridDim.x][2D]
-    unsigned* counter;
+    const float4* node;     // {s, r, c_hi, c_lo}
+    const float4* yin;      // [N][W/4]
+    float4* yout;           // [N][W/4]
+    const double* sums_in;  // [2W] (sum t, sum t^2) of the previous step; nullptr: Z = Theta (mu 0, sigma 1)
+    double* sums_out;       // [2W], zero on entry
     int32_t n;
     float theta, alpha;
     int linear;
+    double grid_c;  // 1.5 * 2^(52-g): (x + grid_c) - grid_c rounds x to the 2^-g grid
 };
 
-__device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
-
-__device__ __forceinline__ void add4(float4& a, const float4& b) {
-    a.x += b.x;
-    a.y += b.y;
-    a.z += b.z;
-    a.w += b.w;
+// (mu, 1/sigma) of column c from exact sums; population std (reading A2), floor 1e-8 -> 0 (A3)
+__device__ __forceinline__ void column_stats(const double* sums, int c, int W, int32_t n, double& mu, double& isg) {
+    const double invN = 1.0 / (double)n;
+    const double m = sums[c] * invN;
+    double var = sums[W + c] * invN - m * m;
+    var = var > 0.0 ? var : 0.0;
+    const double sd = sqrt(var);
+    mu = m;
+    isg = sd < 1e-8 ? 0.0 : 1.0 / sd;
 }
 
-template <int D>
-__global__ void __launch_bounds__(kLayerThreads) layer_kernel(const LayerParams p) {
-    constexpr int LPR = D / 4;   // lanes per feature row (one float4 each)
-    constexpr int G = 32 / LPR;  // neighbour groups per warp
-    constexpr int NW = kLayerThreads / 32;
-    constexpr int B = LPR < 8 ? LPR : 8;  // loads in flight per lane per batch
-    __shared__ double red[NW][2 * D];
-    __shared__ double fin[kLayerThreads];
-    __shared__ int is_last;
+__device__ __forceinline__ double grid_round(double x, double c) { return __dsub_rn(__dadd_rn(x, c), c); }
+
+__device__ __forceinline__ int4 ld_idx4(const int32_t* p) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int2 ld_idx2(const int32_t* p) {
+    int2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ld_idx1(const int32_t* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// 256-bit vector access (sm_100: LDG.256 / STG.256) and packed fp32 adds (FADD2)
+__device__ __forceinline__ void ldg256(const void* ptr, uint64_t (&v)[4]) {
+    asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(ptr));
+}
+__device__ __forceinline__ void stg256(void* ptr, const uint64_t (&v)[4]) {
+    asm volatile("st.global.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3])
+                 : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); }
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float2 unpack2(uint64_t v) {
+    float2 f;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(v));
+    return f;
+}
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+    uint64_t v;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(v) : "f"(a), "f"(b));
+    return v;
+}
+
+template <int IPL>
+__device__ __forceinline__ void load_idx(const int32_t* ci, int32_t e0, int32_t end, int q, int (&jr)[IPL]) {
+#pragma unroll
+    for (int k = 0; k < IPL; ++k) {
+        const int32_t e = e0 + q * IPL + k;
+        jr[k] = e < end ? ld_idx1(ci + e) : 0;
+    }
+}
+
+// One filter step on a W-column slice.
+//  - A group of LPR = W/8 lanes owns one row at a time; each lane holds 8 columns, so a
+//    neighbour costs one 256-bit gather and 4 packed fp32 adds per lane.  G = 32/LPR rows
+//    per warp run side by side, in descending-degree order (similar trip counts).
+//  - Neighbour indices come 16 at a time (IPL per lane, broadcast by shuffles); the next
+//    chunk's indices are fetched while this chunk is gathered.
+//  - Column statistics: each warp stages its G x W tile of t in shared memory and every
+//    lane folds 8 of those values (OC whole columns) into fp64 registers, so the per-lane
+//    state is 2*OC doubles instead of 16.
+template <int W, int MB>
+__global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) {
+    constexpr int LPR = W / 8;
+    constexpr int G = 32 / LPR;
+    constexpr int IPL = kChunk / LPR;
+    constexpr int NG = kWarps * G;            // row groups per block
+    constexpr int OC = W >= 32 ? W / 32 : 1;  // statistics columns owned per lane
+    constexpr int OR = W >= 32 ? G : G / 2;   // ... each over OR rows of the warp tile
+    __shared__ double2 st[W];                 // (mu, 1/sigma) of the previous step
+    __shared__ __align__(16) float stage[kWarps][G * W];
+    extern __shared__ double dyn_smem[];
+    double (*acc_f)[W] = reinterpret_cast<double (*)[W]>(dyn_smem);  // [NG][W] long-row partials
+    for (int c = threadIdx.x; c < W; c += kThreads) {
+        double m = 0.0, is = 1.0;
+        if (p.sums_in) column_stats(p.sums_in, c, W, p.n, m, is);
+        st[c] = make_double2(m, is);
+    }
+    for (int t = threadIdx.x; t < NG * W; t += kThreads) (&acc_f[0][0])[t] = 0.0;
+    __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q = lane % LPR, g = lane / LPR;
-    double mu[4], isg[4];
+    const int grp = warp * G + g;
+    const unsigned gmask = ((LPR == 32) ? kFull : ((1u << LPR) - 1u)) << (g * LPR);
+    const uint64_t* yin = reinterpret_cast<const uint64_t*>(p.yin);  // row j, lane q: yin + (j*LPR + q)*4
+    uint64_t* yout = reinterpret_cast<uint64_t*>(p.yout);
+    float* tile = stage[warp];
+    const int oc0 = W >= 32 ? lane * OC : lane / 2;  // owned statistics columns / rows
+    const int or0 = W >= 32 ? 0 : (lane & 1) * OR;
+    double s1[OC], s2[OC];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const double2 m = p.st_in[4 * q + k];
-        mu[k] = m.x;
-        isg[k] = m.y;
-    }
-    double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < OC; ++k) s1[k] = s2[k] = 0.0;
 
-    for (int32_t row = blockIdx.x * NW + warp; row < p.n; row += gridDim.x * NW) {
-        const int32_t beg = __ldg(p.rp + row), end = __ldg(p.rp + row + 1);
-        // neighbour sum: fp32 within a 32-neighbour chunk, chunks folded in fp64
-        double ad[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int32_t e0 = beg; e0 < end; e0 += 32) {
-            const int cnt = min(32, end - e0);
-            const int32_t jl = lane < cnt ? __ldg(p.ci + e0 + lane) : 0;
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t step = (int64_t)gridDim.x * NG;
+    // warp-uniform batches of G consecutive rows of the relabelled (degree-sorted) CSR
+    for (int64_t base = (int64_t)blockIdx.x * NG + warp * G; base < p.n; base += step) {
+        const int32_t row = (int32_t)(base + g);
+        const bool valid = row < p.n;
+        float t8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (valid) {
+            const int32_t beg = __ldg(p.rp + row), end = __ldg(p.rp + row + 1);
+            const uint64_t* own_ptr = yin + ((size_t)row * LPR + q) * 4;
+            prefetch_l2(own_ptr);  // the row's own values are needed only after its gathers
+            prefetch_l2(p.node + row);
+            // neighbour sum: packed fp32 within up to kFoldChunks chunks, then folded into
+            // fp64 partials in shared memory (only rows longer than 64 neighbours fold)
+            uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+            int nc = 0;
+            bool folded = false;
+            double* af = acc_f[grp] + 8 * q;
+            int jr[IPL];
+            load_idx<IPL>(p.ci, beg, end, q, jr);
+            for (int32_t e0 = beg; e0 < end; e0 += kChunk) {
+                const int32_t e1 = e0 + kChunk;
+                int jn[IPL];
+                load_idx<IPL>(p.ci, e1, end, q, jn);  // prefetch the next chunk's indices
+                const int cnt = end - e0;             // >= 1; the chunk is full when >= kChunk
+                if (cnt >= kChunk) {
 #pragma unroll
-            for (int t0 = 0; t0 < LPR; t0 += B) {
-                if (t0 * G >= cnt) break;
-                float4 v[B];
+                    for (int u = 0; u < kChunk; ++u) {
+                        const int j = __shfl_sync(gmask, jr[u % IPL], u / IPL, LPR);
+                        uint64_t v[4];
+                        ldg256(yin + ((size_t)j * LPR + q) * 4, v);
 #pragma unroll
-                for (int t = 0; t < B; ++t) {
-                    const int k = (t0 + t) * G + g;
-                    const int32_t j = __shfl_sync(kFull, jl, k);
-                    v[t] = (k < cnt) ? ldg4(p.yin + (size_t)j * LPR + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[k]);
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kChunk; ++u) {
+                        const int j = __shfl_sync(gmask, jr[u % IPL], u / IPL, LPR);
+                        if (u < cnt) {
+                            uint64_t v[4];
+                            ldg256(yin + ((size_t)j * LPR + q) * 4, v);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[k]);
+                        }
+                    }
+                }
+                if (++nc == kFoldChunks && e1 < end) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float2 f = unpack2(acc[k]);
+                        af[2 * k] += (double)f.x;
+                        af[2 * k + 1] += (double)f.y;
+                        acc[k] = 0ull;
+                    }
+                    nc = 0;
+                    folded = true;
                 }
 #pragma unroll
-                for (int t = 0; t < B; ++t) add4(acc, v[t]);
+                for (int k = 0; k < IPL; ++k) jr[k] = jn[k];
             }
-            ad[0] += (double)acc.x;
-            ad[1] += (double)acc.y;
-            ad[2] += (double)acc.z;
-            ad[3] += (double)acc.w;
-        }
-#pragma unroll
-        for (int o = LPR; o < 32; o <<= 1) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) ad[k] += __shfl_xor_sync(kFull, ad[k], o);
-        }
-        if (g == 0) {
-            const float4 nd = __ldg(p.node + row);  // {s, r, c_hi, c_lo}
-            const float4 own = ldg4(p.yin + (size_t)row * LPR + q);
-            const double si = (double)nd.x, ci = (double)nd.z + (double)nd.w;
-            const float y[4] = {own.x, own.y, own.z, own.w};
-            float o4[4];
+            double ad[8];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const float tself = y[k] * nd.y;  // t_i = y_i / s_i
-                const double P = ((double)p.theta * (double)tself + (double)p.alpha * si * ad[k] - mu[k] * ci) * isg[k];
-                const float t = p.linear ? (float)P : tanhf((float)P);
-                s1[k] += (double)t;
-                s2[k] = fma((double)t, (double)t, s2[k]);
-                o4[k] = nd.x * t;
+                const float2 f = unpack2(acc[k]);
+                ad[2 * k] = (double)f.x;
+                ad[2 * k + 1] = (double)f.y;
             }
-            p.yout[(size_t)row * LPR + q] = make_float4(o4[0], o4[1], o4[2], o4[3]);
+            if (folded) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    ad[k] += af[k];
+                    af[k] = 0.0;
+                }
+            }
+            const float4 nd = __ldg(p.node + row);
+            uint64_t own[4];
+            ldg256(own_ptr, own);
+            const double si = (double)nd.x, cc = (double)nd.z + (double)nd.w;
+            uint64_t o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 y = unpack2(own[k]);
+                float yy[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double2 m = st[8 * q + 2 * k + h];
+                    const float tself = (h ? y.y : y.x) * nd.y;  // t_i = y_i / s_i
+                    const double P =
+                        ((double)p.theta * (double)tself + (double)p.alpha * si * ad[2 * k + h] - m.x * cc) * m.y;
+                    const float t = p.linear ? (float)P : tanhf((float)P);
+                    t8[2 * k + h] = t;
+                    yy[h] = nd.x * t;
+                }
+                o[k] = pack2(yy[0], yy[1]);
+            }
+            stg256(yout + ((size_t)row * LPR + q) * 4, o);
+        }
+        if (!p.linear) {
+            // stage the warp's G x W tile of t (invalid rows contribute 0) and fold owned columns
+            *reinterpret_cast<float4*>(tile + g * W + 8 * q) = make_float4(t8[0], t8[1], t8[2], t8[3]);
+            *reinterpret_cast<float4*>(tile + g * W + 8 * q + 4) = make_float4(t8[4], t8[5], t8[6], t8[7]);
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < OR; ++r) {
+#pragma unroll
+                for (int k = 0; k < OC; ++k) {
+                    const double x = (double)tile[(or0 + r) * W + oc0 + k];
+                    s1[k] += grid_round(x, p.grid_c);
+                    s2[k] += grid_round(x * x, p.grid_c);
+                }
+            }
+            __syncwarp();
         }
     }
     if (p.linear) return;
-
-    // ---- block partials of (sum t, sum t^2) per column, fixed order
-    if (g == 0) {
+    // exact sums: every partial is a multiple of the grid, so any combination order is exact
+    if (W < 32) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            red[warp][4 * q + k] = s1[k];
-            red[warp][D + 4 * q + k] = s2[k];
+        for (int k = 0; k < OC; ++k) {
+            s1[k] += __shfl_xor_sync(kFull, s1[k], 1);
+            s2[k] += __shfl_xor_sync(kFull, s2[k], 1);
+        }
+    }
+    __syncthreads();  // acc_f is reused as the per-warp reduction buffer [kWarps][2W]
+    double* red = dyn_smem;
+    if (W >= 32 || (lane & 1) == 0) {
+#pragma unroll
+        for (int k = 0; k < OC; ++k) {
+            red[warp * 2 * W + oc0 + k] = s1[k];
+            red[warp * 2 * W + W + oc0 + k] = s2[k];
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < 2 * D; t += kLayerThreads) {
+    for (int t = threadIdx.x; t < 2 * W; t += kThreads) {
         double v = 0.0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) v += red[w][t];
-        p.partials[(size_t)blockIdx.x * (2 * D) + t] = v;
+        for (int w = 0; w < kWarps; ++w) v += red[w * 2 * W + t];
+        atomicAdd(p.sums_out + t, v);
     }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) is_last = (atomicAdd(p.counter, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-
-    // ---- last block: fixed-order reduction over blocks, then (mu, 1/sigma)
-    constexpr int NS = 2 * D;
-    constexpr int NG = kLayerThreads / NS > 0 ? kLayerThreads / NS : 1;
-    double v = 0.0;
-    if (threadIdx.x < NS * NG) {
-        const int t = threadIdx.x % NS, grp = threadIdx.x / NS;
-#pragma unroll 8
-        for (int b = grp; b < (int)gridDim.x; b += NG) v += __ldcg(p.partials + (size_t)b * NS + t);
-    }
-    fin[threadIdx.x] = v;
-    __syncthreads();
-    if (threadIdx.x < NS) {
-        double tot = 0.0;
-        for (int grp = 0; grp < NG; ++grp) tot += fin[grp * NS + threadIdx.x];
-        red[0][threadIdx.x] = tot;
-    }
-    __syncthreads();
-    if (threadIdx.x < D) {
-        const double S = red[0][threadIdx.x], Q = red[0][D + threadIdx.x];
-        const double invN = 1.0 / (double)p.n;
-        const double m = S * invN;
-        double var = Q * invN - m * m;  // population variance (reading A2)
-        var = var > 0.0 ? var : 0.0;
-        const double sd = sqrt(var);
-        const double inv = sd < 1e-8 ? 0.0 : 1.0 / sd;  // degenerate column -> 0 (reading A3)
-        p.st_out[threadIdx.x] = make_double2(m, inv);
-        p.st64_out[threadIdx.x] = m;
-        p.st64_out[D + threadIdx.x] = sd;
-    }
-    if (threadIdx.x == 0) *p.counter = 0u;
 }
 
-template <int D>
-__global__ void output_kernel(float4* __restrict__ y, const float4* __restrict__ node, const double2* __restrict__ st,
-                              int32_t n, int mode) {
-    constexpr int LPR = D / 4;
+// Z~ = sigmoid((t - mu)/sigma) of a slice into columns [col0, col0 + W) of out [N][d]
+// (relabelled row i is written to the row of its original id order[i])
+template <int W>
+__global__ void output_kernel(const float4* __restrict__ y, const float4* __restrict__ node,
+                              const double* __restrict__ sums, const int32_t* __restrict__ order, int32_t n, int d,
+                              int col0, int mode, float* __restrict__ out) {
+    constexpr int LPR = W / 4;
     const int64_t total = (int64_t)n * LPR;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
         const int64_t i = idx / LPR;
         const int q = (int)(idx % LPR);
         const float r = node[i].y;
-        float4 v = y[idx];
+        const float4 v = y[idx];
         float a[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -263,30 +393,14 @@ __global__ void output_kernel(float4* __restrict__ y, const float4* __restrict__
             if (mode == IGP_MODE_LINEAR) {
                 a[k] = t;
             } else {
-                const double2 m = st[4 * q + k];
-                const float z = (float)(((double)t - m.x) * m.y);
+                double mu = 0.0, isg = 1.0;
+                if (sums) column_stats(sums, 4 * q + k, W, n, mu, isg);
+                const float z = (float)(((double)t - mu) * isg);
                 a[k] = (mode == IGP_MODE_FULL) ? 1.0f / (1.0f + expf(-z)) : z;
             }
         }
-        y[idx] = make_float4(a[0], a[1], a[2], a[3]);
+        *(float4*)(out + (int64_t)order[i] * d + col0 + 4 * q) = make_float4(a[0], a[1], a[2], a[3]);
     }
-}
-
-template <int D>
-int layer_grid(int32_t n, const DeviceInfo& di) {
-    static int occ_cache[64] = {0};
-    int& occ = occ_cache[di.device & 63];
-    if (occ == 0) {
-        int o = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, layer_kernel<D>, kLayerThreads, 0) != cudaSuccess || o < 1)
-            o = 1;
-        occ = o;
-    }
-    const int64_t rows_per_block = kLayerThreads / 32;
-    int64_t want = (n + rows_per_block - 1) / rows_per_block;
-    int64_t cap = (int64_t)di.num_sms * occ;
-    int64_t gsz = want < cap ? want : cap;
-    return (int)(gsz < 1 ? 1 : gsz);
 }
 
 int simple_grid(int64_t items, int threads, const DeviceInfo& di, int per_sm = 8) {
@@ -295,80 +409,146 @@ int simple_grid(int64_t items, int threads, const DeviceInfo& di, int per_sm = 8
     return (int)(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
-template <int D>
-igp_status run_embed_d(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s, EmbedTiming* timing) {
-    DeviceInfo di;
-    if (!device_info(&di)) return IGP_ERR_CUDA;
+template <int W>
+constexpr size_t layer_smem() {
+    return sizeof(double) * (size_t)(kWarps * (256 / W)) * W;  // acc_f: NG x W doubles (>= kWarps x 2W)
+}
+
+template <int W, int MB>
+int layer_grid(int32_t n, const DeviceInfo& di) {
+    static int occ_cache[64] = {0};
+    int& occ = occ_cache[di.device & 63];
+    if (occ == 0) {
+        cudaFuncSetAttribute(layer_kernel<W, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)layer_smem<W>());
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, layer_kernel<W, MB>, kThreads, layer_smem<W>()) !=
+                cudaSuccess ||
+            o < 1)
+            o = 1;
+        occ = o;
+    }
+    const int64_t rows_per_block = (int64_t)kWarps * (32 / (W / 8));
+    const int64_t want = (n + rows_per_block - 1) / rows_per_block;
+    const int64_t cap = (int64_t)di.num_sms * occ;
+    const int64_t g = want < cap ? want : cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
+// Measured random-gather bandwidth (GB/s) of B200 for row size R = 4W bytes vs the
+// gathered footprint (profiles/r01/gather_microbench.txt, LDG.128, 40M gathers).
+double gather_gbps(int row_bytes, double footprint_mb) {
+    static const double F[10] = {8, 16, 32, 48, 64, 96, 128, 192, 256, 512};
+    static const double T64[10] = {14515, 14580, 14547, 14387, 12495, 8663, 6775, 5039, 4314, 3161};
+    static const double T128[10] = {19519, 19154, 18961, 18932, 18094, 14165, 11858, 9615, 8565, 6465};
+    static const double T256[10] = {18934, 18520, 18268, 18172, 17635, 15312, 13101, 10682, 9541, 8173};
+    const double* T = row_bytes <= 64 ? T64 : (row_bytes <= 128 ? T128 : T256);
+    if (footprint_mb <= F[0]) return T[0];
+    for (int k = 1; k < 10; ++k)
+        if (footprint_mb <= F[k]) {
+            const double a = (log(footprint_mb) - log(F[k - 1])) / (log(F[k]) - log(F[k - 1]));
+            return T[k - 1] + a * (T[k] - T[k - 1]);
+        }
+    return T[9] * pow(512.0 / footprint_mb, 0.3);
+}
+
+// slice width: minimise predicted gather time + the CSR re-read per slice (IGP_SLICE_WIDTH overrides)
+int choose_width(int d, int32_t n, int64_t nnz) {
+    if (const char* env = getenv("IGP_SLICE_WIDTH")) {
+        const int w = atoi(env);
+        if ((w == 16 || w == 32 || w == 64 || w == 128) && w <= d && d % w == 0) return w;
+    }
+    int best = d;
+    double best_t = 1e300;
+    for (int w = d; w >= 16; w /= 2) {  // from the widest: fewer slices win ties
+        const double slices = (double)d / w;
+        const double gather = (double)nnz * 4.0 * w / (gather_gbps(4 * w, (double)n * 4.0 * w / 1048576.0) * 1e9);
+        const double csr = (4.0 * (double)nnz + 8.0 * n) / 6.0e12;
+        const double t = slices * (gather + csr);
+        if (t < best_t * 0.97) {
+            best_t = t;
+            best = w;
+        }
+    }
+    if (d / best > kMaxSlices) best = d / kMaxSlices;
+    return best;
+}
+
+template <int W, int MB>
+igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s,
+                       EmbedTiming* timing, const DeviceInfo& di) {
     const int32_t n = g.n;
-    const int L = o.steps;
-    const int grid = layer_grid<D>(n, di);
-    const size_t nd = (size_t)n * D;
-    // workspace: node | y (N x D) | partials | st | st64 | counter
-    size_t off_node = 0;
-    size_t off_y = off_node + sizeof(float4) * (size_t)n;
-    size_t off_part = off_y + sizeof(float) * nd;
-    size_t off_st = off_part + sizeof(double) * (size_t)grid * 2 * D;
-    size_t off_st64 = off_st + sizeof(double2) * (size_t)(L + 1) * D;
-    size_t off_cnt = off_st64 + sizeof(double) * (size_t)(L + 1) * 2 * D;
-    size_t total = off_cnt + 256;
+    const int L = o.steps, d = o.d, nslices = d / W;
+    const int grid = layer_grid<W, MB>(n, di);
+    const size_t nw = (size_t)n * W;
+    // workspace: node | y0 | y1 (N x W each) | sums [slices][L+1][2W]
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t off_node = 0;
+    const size_t off_y0 = al(off_node + sizeof(float4) * (size_t)n);
+    const size_t off_y1 = al(off_y0 + sizeof(float) * nw);
+    const size_t off_sums = al(off_y1 + sizeof(float) * nw);
+    const size_t sums_bytes = sizeof(double) * (size_t)nslices * (L + 1) * 2 * W;
     char* ws = nullptr;
-    IGP_CUDA(alloc_async((void**)&ws, total, s), "embed workspace alloc");
+    IGP_CUDA(alloc_async((void**)&ws, off_sums + sums_bytes, s), "embed workspace alloc");
     float4* node = (float4*)(ws + off_node);
-    float* ybuf = (float*)(ws + off_y);
-    double* partials = (double*)(ws + off_part);
-    double2* st = (double2*)(ws + off_st);
-    double* st64 = (double*)(ws + off_st64);
-    unsigned* counter = (unsigned*)(ws + off_cnt);
-    auto buf = [&](int l) -> float* { return ((L - l) % 2 == 0) ? out : ybuf; };
+    float4* ybuf[2] = {(float4*)(ws + off_y0), (float4*)(ws + off_y1)};
+    double* sums = (double*)(ws + off_sums);
+    // stats grid 2^-gexp with N * 2^gexp < 2^51 (|sum t|, sum t^2 <= N)
+    int lg = 0;
+    while (lg < 62 && ((int64_t)1 << lg) <= (int64_t)n) ++lg;
+    const int gexp = 51 - lg;
+    const double grid_c = 1.5 * ldexp(1.0, 52 - gexp);
 
     igp_status rc = IGP_OK;
+    const bool timed = (o.flags & IGP_FLAG_TIME_LAYERS) && timing;
     do {
-        scale_kernel<<<simple_grid(n, 256, di), 256, 0, s>>>(g.row_ptr, n, (double)o.tau, (double)o.eps, node, st, D,
-                                                               counter);
+        // all filter-step work runs on the relabelled CSR (rows by descending degree)
+        scale_kernel<<<simple_grid(n, 256, di), 256, 0, s>>>(g.rp_perm, n, (double)o.tau, (double)o.eps, node);
         if ((rc = launch_status("scale_kernel")) != IGP_OK) break;
-        // (an empty graph gives c_i = theta for every row)
-        affine_kernel<<<simple_grid((int64_t)n * 32, 256, di), 256, 0, s>>>(g.row_ptr, g.col_idx, n, o.theta,
+        affine_kernel<<<simple_grid((int64_t)n * 32, 256, di), 256, 0, s>>>(g.rp_perm, g.col_perm, n, o.theta,
                                                                               o.alpha, node);
         if ((rc = launch_status("affine_kernel")) != IGP_OK) break;
-        input_kernel<<<simple_grid((int64_t)nd / 4, 256, di), 256, 0, s>>>(o.seed, o.subsequence, n, D, node,
-                                                                            (float4*)buf(0));
-        if ((rc = launch_status("input_kernel")) != IGP_OK) break;
-        const bool timed = (o.flags & IGP_FLAG_TIME_LAYERS) && timing;
-        if (timed) {
-            if (!timing->ev0) cudaEventCreate(&timing->ev0);
-            if (!timing->ev1) cudaEventCreate(&timing->ev1);
-            cudaEventRecord(timing->ev0, s);
-        }
+        if ((rc = cuda_status(cudaMemsetAsync(sums, 0, sums_bytes, s), "sums memset")) != IGP_OK) break;
         const int linear = (o.mode == IGP_MODE_LINEAR) ? 1 : 0;
-        for (int l = 1; l <= L; ++l) {
-            LayerParams lp;
-            lp.rp = g.row_ptr;
-            lp.ci = g.col_idx;
-            lp.node = node;
-            lp.yin = (const float4*)buf(l - 1);
-            lp.yout = (float4*)buf(l);
-            lp.st_in = linear ? st : st + (size_t)(l - 1) * D;
-            lp.st_out = st + (size_t)l * D;
-            lp.st64_out = st64 + (size_t)l * 2 * D;
-            lp.partials = partials;
-            lp.counter = counter;
-            lp.n = n;
-            lp.theta = o.theta;
-            lp.alpha = o.alpha;
-            lp.linear = linear;
-            layer_kernel<D><<<grid, kLayerThreads, 0, s>>>(lp);
-            if ((rc = launch_status("layer_kernel")) != IGP_OK) break;
+        for (int k = 0; k < nslices && rc == IGP_OK; ++k) {
+            const int col0 = k * W;
+            double* sk = sums + (size_t)k * (L + 1) * 2 * W;
+            input_kernel<W><<<simple_grid((int64_t)n * (W / 4), 256, di), 256, 0, s>>>(o.seed, o.subsequence, n, d,
+                                                                                      col0, g.order, node, ybuf[0]);
+            if ((rc = launch_status("input_kernel")) != IGP_OK) break;
+            if (timed) {
+                if (!timing->ev0[k]) cudaEventCreate(&timing->ev0[k]);
+                if (!timing->ev1[k]) cudaEventCreate(&timing->ev1[k]);
+                cudaEventRecord(timing->ev0[k], s);
+            }
+            for (int l = 1; l <= L; ++l) {
+                LayerArgs a;
+                a.rp = g.rp_perm;
+                a.ci = g.col_perm;
+                a.node = node;
+                a.yin = ybuf[(l - 1) & 1];
+                a.yout = ybuf[l & 1];
+                a.sums_in = (linear || l == 1) ? nullptr : sk + (size_t)(l - 1) * 2 * W;
+                a.sums_out = sk + (size_t)l * 2 * W;
+                a.n = n;
+                a.theta = o.theta;
+                a.alpha = o.alpha;
+                a.linear = linear;
+                a.grid_c = grid_c;
+                layer_kernel<W, MB><<<grid, kThreads, layer_smem<W>(), s>>>(a);
+                if ((rc = launch_status("layer_kernel")) != IGP_OK) break;
+            }
+            if (rc != IGP_OK) break;
+            if (timed) cudaEventRecord(timing->ev1[k], s);
+            const double* sfin = (linear || L == 0) ? nullptr : sk + (size_t)L * 2 * W;
+            output_kernel<W><<<simple_grid((int64_t)n * (W / 4), 256, di), 256, 0, s>>>(ybuf[L & 1], node, sfin, g.order, n,
+                                                                                        d, col0, o.mode, out);
+            if ((rc = launch_status("output_kernel")) != IGP_OK) break;
         }
-        if (rc != IGP_OK) break;
-        if (timed) {
-            cudaEventRecord(timing->ev1, s);
-            timing->launches = L;
+        if (rc == IGP_OK && timed) {
+            timing->slices = nslices;
+            timing->launches = L * nslices;
             timing->valid = true;
         }
-        const double2* st_final = linear ? st : st + (size_t)L * D;
-        output_kernel<D><<<simple_grid((int64_t)nd / 4, 256, di), 256, 0, s>>>((float4*)out, node, st_final, n,
-                                                                               o.mode);
-        if ((rc = launch_status("output_kernel")) != IGP_OK) break;
     } while (0);
     free_async(ws, s);
     return rc;
@@ -377,14 +557,20 @@ igp_status run_embed_d(const CsrDevice& g, const igp_embed_opts& o, float* out, 
 }  // namespace
 
 igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s, EmbedTiming* timing) {
-    switch (o.d) {
-        case 16: return run_embed_d<16>(g, o, out, s, timing);
-        case 32: return run_embed_d<32>(g, o, out, s, timing);
-        case 64: return run_embed_d<64>(g, o, out, s, timing);
-        case 128: return run_embed_d<128>(g, o, out, s, timing);
-        default:
-            set_error("igp_embed: d must be one of 16, 32, 64, 128");
-            return IGP_ERR_UNSUPPORTED;
+    DeviceInfo di;
+    if (!device_info(&di)) return IGP_ERR_CUDA;
+    if (o.d != 16 && o.d != 32 && o.d != 64 && o.d != 128) {
+        set_error("igp_embed: d must be one of 16, 32, 64, 128");
+        return IGP_ERR_UNSUPPORTED;
+    }
+    if (timing) timing->valid = false;
+    const char* occ_env = getenv("IGP_LAYER_OCC");  // development knob: 3 or 4 blocks per SM
+    const bool occ4 = occ_env ? atoi(occ_env) == 4 : kDefaultOcc4;
+    switch (choose_width(o.d, g.n, g.nnz)) {
+        case 16: return occ4 ? run_embed_w<16, 4>(g, o, out, s, timing, di) : run_embed_w<16, 3>(g, o, out, s, timing, di);
+        case 32: return occ4 ? run_embed_w<32, 4>(g, o, out, s, timing, di) : run_embed_w<32, 3>(g, o, out, s, timing, di);
+        case 64: return occ4 ? run_embed_w<64, 4>(g, o, out, s, timing, di) : run_embed_w<64, 3>(g, o, out, s, timing, di);
+        default: return occ4 ? run_embed_w<128, 4>(g, o, out, s, timing, di) : run_embed_w<128, 3>(g, o, out, s, timing, di);
     }
 }
 

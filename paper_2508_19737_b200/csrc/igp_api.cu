@@ -175,19 +175,24 @@ igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t* d_col_
     return IGP_OK;
 }
 
-static void release_graph(igp_graph_t g) {
+static void release_graph(igp_graph_t g, cudaStream_t s) {
     // the CSR lives in the stream-ordered pool; callers have drained all work on it
-    free_async(g->csr.row_ptr, (cudaStream_t)0);
-    free_async(g->csr.col_idx, (cudaStream_t)0);
-    if (g->timing.ev0) cudaEventDestroy(g->timing.ev0);
-    if (g->timing.ev1) cudaEventDestroy(g->timing.ev1);
+    free_async(g->csr.row_ptr, s);
+    free_async(g->csr.col_idx, s);
+    free_async(g->csr.order, s);
+    free_async(g->csr.rp_perm, s);
+    free_async(g->csr.col_perm, s);
+    for (int k = 0; k < kMaxSlices; ++k) {
+        if (g->timing.ev0[k]) cudaEventDestroy(g->timing.ev0[k]);
+        if (g->timing.ev1[k]) cudaEventDestroy(g->timing.ev1[k]);
+    }
     delete g;
 }
 
 igp_status igp_destroy_graph(igp_graph_t g) {
     if (!g) return IGP_OK;
     cudaDeviceSynchronize();  // no stream may still read the CSR
-    release_graph(g);
+    release_graph(g, (cudaStream_t)0);
     return IGP_OK;
 }
 
@@ -227,7 +232,11 @@ igp_status igp_last_layer_time_ms(igp_graph_t g, float* total_ms, int32_t* launc
         return IGP_ERR_INPUT;
     }
     float ms = 0.0f;
-    IGP_CUDA(cudaEventElapsedTime(&ms, g->timing.ev0, g->timing.ev1), "cudaEventElapsedTime");
+    for (int k = 0; k < g->timing.slices; ++k) {
+        float t = 0.0f;
+        IGP_CUDA(cudaEventElapsedTime(&t, g->timing.ev0[k], g->timing.ev1[k]), "cudaEventElapsedTime");
+        ms += t;
+    }
     if (total_ms) *total_ms = ms;
     if (launches) *launches = g->timing.launches;
     return IGP_OK;
@@ -258,11 +267,7 @@ igp_status igp_embed_host(const int32_t* h_edges, int64_t num_edges, int32_t num
     free_async(d_out, s);
     igp_status st2 = cuda_status(cudaStreamSynchronize(s), "stream sync");
     // release the graph without a device-wide sync (its only user, `s`, is drained)
-    free_async(g->csr.row_ptr, s);
-    free_async(g->csr.col_idx, s);
-    if (g->timing.ev0) cudaEventDestroy(g->timing.ev0);
-    if (g->timing.ev1) cudaEventDestroy(g->timing.ev1);
-    delete g;
+    release_graph(g, s);
     return st != IGP_OK ? st : st2;
 }
 

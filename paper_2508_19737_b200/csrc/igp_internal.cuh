@@ -58,10 +58,14 @@ inline igp_status launch_status(const char* what) {
 // ---------------------------------------------------------------------------
 struct CsrDevice {
     int32_t* row_ptr = nullptr;  // [N+1]
-    int32_t* col_idx = nullptr;  // [nnz]
+    int32_t* col_idx = nullptr;  // [nnz + kColPad] (pad zero-filled: vector index loads may overrun a row)
+    int32_t* order = nullptr;    // [N] order[r] = original id of relabelled row r (descending degree)
+    int32_t* rp_perm = nullptr;  // [N+1] CSR of the relabelled graph (row r = node order[r]) ...
+    int32_t* col_perm = nullptr; // [nnz + kColPad]  ... with relabelled, ascending column ids
     int32_t n = 0;
     int64_t nnz = 0;
 };
+constexpr int kColPad = 16;
 igp_status build_csr(const int32_t* d_edges, int64_t num_edges, int32_t n, cudaStream_t s,
                      CsrDevice* out);
 
@@ -77,8 +81,10 @@ igp_status launch_philox_normal(uint64_t seed, uint64_t sub, int64_t count, floa
 // ---------------------------------------------------------------------------
 // embed.cu
 // ---------------------------------------------------------------------------
+constexpr int kMaxSlices = 8;
 struct EmbedTiming {
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0[kMaxSlices] = {}, ev1[kMaxSlices] = {};  // around each slice's L filter-step launches
+    int32_t slices = 0;
     int32_t launches = 0;
     bool valid = false;
 };
