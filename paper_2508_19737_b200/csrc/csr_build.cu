@@ -508,7 +508,8 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, cudaStream_t 
     c.n = n;
     igp_status st = cuda_status(alloc_async((void**)&c.row_ptr, sizeof(int32_t) * ((size_t)n + 1), s), "alloc");
     if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.order, sizeof(int32_t) * (size_t)n, s), "alloc");
-    if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 1), s), "alloc");
+    // rp_perm padded by 4 entries: 16-byte bulk copies of a row-pointer slice may overrun the end
+    if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 5), s), "alloc");
     auto fail = [&](igp_status e) {
         free_async(ws, s);
         free_async(c.row_ptr, s);
@@ -577,6 +578,7 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, cudaStream_t 
     inverse_perm_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n, inv, c.row_ptr, degp);
     IGP_STEP(launch_status("inverse_perm_kernel"));
     IGP_STEP(scan_exclusive(degp, c.rp_perm, n, s));
+    IGP_STEP(cuda_status(cudaMemsetAsync(c.rp_perm + n + 1, 0, 4 * sizeof(int32_t), s), "pad memset"));
     if (c.nnz > 0) {
         perm_scatter_kernel<<<rg, 256, 0, s>>>(c.order, inv, c.row_ptr, c.col_idx, c.rp_perm, c.col_perm, n);
         IGP_STEP(launch_status("perm_scatter_kernel"));

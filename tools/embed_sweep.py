@@ -11,7 +11,7 @@ from synth.dcsbm import CONFIGS, generate  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "headline"]
 widths = [int(w) for w in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["16", "32", "64"])]
-occs = [int(o) for o in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["3", "4"])]
+occs = [int(o) for o in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["3"])]
 edges, _ = generate(cfg)
 e = torch.from_numpy(edges).cuda()
 g = igp.build_graph(e, cfg.num_nodes)
