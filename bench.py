@@ -127,13 +127,14 @@ class ClockSampler:
 
 
 def load_traffic(config_name):
-    """Per-launch DRAM bytes of the filter-step kernel from a committed ncu --set full capture."""
+    """DRAM bytes (read + write) of one filter step, from the committed ncu --set full
+    capture of one slice launch (profiles/ncu_traffic.json) times the launches per step."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             t = json.load(f)
         v = t.get(config_name)
-        return None if v is None else float(v["dram_bytes_per_launch"])
+        return None if v is None else float(v["dram_bytes_per_launch"]) * int(v["launches_per_step"])
     except Exception:
         return None
 
@@ -278,19 +279,25 @@ def run_gpu(args, cfg):
     value, t_max = aggregate(per_ms, per_units)
     value /= 1e9
 
-    # roofline of the dominant kernel (filter step)
+    # roofline of the dominant kernel (the filter step).  One filter step over all d
+    # columns is d/W launches of layer_kernel<W> (column slices); the
+    # algorithmic bytes are those of the whole step (SURVEY.md §8(d) B_step), so
+    # achieved = B_step / (time of the d/W launches that make up one step).
     tot_layer_ms = sum(m for m, _ in layer_ms)
     tot_launches = sum(n for _, n in layer_ms)
-    avg_layer_s = tot_layer_ms / 1e3 / max(tot_launches, 1)
+    slices = max(1, tot_launches // max(1, L * len(layer_ms)))
+    width = d // slices
+    avg_launch_s = tot_layer_ms / 1e3 / max(tot_launches, 1)
+    step_s = avg_launch_s * slices
     b_step = step_bytes(N, nnz, d)
     peak, peak_src = hbm_peak()
-    achieved = b_step / avg_layer_s / 1e9
+    achieved = b_step / step_s / 1e9
+    traffic = load_traffic(cfg.name)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": load_traffic(cfg.name), "kernel": f"layer_kernel<{d}>",
-            "algorithmic_bytes_per_launch": b_step, "avg_launch_us": avg_layer_s * 1e6,
-            "peak_source": peak_src,
-            "l2_gather_bytes_per_launch": 4 * nnz * d,
-            "l2_gather_GBps": 4 * nnz * d / avg_layer_s / 1e9,
+            "traffic": traffic, "kernel": f"layer_kernel<{width}> x {slices} slice launches per filter step",
+            "per": "filter step (all d columns)", "algorithmic_bytes": b_step,
+            "step_us": step_s * 1e6, "avg_launch_us": avg_launch_s * 1e6, "peak_source": peak_src,
+            "gather_bytes_per_step": 4 * nnz * d, "gather_GBps": 4 * nnz * d / step_s / 1e9,
             "share_of_step": tot_layer_ms / ms_total}
 
     line = {"metric": "FFP embed throughput (GEdge·feat/s)", "value": value, "unit": "GEdge·feat/s",
