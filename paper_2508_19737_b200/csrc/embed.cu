@@ -44,6 +44,8 @@ constexpr int kFoldChunks = 4;  // fp32 partial sums span at most 64 neighbours
 constexpr int kBatch = 8;       // gathers issued back to back per lane (full chunks)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kDefaultOcc = 2;
+constexpr float kIdxEvictFirst = 1.0f;  // the index stream is read once per launch
+constexpr float kStoreEvictFirst = 1.0f;  // measured +2% (profiles/r01)
 
 __global__ void scale_kernel(const int32_t* __restrict__ rp, int32_t n, double tau, double eps,
                              float4* __restrict__ node) {
@@ -124,6 +126,8 @@ struct LayerArgs {
     float theta, alpha;
     int linear;
     double grid_c;  // 1.5 * 2^(52-g): (x + grid_c) - grid_c rounds x to the 2^-g grid
+    float idx_ef;   // fraction of index-stream loads marked L2 evict_first
+    float st_ef;    // fraction of output stores marked L2 evict_first
 };
 
 // (mu, 1/sigma) of column c from exact sums; population std (reading A2), floor 1e-8 -> 0 (A3)
@@ -151,18 +155,25 @@ __device__ __forceinline__ int2 ld_idx2(const int32_t* p) {
     asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
 }
-__device__ __forceinline__ int ld_idx1(const int32_t* p) {
+__device__ __forceinline__ int ld_idx1(const int32_t* p, uint64_t pol) {
     int v;
-    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
+}
+// L2 policy: a fraction `frac` of the accesses are marked evict_first, the rest unchanged
+__device__ __forceinline__ uint64_t evict_first_policy(float frac) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.L2::evict_unchanged.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+    return pol;
 }
 
 // 256-bit vector access (sm_100: LDG.256 / STG.256) and packed fp32 adds (FADD2)
 __device__ __forceinline__ void ldg256(const void* ptr, uint64_t (&v)[4]) {
     asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(ptr));
 }
-__device__ __forceinline__ void stg256(void* ptr, const uint64_t (&v)[4]) {
-    asm volatile("st.global.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3])
+__device__ __forceinline__ void stg256(void* ptr, const uint64_t (&v)[4], uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(ptr), "l"(v[0]), "l"(v[1]),
+                 "l"(v[2]), "l"(v[3]), "l"(pol)
                  : "memory");
 }
 __device__ __forceinline__ void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); }
@@ -183,11 +194,12 @@ __device__ __forceinline__ uint64_t pack2(float a, float b) {
 }
 
 template <int IPL>
-__device__ __forceinline__ void load_idx(const int32_t* ci, int32_t e0, int32_t end, int q, int (&jr)[IPL]) {
+__device__ __forceinline__ void load_idx(const int32_t* ci, int32_t e0, int32_t end, int q, uint64_t pol,
+                                         int (&jr)[IPL]) {
 #pragma unroll
     for (int k = 0; k < IPL; ++k) {
         const int32_t e = e0 + q * IPL + k;
-        jr[k] = e < end ? ld_idx1(ci + e) : 0;
+        jr[k] = e < end ? ld_idx1(ci + e, pol) : 0;
     }
 }
 
@@ -227,6 +239,8 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
     const uint64_t* yin = reinterpret_cast<const uint64_t*>(p.yin);  // row j, lane q: yin + (j*LPR + q)*4
     uint64_t* yout = reinterpret_cast<uint64_t*>(p.yout);
     float* tile = stage[warp];
+    const uint64_t pol_idx = evict_first_policy(p.idx_ef);
+    const uint64_t pol_st = evict_first_policy(p.st_ef);
     const int oc0 = W >= 32 ? lane * OC : lane / 2;  // owned statistics columns / rows
     const int or0 = W >= 32 ? 0 : (lane & 1) * OR;
     double s1[OC], s2[OC];
@@ -251,11 +265,11 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
             bool folded = false;
             double* af = acc_f[grp] + 8 * q;
             int jr[IPL];
-            load_idx<IPL>(p.ci, beg, end, q, jr);
+            load_idx<IPL>(p.ci, beg, end, q, pol_idx, jr);
             for (int32_t e0 = beg; e0 < end; e0 += kChunk) {
                 const int32_t e1 = e0 + kChunk;
                 int jn[IPL];
-                load_idx<IPL>(p.ci, e1, end, q, jn);  // prefetch the next chunk's indices
+                load_idx<IPL>(p.ci, e1, end, q, pol_idx, jn);  // prefetch the next chunk's indices
                 const int cnt = end - e0;             // >= 1; the chunk is full when >= kChunk
                 if (cnt >= kChunk) {
                     // issue kBatch gathers before consuming any, so kBatch x 32 B per lane are in flight
@@ -334,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
                 }
                 o[k] = pack2(yy[0], yy[1]);
             }
-            stg256(yout + ((size_t)row * LPR + q) * 4, o);
+            stg256(yout + ((size_t)row * LPR + q) * 4, o, pol_st);
         }
         if (!p.linear) {
             // stage the warp's G x W tile of t (invalid rows contribute 0) and fold owned columns
@@ -508,6 +522,10 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     const int gexp = 51 - lg;
     const double grid_c = 1.5 * ldexp(1.0, 52 - gexp);
 
+    float idx_ef = kIdxEvictFirst, st_ef = kStoreEvictFirst;  // L2 policies (development knobs)
+    if (const char* e = getenv("IGP_IDX_EF")) idx_ef = (float)atof(e);
+    if (const char* e = getenv("IGP_ST_EF")) st_ef = (float)atof(e);
+
     igp_status rc = IGP_OK;
     const bool timed = (o.flags & IGP_FLAG_TIME_LAYERS) && timing;
     do {
@@ -544,6 +562,8 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 a.alpha = o.alpha;
                 a.linear = linear;
                 a.grid_c = grid_c;
+                a.idx_ef = idx_ef;
+                a.st_ef = st_ef;
                 layer_kernel<W, MB><<<grid, kThreads, layer_smem<W>(), s>>>(a);
                 if ((rc = launch_status("layer_kernel")) != IGP_OK) break;
             }

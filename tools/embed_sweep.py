@@ -11,17 +11,22 @@ from synth.dcsbm import CONFIGS, generate  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "headline"]
 widths = [int(w) for w in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["16", "32", "64"])]
-occs = [int(o) for o in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["3"])]
+occs = [int(o) for o in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["2"])]
+envs = [kv for kv in (sys.argv[4].split(";") if len(sys.argv) > 4 else [""])]
 edges, _ = generate(cfg)
 e = torch.from_numpy(edges).cuda()
 g = igp.build_graph(e, cfg.num_nodes)
 out = torch.empty((cfg.num_nodes, cfg.d), device="cuda")
 ref = None
-for w, occ in [(w, o) for w in widths for o in occs]:
+for w, occ, env in [(w, o, e) for w in widths for o in occs for e in envs]:
     if w > cfg.d:
         continue
     os.environ["IGP_SLICE_WIDTH"] = str(w)
     os.environ["IGP_LAYER_OCC"] = str(occ)
+    for kv in env.split(","):
+        if "=" in kv:
+            k, v = kv.split("=")
+            os.environ[k] = v
     for _ in range(2):
         igp.embed(g, cfg.tau, cfg.d, cfg.steps, 0, out=out)
     torch.cuda.synchronize()
@@ -41,6 +46,6 @@ for w, occ in [(w, o) for w in widths for o in occs]:
         ref = out.clone()
     diff = float((out - ref).abs().max())
     units = g.nnz * cfg.d * cfg.steps
-    print(f"{cfg.name} W={w:3d} occ={occ}: embed {ms:8.2f} ms  {units / ms / 1e6:8.1f} GEdge-feat/s  "
+    print(f"{cfg.name} W={w:3d} occ={occ} {env:28s}: embed {ms:8.2f} ms  {units / ms / 1e6:8.1f} GEdge-feat/s  "
           f"filter launches {nl} avg {lms / nl * 1e3:8.1f} us (per full step {lms / cfg.steps:7.3f} ms)  "
           f"max|diff vs first W| {diff:.2e}", flush=True)
