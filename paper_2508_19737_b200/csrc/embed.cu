@@ -253,66 +253,80 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
         const int32_t row = (int32_t)(base + g);
         const bool valid = row < p.n;
         float t8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        int32_t beg = 0, end = 0;
+        const uint64_t* own_ptr = yin + ((size_t)row * LPR + q) * 4;
         if (valid) {
-            const int32_t beg = __ldg(p.rp + row), end = __ldg(p.rp + row + 1);
-            const uint64_t* own_ptr = yin + ((size_t)row * LPR + q) * 4;
+            beg = __ldg(p.rp + row);
+            end = __ldg(p.rp + row + 1);
             prefetch_l2(own_ptr);  // the row's own values are needed only after its gathers
             prefetch_l2(p.node + row);
-            // neighbour sum: packed fp32 within up to kFoldChunks chunks, then folded into
-            // fp64 partials in shared memory (only rows longer than 64 neighbours fold)
-            uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-            int nc = 0;
-            bool folded = false;
-            double* af = acc_f[grp] + 8 * q;
-            int jr[IPL];
-            load_idx<IPL>(p.ci, beg, end, q, pol_idx, jr);
-            for (int32_t e0 = beg; e0 < end; e0 += kChunk) {
-                const int32_t e1 = e0 + kChunk;
-                int jn[IPL];
-                load_idx<IPL>(p.ci, e1, end, q, pol_idx, jn);  // prefetch the next chunk's indices
-                const int cnt = end - e0;             // >= 1; the chunk is full when >= kChunk
-                if (cnt >= kChunk) {
-                    // issue kBatch gathers before consuming any, so kBatch x 32 B per lane are in flight
+        }
+        // neighbour sum: packed fp32 within up to kFoldChunks chunks, then folded into
+        // fp64 partials in shared memory (only rows longer than 64 neighbours fold).
+        // The chunk loop is warp-uniform (the warp's rows have similar degrees), so the
+        // index broadcasts are full-warp shuffles and fully-populated chunks run unpredicated.
+        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+        int nc = 0;
+        bool folded = false;
+        double* af = acc_f[grp] + 8 * q;
+        const int nch = (end - beg + kChunk - 1) / kChunk;
+        const int max_nch = __reduce_max_sync(kFull, nch);
+        int jr[IPL];
+        load_idx<IPL>(p.ci, beg, end, q, pol_idx, jr);
+        for (int c = 0; c < max_nch; ++c) {
+            const int32_t e0 = beg + c * kChunk, e1 = e0 + kChunk;
+            int jn[IPL];
+            load_idx<IPL>(p.ci, e1, end, q, pol_idx, jn);  // prefetch the next chunk's indices
+            int cnt = end - e0;
+            cnt = cnt < 0 ? 0 : (cnt > kChunk ? kChunk : cnt);
+            if (__all_sync(kFull, cnt == kChunk)) {
+                // issue kBatch gathers before consuming any, so kBatch x 32 B per lane are in flight
 #pragma unroll
-                    for (int u0 = 0; u0 < kChunk; u0 += kBatch) {
-                        uint64_t v[kBatch][4];
+                for (int u0 = 0; u0 < kChunk; u0 += kBatch) {
+                    uint64_t v[kBatch][4];
 #pragma unroll
-                        for (int t = 0; t < kBatch; ++t) {
-                            const int u = u0 + t;
-                            const int j = __shfl_sync(gmask, jr[u % IPL], u / IPL, LPR);
-                            ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
-                        }
-#pragma unroll
-                        for (int t = 0; t < kBatch; ++t)
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[t][k]);
+                    for (int t = 0; t < kBatch; ++t) {
+                        const int u = u0 + t;
+                        const int j = __shfl_sync(kFull, jr[u % IPL], u / IPL, LPR);
+                        ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
                     }
-                } else {
 #pragma unroll
-                    for (int u = 0; u < kChunk; ++u) {
-                        const int j = __shfl_sync(gmask, jr[u % IPL], u / IPL, LPR);
-                        if (u < cnt) {
-                            uint64_t v[4];
-                            ldg256(yin + ((size_t)j * LPR + q) * 4, v);
+                    for (int t = 0; t < kBatch; ++t)
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[k]);
-                        }
-                    }
+                        for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[t][k]);
                 }
-                if (++nc == kFoldChunks && e1 < end) {
+            } else {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const float2 f = unpack2(acc[k]);
-                        af[2 * k] += (double)f.x;
-                        af[2 * k + 1] += (double)f.y;
-                        acc[k] = 0ull;
+                for (int u0 = 0; u0 < kChunk; u0 += kBatch) {
+                    uint64_t v[kBatch][4];
+#pragma unroll
+                    for (int t = 0; t < kBatch; ++t) {
+                        const int u = u0 + t;
+                        const int j = __shfl_sync(kFull, jr[u % IPL], u / IPL, LPR);
+                        v[t][0] = v[t][1] = v[t][2] = v[t][3] = 0ull;
+                        if (u < cnt) ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
                     }
-                    nc = 0;
-                    folded = true;
-                }
 #pragma unroll
-                for (int k = 0; k < IPL; ++k) jr[k] = jn[k];
+                    for (int t = 0; t < kBatch; ++t)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[t][k]);
+                }
             }
+            if (++nc == kFoldChunks && e1 < end) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float2 f = unpack2(acc[k]);
+                    af[2 * k] += (double)f.x;
+                    af[2 * k + 1] += (double)f.y;
+                    acc[k] = 0ull;
+                }
+                nc = 0;
+                folded = true;
+            }
+#pragma unroll
+            for (int k = 0; k < IPL; ++k) jr[k] = jn[k];
+        }
+        if (valid) {
             double ad[8];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
