@@ -193,13 +193,42 @@ __device__ __forceinline__ uint64_t pack2(float a, float b) {
     return v;
 }
 
+__device__ __forceinline__ int4 ld_idx4h(const int32_t* p, uint64_t pol) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int2 ld_idx2h(const int32_t* p, uint64_t pol) {
+    int2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+// indices [e0 + q*IPL, e0 + (q+1)*IPL) of an aligned chunk (e0 % 4 == 0); the col arrays are
+// padded, so a chunk may run past the row (those slots are masked by the caller)
 template <int IPL>
 __device__ __forceinline__ void load_idx(const int32_t* ci, int32_t e0, int32_t end, int q, uint64_t pol,
                                          int (&jr)[IPL]) {
+    const int32_t e = e0 + q * IPL;
+    if (e >= end) {
 #pragma unroll
-    for (int k = 0; k < IPL; ++k) {
-        const int32_t e = e0 + q * IPL + k;
-        jr[k] = e < end ? ld_idx1(ci + e, pol) : 0;
+        for (int k = 0; k < IPL; ++k) jr[k] = 0;
+        return;
+    }
+    if constexpr (IPL >= 4) {
+#pragma unroll
+        for (int k = 0; k < IPL; k += 4) {
+            const int4 v = ld_idx4h(ci + e + k, pol);
+            jr[k] = v.x, jr[k + 1] = v.y, jr[k + 2] = v.z, jr[k + 3] = v.w;
+        }
+    } else if constexpr (IPL == 2) {
+        const int2 v = ld_idx2h(ci + e, pol);
+        jr[0] = v.x, jr[1] = v.y;
+    } else {
+        jr[0] = ld_idx1(ci + e, pol);
     }
 }
 
@@ -269,17 +298,20 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
         int nc = 0;
         bool folded = false;
         double* af = acc_f[grp] + 8 * q;
-        const int nch = (end - beg + kChunk - 1) / kChunk;
+        // chunks start 16-byte aligned (vector index loads); slots outside [beg, end) are masked
+        const int32_t start = beg & ~3;
+        const int nch = end > beg ? (end - start + kChunk - 1) / kChunk : 0;
         const int max_nch = __reduce_max_sync(kFull, nch);
         int jr[IPL];
-        load_idx<IPL>(p.ci, beg, end, q, pol_idx, jr);
+        load_idx<IPL>(p.ci, start, end, q, pol_idx, jr);
         for (int c = 0; c < max_nch; ++c) {
-            const int32_t e0 = beg + c * kChunk, e1 = e0 + kChunk;
+            const int32_t e0 = start + c * kChunk, e1 = e0 + kChunk;
             int jn[IPL];
             load_idx<IPL>(p.ci, e1, end, q, pol_idx, jn);  // prefetch the next chunk's indices
-            int cnt = end - e0;
-            cnt = cnt < 0 ? 0 : (cnt > kChunk ? kChunk : cnt);
-            if (__all_sync(kFull, cnt == kChunk)) {
+            const int lo = beg > e0 ? beg - e0 : 0;        // valid slots of this chunk: [lo, hi)
+            int hi = end - e0;
+            hi = hi < 0 ? 0 : (hi > kChunk ? kChunk : hi);
+            if (__all_sync(kFull, lo == 0 && hi == kChunk)) {
                 // issue kBatch gathers before consuming any, so kBatch x 32 B per lane are in flight
 #pragma unroll
                 for (int u0 = 0; u0 < kChunk; u0 += kBatch) {
@@ -304,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
                         const int u = u0 + t;
                         const int j = __shfl_sync(kFull, jr[u % IPL], u / IPL, LPR);
                         v[t][0] = v[t][1] = v[t][2] = v[t][3] = 0ull;
-                        if (u < cnt) ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
+                        if (u >= lo && u < hi) ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
                     }
 #pragma unroll
                     for (int t = 0; t < kBatch; ++t)
