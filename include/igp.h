@@ -78,6 +78,17 @@ typedef enum {
 IGP_API igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes,
                            igp_stream_t stream, igp_graph_t* out);
 
+#define IGP_BUILD_DEFAULT 0u
+#define IGP_BUILD_NO_REORDER 1u /* keep the original node order for the filter steps (no degree-sorted
+                                   relabelling; results differ only by fp32 summation order) */
+
+/* As igp_build_graph; `flags` selects the filter steps' row order.  By default the
+ * handle also holds a relabelled copy of the CSR with rows by descending degree (ties by
+ * ascending id), which the embed kernels traverse; IGP_BUILD_NO_REORDER skips it.  Unknown
+ * flags -> IGP_ERR_INPUT. */
+IGP_API igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes, uint32_t flags,
+                                      igp_stream_t stream, igp_graph_t* out);
+
 /* Query a graph: N, nnz = 2M (directed CSR entries) and M.  Any output pointer may be NULL. */
 IGP_API igp_status igp_graph_info(igp_graph_t g, int32_t* num_nodes, int64_t* nnz, int64_t* num_undirected_edges);
 

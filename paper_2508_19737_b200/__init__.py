@@ -49,6 +49,7 @@ class EmbedOpts(ctypes.Structure):
 _P, _i32, _i64, _u64, _f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
 SIGNATURES = {
     "igp_build_graph": (ctypes.c_int, [_P, _i64, _i32, _P, ctypes.POINTER(_P)]),
+    "igp_build_graph_ex": (ctypes.c_int, [_P, _i64, _i32, ctypes.c_uint32, _P, ctypes.POINTER(_P)]),
     "igp_graph_info": (ctypes.c_int, [_P, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "igp_graph_copy_csr": (ctypes.c_int, [_P, _P, _P, _P]),
     "igp_destroy_graph": (ctypes.c_int, [_P]),
@@ -66,7 +67,7 @@ SIGNATURES = {
 }
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2508_19737_b200._build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2508_19737_b200/_build.py` "
                       "(there is no CPU fallback)")
 _lib = ctypes.CDLL(LIB_PATH)
 for _name, (_res, _args) in SIGNATURES.items():
@@ -144,17 +145,21 @@ class Graph:
         self.close()
 
 
-def build_graph(edges: torch.Tensor, num_nodes: int, stream=None) -> Graph:
-    """igp_build_graph: canonical CSR of the undirected simple graph.
+BUILD_NO_REORDER = 1
 
-    ``edges``: CUDA int32 tensor [E, 2] (duplicates / both orientations / self loops allowed)."""
+
+def build_graph(edges: torch.Tensor, num_nodes: int, stream=None, reorder: bool = True) -> Graph:
+    """igp_build_graph_ex: canonical CSR of the undirected simple graph.
+
+    ``edges``: CUDA int32 tensor [E, 2] (duplicates / both orientations / self loops allowed).
+    ``reorder=False`` keeps the original row order for the filter steps (IGP_BUILD_NO_REORDER)."""
     _require_cuda(edges, torch.int32, "edges")
     if edges.dim() != 2 or edges.shape[1] != 2:
         raise ValueError("edges must have shape [E, 2]")
     h = _P()
     with torch.cuda.device(edges.device):
-        _check(_lib.igp_build_graph(ctypes.c_void_p(edges.data_ptr()), edges.shape[0], int(num_nodes),
-                                    _stream_ptr(stream), ctypes.byref(h)))
+        _check(_lib.igp_build_graph_ex(ctypes.c_void_p(edges.data_ptr()), edges.shape[0], int(num_nodes),
+                                       0 if reorder else BUILD_NO_REORDER, _stream_ptr(stream), ctypes.byref(h)))
     return Graph(h, edges.device)
 
 

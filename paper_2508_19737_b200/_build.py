@@ -1,6 +1,6 @@
 """Build libigp.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension).
 
-    python -m paper_2508_19737_b200._build
+    python paper_2508_19737_b200/_build.py      (not -m: importing the package loads libigp.so)
 """
 from __future__ import annotations
 

@@ -468,7 +468,12 @@ igp_status segmented_sort(const int32_t* off, int32_t* data, int32_t* ucnt, int3
 
 }  // namespace
 
-igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, cudaStream_t s, CsrDevice* out) {
+__global__ void iota_kernel(int32_t* __restrict__ a, int32_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) a[i] = (int32_t)i;
+}
+
+igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder, cudaStream_t s, CsrDevice* out) {
     DeviceInfo di;
     if (!device_info(&di)) return IGP_ERR_CUDA;
     const int64_t raw = 2 * E;  // both orientations, before dedup / self-loop removal
@@ -509,14 +514,17 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, cudaStream_t 
     igp_status st = cuda_status(alloc_async((void**)&c.row_ptr, sizeof(int32_t) * ((size_t)n + 1), s), "alloc");
     if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.order, sizeof(int32_t) * (size_t)n, s), "alloc");
     // rp_perm padded by 4 entries: 16-byte bulk copies of a row-pointer slice may overrun the end
-    if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 5), s), "alloc");
+    if (st == IGP_OK && reorder)
+        st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 5), s), "alloc");
     auto fail = [&](igp_status e) {
         free_async(ws, s);
         free_async(c.row_ptr, s);
         free_async(c.order, s);
-        free_async(c.rp_perm, s);
         free_async(c.col_idx, s);
-        free_async(c.col_perm, s);
+        if (reorder) {
+            free_async(c.rp_perm, s);
+            free_async(c.col_perm, s);
+        }
         return e;
     };
     if (st != IGP_OK) return fail(st);
@@ -542,16 +550,21 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, cudaStream_t 
     // B4-B5: per-row sort + dedup, row pointers
     IGP_STEP(segmented_sort(off, tmp, ucnt, n, E, n, sc, s, di));
     IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
-    // B6a: degree-descending order (counting sort by degree, then ascending id per bucket)
-    IGP_STEP(cuda_status(cudaMemsetAsync(hist, 0, sizeof(int32_t) * kDegBuckets, s), "memset"));
-    degree_hist_kernel<<<grid_for(n, 256, di.num_sms, 4), 256, 0, s>>>(c.row_ptr, n, hist);
-    IGP_STEP(launch_status("degree_hist_kernel"));
-    IGP_STEP(scan_exclusive(hist, boff, kDegBuckets, s));
-    IGP_STEP(cuda_status(cudaMemcpyAsync(fill, boff, sizeof(int32_t) * (kDegBuckets + 1), cudaMemcpyDeviceToDevice, s),
-                         "copy"));
-    degree_scatter_kernel<<<(n + kSchedTile - 1) / kSchedTile, 256, 0, s>>>(c.row_ptr, n, fill, c.order);
-    IGP_STEP(launch_status("degree_scatter_kernel"));
-    IGP_STEP(segmented_sort(boff, c.order, hist, kDegBuckets, n, n, sc, s, di));
+    if (reorder) {
+        // B6a: degree-descending order (counting sort by degree, then ascending id per bucket)
+        IGP_STEP(cuda_status(cudaMemsetAsync(hist, 0, sizeof(int32_t) * kDegBuckets, s), "memset"));
+        degree_hist_kernel<<<grid_for(n, 256, di.num_sms, 4), 256, 0, s>>>(c.row_ptr, n, hist);
+        IGP_STEP(launch_status("degree_hist_kernel"));
+        IGP_STEP(scan_exclusive(hist, boff, kDegBuckets, s));
+        IGP_STEP(cuda_status(
+            cudaMemcpyAsync(fill, boff, sizeof(int32_t) * (kDegBuckets + 1), cudaMemcpyDeviceToDevice, s), "copy"));
+        degree_scatter_kernel<<<(n + kSchedTile - 1) / kSchedTile, 256, 0, s>>>(c.row_ptr, n, fill, c.order);
+        IGP_STEP(launch_status("degree_scatter_kernel"));
+        IGP_STEP(segmented_sort(boff, c.order, hist, kDegBuckets, n, n, sc, s, di));
+    } else {
+        iota_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n);  // identity labelling
+        IGP_STEP(launch_status("iota_kernel"));
+    }
     // the build's single host synchronisation: nnz and the error flag
     int32_t host_vals[2] = {0, 0};
     IGP_STEP(cuda_status(cudaMemcpyAsync(&host_vals[0], c.row_ptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
@@ -566,13 +579,22 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, cudaStream_t 
     c.nnz = host_vals[0];
     const size_t cbytes = sizeof(int32_t) * (size_t)(c.nnz + kColPad);
     IGP_STEP(cuda_status(alloc_async((void**)&c.col_idx, cbytes, s), "col_idx alloc"));
-    IGP_STEP(cuda_status(alloc_async((void**)&c.col_perm, cbytes, s), "col_perm alloc"));
+    if (reorder) IGP_STEP(cuda_status(alloc_async((void**)&c.col_perm, cbytes, s), "col_perm alloc"));
     IGP_STEP(cuda_status(cudaMemsetAsync(c.col_idx + c.nnz, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
-    IGP_STEP(cuda_status(cudaMemsetAsync(c.col_perm + c.nnz, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
+    if (reorder)
+        IGP_STEP(cuda_status(cudaMemsetAsync(c.col_perm + c.nnz, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
     const int rg = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
     if (c.nnz > 0) {
         compact_kernel<<<rg, 256, 0, s>>>(off, tmp, c.row_ptr, c.col_idx, n);
         IGP_STEP(launch_status("compact_kernel"));
+    }
+    if (!reorder) {  // the filter steps run on the canonical CSR itself
+        c.rp_perm = c.row_ptr;
+        c.col_perm = c.col_idx;
+        c.perm_alias = true;
+        free_async(ws, s);
+        *out = c;
+        return IGP_OK;
     }
     // B6b: the relabelled CSR the filter steps run on (rows by descending degree)
     inverse_perm_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n, inv, c.row_ptr, degp);

@@ -118,7 +118,17 @@ uint64_t igp_kernel_launch_count(void) { return g_launches.load(); }
 
 igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes, igp_stream_t stream,
                            igp_graph_t* out) {
+    return igp_build_graph_ex(d_edges, num_edges, num_nodes, IGP_BUILD_DEFAULT, stream, out);
+}
+
+igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes, uint32_t flags,
+                              igp_stream_t stream, igp_graph_t* out) {
     set_error("");
+    if (flags & ~(uint32_t)IGP_BUILD_NO_REORDER) {
+        if (out) *out = nullptr;
+        set_error("unknown build flags");
+        return IGP_ERR_INPUT;
+    }
     if (!out) {
         set_error("out handle pointer is NULL");
         return IGP_ERR_INPUT;
@@ -138,7 +148,8 @@ igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, int32_t nu
     }
     igp_graph_s* g = new (std::nothrow) igp_graph_s();
     if (!g) return IGP_ERR_OOM;
-    igp_status st = build_csr(d_edges, num_edges, num_nodes, (cudaStream_t)stream, &g->csr);
+    igp_status st = build_csr(d_edges, num_edges, num_nodes, (flags & IGP_BUILD_NO_REORDER) == 0,
+                              (cudaStream_t)stream, &g->csr);
     if (st != IGP_OK) {
         delete g;
         return st;
@@ -180,8 +191,10 @@ static void release_graph(igp_graph_t g, cudaStream_t s) {
     free_async(g->csr.row_ptr, s);
     free_async(g->csr.col_idx, s);
     free_async(g->csr.order, s);
-    free_async(g->csr.rp_perm, s);
-    free_async(g->csr.col_perm, s);
+    if (!g->csr.perm_alias) {
+        free_async(g->csr.rp_perm, s);
+        free_async(g->csr.col_perm, s);
+    }
     for (int k = 0; k < kMaxSlices; ++k) {
         if (g->timing.ev0[k]) cudaEventDestroy(g->timing.ev0[k]);
         if (g->timing.ev1[k]) cudaEventDestroy(g->timing.ev1[k]);

@@ -62,11 +62,12 @@ struct CsrDevice {
     int32_t* order = nullptr;    // [N] order[r] = original id of relabelled row r (descending degree)
     int32_t* rp_perm = nullptr;  // [N+1] CSR of the relabelled graph (row r = node order[r]) ...
     int32_t* col_perm = nullptr; // [nnz + kColPad]  ... with relabelled, ascending column ids
+    bool perm_alias = false;     // no relabelling: rp_perm/col_perm alias row_ptr/col_idx, order = identity
     int32_t n = 0;
     int64_t nnz = 0;
 };
 constexpr int kColPad = 16;
-igp_status build_csr(const int32_t* d_edges, int64_t num_edges, int32_t n, cudaStream_t s,
+igp_status build_csr(const int32_t* d_edges, int64_t num_edges, int32_t n, bool reorder, cudaStream_t s,
                      CsrDevice* out);
 
 // exclusive scan of n int32 counts: out[0..n], out[n] = total (int32 range checked by caller)

@@ -20,8 +20,8 @@ def declared_symbols():
 
 @pytest.fixture(scope="module")
 def igp():
-    from paper_2508_19737_b200 import _build
-    _build.build()
+    import __graft_entry__
+    __graft_entry__.build()
     import paper_2508_19737_b200 as m
     return m
 

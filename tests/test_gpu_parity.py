@@ -255,3 +255,34 @@ def test_headline_full_steps_properties(igp, headline):
     assert torch.allclose(pre.mean(0), torch.zeros(c.d, dtype=torch.float64, device=pre.device), atol=1e-4)
     assert torch.allclose(pre.std(0, unbiased=False), torch.ones(c.d, dtype=torch.float64, device=pre.device),
                           atol=1e-4)
+
+
+# ------------------------------------------------------------------ row order (IGP_BUILD_NO_REORDER)
+@pytest.mark.parametrize("cfg", ["tiny", "medium"])
+def test_embed_without_relabelling(igp, cfg):
+    """The filter steps on the original row order (no degree-sorted relabelling) meet the
+    same bar; the two orders differ only by fp32 summation order."""
+    c = CONFIGS[cfg]
+    edges, _ = generate(c)
+    e = torch.from_numpy(edges).cuda()
+    g0 = igp.build_graph(e, c.num_nodes, reorder=False)
+    g1 = igp.build_graph(e, c.num_nodes)
+    rp0, ci0 = g0.csr()
+    rp1, ci1 = g1.csr()
+    assert torch.equal(rp0, rp1) and torch.equal(ci0, ci1)  # the canonical CSR is the same
+    z0 = igp.embed(g0, c.tau, c.d, c.steps, 0).cpu().numpy()
+    z1 = igp.embed(g1, c.tau, c.d, c.steps, 0).cpu().numpy()
+    rp, ci, _ = oracle.build_csr(edges, c.num_nodes)
+    ref = oracle.embed(rp, ci, c.num_nodes, c.d, c.steps, c.tau, seed=0, nthreads=NTHREADS)
+    err0 = row_rel_err(z0, ref)
+    record(f"{cfg}_no_reorder", err0)
+    assert err0 <= TOL
+    assert row_rel_err(z0, z1) <= TOL
+
+
+def test_build_flags_rejected(igp):
+    import ctypes
+    h = ctypes.c_void_p()
+    e = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+    st = igp.lib().igp_build_graph_ex(ctypes.c_void_p(e.data_ptr()), 1, 2, 0x80, None, ctypes.byref(h))
+    assert st == 2
