@@ -89,6 +89,14 @@ IGP_API igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, in
 IGP_API igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes, uint32_t flags,
                                       igp_stream_t stream, igp_graph_t* out);
 
+/* Streaming update (Alg. 2 l.1): merge a batch of new edges (same rules as
+ * igp_build_graph, node ids in [0, N)) into the graph in place, on the device: the result
+ * is the canonical CSR of the union, as if built from all edges at once, with the row
+ * order (relabelling) recomputed.  One host sync; the previous CSR is released in stream
+ * order.  On error the graph is unchanged.  Not safe concurrently with an embed of g. */
+IGP_API igp_status igp_graph_add_edges(igp_graph_t g, const int32_t* d_edges, int64_t num_edges,
+                                       igp_stream_t stream);
+
 /* Query a graph: N, nnz = 2M (directed CSR entries) and M.  Any output pointer may be NULL. */
 IGP_API igp_status igp_graph_info(igp_graph_t g, int32_t* num_nodes, int64_t* nnz, int64_t* num_undirected_edges);
 

@@ -50,6 +50,7 @@ _P, _i32, _i64, _u64, _f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ct
 SIGNATURES = {
     "igp_build_graph": (ctypes.c_int, [_P, _i64, _i32, _P, ctypes.POINTER(_P)]),
     "igp_build_graph_ex": (ctypes.c_int, [_P, _i64, _i32, ctypes.c_uint32, _P, ctypes.POINTER(_P)]),
+    "igp_graph_add_edges": (ctypes.c_int, [_P, _P, _i64, _P]),
     "igp_graph_info": (ctypes.c_int, [_P, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "igp_graph_copy_csr": (ctypes.c_int, [_P, _P, _P, _P]),
     "igp_destroy_graph": (ctypes.c_int, [_P]),
@@ -121,6 +122,17 @@ class Graph:
         _check(_lib.igp_graph_copy_csr(self.handle, ctypes.c_void_p(rp.data_ptr()), ctypes.c_void_p(ci.data_ptr()),
                                        _stream_ptr(stream)))
         return rp, ci[: self.nnz]
+
+    def add_edges(self, edges: torch.Tensor, stream=None):
+        """igp_graph_add_edges: merge new edges (CUDA int32 [E, 2]) into this graph in place."""
+        _require_cuda(edges, torch.int32, "edges")
+        with torch.cuda.device(self.device):
+            _check(_lib.igp_graph_add_edges(self.handle, ctypes.c_void_p(edges.data_ptr()), edges.shape[0],
+                                            _stream_ptr(stream)))
+        n, nnz, m = _i32(), _i64(), _i64()
+        _check(_lib.igp_graph_info(self.handle, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(m)))
+        self.nnz, self.num_edges = nnz.value, m.value
+        return self
 
     def last_layer_time_ms(self):
         ms, n = _f32(), _i32()

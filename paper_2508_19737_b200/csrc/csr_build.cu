@@ -468,15 +468,38 @@ igp_status segmented_sort(const int32_t* off, int32_t* data, int32_t* ucnt, int3
 
 }  // namespace
 
+// merge support: row counts start at the base graph's degrees, and the base rows are
+// copied into the front of each bucket before the new edges are scattered behind them
+__global__ void base_degree_kernel(const int32_t* __restrict__ rp, int32_t n, int32_t* __restrict__ cnt) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) cnt[i] = rp[i + 1] - rp[i];
+}
+
+__global__ void base_copy_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, int32_t n,
+                                 const int32_t* __restrict__ off, int32_t* __restrict__ tmp) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
+        const int32_t src = rp[r], len = rp[r + 1] - src, dst = off[r];
+        for (int32_t k = lane; k < len; k += 32) tmp[dst + k] = ci[src + k];
+    }
+}
+
 __global__ void iota_kernel(int32_t* __restrict__ a, int32_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) a[i] = (int32_t)i;
 }
 
-igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder, cudaStream_t s, CsrDevice* out) {
+igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder, cudaStream_t s, CsrDevice* out,
+                     const CsrDevice* base) {
     DeviceInfo di;
     if (!device_info(&di)) return IGP_ERR_CUDA;
-    const int64_t raw = 2 * E;  // both orientations, before dedup / self-loop removal
+    // both orientations of the new edges (before dedup / self-loop removal), plus the base rows
+    const int64_t raw = 2 * E + (base ? base->nnz : 0);
+    if (raw > (int64_t)INT32_MAX) {
+        set_error("edge count exceeds the int32 CSR index range");
+        return IGP_ERR_UNSUPPORTED;
+    }
     const int32_t words = (n + 31) >> 5;
     const int32_t lists = n > kDegBuckets ? n : kDegBuckets;
     // temporaries in one stream-ordered block
@@ -533,22 +556,35 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder,
         igp_status _s = (expr);                         \
         if (_s != IGP_OK) return fail(_s);              \
     } while (0)
-    IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
     IGP_STEP(cuda_status(cudaMemsetAsync(flags, 0, 4 * sizeof(int32_t), s), "memset"));
-    // B1-B3: count, scan, scatter both orientations into row buckets
+    // B1-B3: count, scan, scatter both orientations into row buckets (behind the base rows)
+    if (base) {
+        base_degree_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(base->row_ptr, n, cnt);
+        IGP_STEP(launch_status("base_degree_kernel"));
+    } else {
+        IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
+    }
     const int eg = grid_for(E, 256, di.num_sms, 16);
     if (E > 0) {
         count_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, cnt, flags);
         IGP_STEP(launch_status("count_kernel"));
     }
     IGP_STEP(scan_exclusive(cnt, off, n, s));
-    if (E > 0) {
+    const int rg0 = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
+    if (base) {
+        base_copy_kernel<<<rg0, 256, 0, s>>>(base->row_ptr, base->col_idx, n, off, tmp);
+        IGP_STEP(launch_status("base_copy_kernel"));
+        base_degree_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(base->row_ptr, n, cnt);
+        IGP_STEP(launch_status("base_degree_kernel"));
+    } else if (E > 0) {
         IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
+    }
+    if (E > 0) {
         scatter_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, off, cnt, tmp);
         IGP_STEP(launch_status("scatter_kernel"));
     }
     // B4-B5: per-row sort + dedup, row pointers
-    IGP_STEP(segmented_sort(off, tmp, ucnt, n, E, n, sc, s, di));
+    IGP_STEP(segmented_sort(off, tmp, ucnt, n, raw, n, sc, s, di));
     IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
     if (reorder) {
         // B6a: degree-descending order (counting sort by degree, then ascending id per bucket)
@@ -604,7 +640,7 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder,
     if (c.nnz > 0) {
         perm_scatter_kernel<<<rg, 256, 0, s>>>(c.order, inv, c.row_ptr, c.col_idx, c.rp_perm, c.col_perm, n);
         IGP_STEP(launch_status("perm_scatter_kernel"));
-        IGP_STEP(segmented_sort(c.rp_perm, c.col_perm, ucnt, n, E, n, sc, s, di));
+        IGP_STEP(segmented_sort(c.rp_perm, c.col_perm, ucnt, n, raw, n, sc, s, di));
     }
 #undef IGP_STEP
     free_async(ws, s);

@@ -142,7 +142,7 @@ igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t
         set_error("num_edges must be >= 0 and d_edges non-NULL when num_edges > 0");
         return IGP_ERR_INPUT;
     }
-    if (2 * num_edges > (int64_t)INT32_MAX) {
+    if (num_edges > (int64_t)INT32_MAX / 2) {
         set_error("2*num_edges exceeds the int32 CSR index range");
         return IGP_ERR_UNSUPPORTED;
     }
@@ -155,7 +155,35 @@ igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t
         return st;
     }
     g->m = g->csr.nnz / 2;
+    g->reorder = (flags & IGP_BUILD_NO_REORDER) == 0;
     *out = g;
+    return IGP_OK;
+}
+
+igp_status igp_graph_add_edges(igp_graph_t g, const int32_t* d_edges, int64_t num_edges, igp_stream_t stream) {
+    set_error("");
+    if (!g) {
+        set_error("graph is NULL");
+        return IGP_ERR_INPUT;
+    }
+    if (num_edges < 0 || (num_edges > 0 && !d_edges)) {
+        set_error("num_edges must be >= 0 and d_edges non-NULL when num_edges > 0");
+        return IGP_ERR_INPUT;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    CsrDevice merged;
+    IGP_TRY(build_csr(d_edges, num_edges, g->csr.n, g->reorder, s, &merged, &g->csr));
+    // the old CSR is released in stream order behind the merge that read it
+    CsrDevice old = g->csr;
+    free_async(old.row_ptr, s);
+    free_async(old.col_idx, s);
+    free_async(old.order, s);
+    if (!old.perm_alias) {
+        free_async(old.rp_perm, s);
+        free_async(old.col_perm, s);
+    }
+    g->csr = merged;
+    g->m = merged.nnz / 2;
     return IGP_OK;
 }
 

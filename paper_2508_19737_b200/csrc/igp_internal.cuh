@@ -67,8 +67,10 @@ struct CsrDevice {
     int64_t nnz = 0;
 };
 constexpr int kColPad = 16;
+// canonical CSR of the new edges, merged with `base` (an existing canonical CSR on the same
+// node set) when base != nullptr
 igp_status build_csr(const int32_t* d_edges, int64_t num_edges, int32_t n, bool reorder, cudaStream_t s,
-                     CsrDevice* out);
+                     CsrDevice* out, const CsrDevice* base = nullptr);
 
 // exclusive scan of n int32 counts: out[0..n], out[n] = total (int32 range checked by caller)
 igp_status scan_exclusive(const int32_t* in, int32_t* out, int32_t n, cudaStream_t s);
@@ -96,6 +98,7 @@ igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cu
 
 struct igp_graph_s {
     igp::CsrDevice csr;
+    bool reorder = true;
     int64_t m = 0;
     igp::EmbedTiming timing;
 };

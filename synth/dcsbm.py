@@ -110,13 +110,14 @@ def generate(cfg: DCSBMConfig, seed: int | None = None):
     return edges, labels
 
 
-def stream_stages(edges_unique: np.ndarray, stages: int = 10, seed: int = 0):
-    """Streaming config: a seeded permutation of the unique undirected edges cut
-    into ``stages`` cumulative prefixes (10% each)."""
+def stream_batches(edges: np.ndarray, stages: int = 10, seed: int = 0):
+    """Streaming config (uniform edge sampling): a seeded permutation of the raw edge list
+    cut into ``stages`` batches of ~1/stages each; stage t's graph is the union of batches
+    0..t (cumulative)."""
     rng = np.random.default_rng(seed + 7919)
-    order = rng.permutation(edges_unique.shape[0])
-    cuts = np.linspace(0, edges_unique.shape[0], stages + 1).astype(np.int64)
-    return [edges_unique[order[: cuts[t + 1]]] for t in range(stages)]
+    order = rng.permutation(edges.shape[0])
+    cuts = np.linspace(0, edges.shape[0], stages + 1).astype(np.int64)
+    return [np.ascontiguousarray(edges[order[cuts[t]:cuts[t + 1]]]) for t in range(stages)]
 
 
 def random_edges(rng: np.random.Generator, n: int, e: int) -> np.ndarray:

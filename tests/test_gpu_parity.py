@@ -286,3 +286,49 @@ def test_build_flags_rejected(igp):
     e = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
     st = igp.lib().igp_build_graph_ex(ctypes.c_void_p(e.data_ptr()), 1, 2, 0x80, None, ctypes.byref(h))
     assert st == 2
+
+
+# ------------------------------------------------------------------ streaming (device CSR merge, Alg. 2 l.1-7)
+def test_streaming_merge_csr_bit_exact_and_embed(igp):
+    """Stage t's graph = union of batches 0..t (uniform edge sampling, 10 stages).
+    igp_graph_add_edges must give the canonical CSR of the cumulative edge list after
+    every stage, and the stage's re-embed (fresh Philox subsequence t, Alg. 2 l.3)
+    matches the oracle on the cumulative graph."""
+    from synth.dcsbm import stream_batches
+    c = CONFIGS["streaming"]
+    edges, _ = generate(c)
+    batches = stream_batches(edges, 10)
+    g = None
+    cum = []
+    for t, b in enumerate(batches):
+        cum.append(b)
+        eb = torch.from_numpy(b).cuda()
+        if g is None:
+            g = igp.build_graph(eb, c.num_nodes)
+        else:
+            g.add_edges(eb)
+        rp, ci = g.csr()
+        torch.cuda.synchronize()
+        allc = np.concatenate(cum)
+        rp_o, ci_o, m_o = oracle.build_csr(allc, c.num_nodes)
+        assert g.num_edges == m_o
+        assert np.array_equal(rp.cpu().numpy(), rp_o) and np.array_equal(ci.cpu().numpy(), ci_o), f"stage {t}"
+        if t in (0, 4, 9):
+            z = igp.embed(g, c.tau, c.d, c.steps, 0, subsequence=t).cpu().numpy()
+            ref = oracle.embed(rp_o, ci_o, c.num_nodes, c.d, c.steps, c.tau, seed=0, sub=t, nthreads=NTHREADS)
+            err = row_rel_err(z, ref)
+            record(f"streaming_stage{t}", err)
+            assert err <= TOL
+
+
+def test_add_edges_errors_leave_graph_unchanged(igp):
+    g = gpu_graph(igp, np.array([[0, 1], [1, 2]], np.int32), 4)
+    with pytest.raises(igp.IGPError):
+        g.add_edges(torch.tensor([[0, 9]], dtype=torch.int32, device="cuda"))
+    rp, ci = g.csr()
+    assert rp.cpu().tolist() == [0, 1, 3, 4, 4] and ci.cpu().tolist() == [1, 0, 2, 1]
+    g.add_edges(torch.tensor([[3, 0], [0, 1]], dtype=torch.int32, device="cuda"))  # one new, one duplicate
+    rp, ci = g.csr()
+    assert rp.cpu().tolist() == [0, 2, 4, 5, 6] and ci.cpu().tolist() == [1, 3, 0, 2, 1, 0]
+    g.add_edges(torch.zeros((0, 2), dtype=torch.int32, device="cuda"))
+    assert g.num_edges == 3
