@@ -216,18 +216,12 @@ def run_gpu(args, cfg):
     N, d, L, tau = cfg.num_nodes, cfg.d, cfg.steps, cfg.tau
     out = torch.empty((N, d), dtype=torch.float32, device=dev)
 
-    layer_ms = []
-
     def step(timed):
-        g = igp.build_graph(edges, N, stream=stream)
+        # the whole step is enqueued without a host sync: asynchronous build (range errors
+        # are checked on the warm-up graphs), embed, stream-ordered release of the graph
+        g = igp.build_graph(edges, N, stream=stream, async_build=True)
         igp.embed(g, tau, d, L, seed, out=out, stream=stream, time_layers=timed)
-        if timed:
-            stream.synchronize()
-            ms, launches = g.last_layer_time_ms()
-            layer_ms.append((ms, launches))
-        nnz = g.nnz
-        g.close()
-        return nnz
+        g.close(stream=stream)
 
     def barrier():
         if world > 1:
@@ -235,9 +229,12 @@ def run_gpu(args, cfg):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    nnz = step(False)
+    g = igp.build_graph(edges, N, stream=stream)  # synchronous build: validates the input, gives nnz
+    nnz = g.nnz
+    g.close()
     for _ in range(args.warmup):
         step(False)
+    igp.layer_timer_reset()
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -253,6 +250,7 @@ def run_gpu(args, cfg):
     launches = igp.kernel_launch_count() - launches0
     clock_rec = clocks.stop()
     ms_total = ev0.elapsed_time(ev1)
+    tot_layer_ms, tot_launches = igp.layer_timer_read()
 
     # embed-only timing (no build), same stream, for the breakdown
     g = igp.build_graph(edges, N, stream=stream)
@@ -283,9 +281,7 @@ def run_gpu(args, cfg):
     # columns is d/W launches of layer_kernel<W> (column slices); the
     # algorithmic bytes are those of the whole step (SURVEY.md §8(d) B_step), so
     # achieved = B_step / (time of the d/W launches that make up one step).
-    tot_layer_ms = sum(m for m, _ in layer_ms)
-    tot_launches = sum(n for _, n in layer_ms)
-    slices = max(1, tot_launches // max(1, L * len(layer_ms)))
+    slices = max(1, tot_launches // max(1, L * args.steps))
     width = d // slices
     avg_launch_s = tot_layer_ms / 1e3 / max(tot_launches, 1)
     step_s = avg_launch_s * slices

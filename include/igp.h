@@ -62,43 +62,57 @@ typedef enum {
  * ------------------------------------------------------------------------- */
 
 /* Build the canonical CSR of the undirected simple graph on num_nodes nodes.
- *   d_edges    device, int32 [num_edges][2] row-major (u, v) pairs; borrowed for
- *              the duration of the call only.  Duplicates, both orientations and
- *              self loops are allowed: self loops are dropped, each unordered
- *              pair {u, v}, u != v, becomes A_uv = A_vu = 1 once.
+ *   d_edges    device, int32 [num_edges][2] row-major (u, v) pairs; borrowed until the
+ *              build's work on `stream` has completed.  Duplicates, both orientations
+ *              and self loops are allowed: self loops are dropped, each unordered pair
+ *              {u, v}, u != v, becomes A_uv = A_vu = 1 once.
  *   num_edges  >= 0 (0 is valid: M = 0, all degrees 0); 2*num_edges must be
  *              <= INT32_MAX (else IGP_ERR_UNSUPPORTED).
  *   num_nodes  N >= 1 (else IGP_ERR_INPUT).
  *   out        receives a new handle owning device row_ptr int32[N+1] and
- *              col_idx int32[2M] (rows ascending, columns strictly ascending).
- * Errors: any index outside [0, N) -> IGP_ERR_INPUT (detected on the device and
- * read back at the build's single host synchronisation).
- * Synchronisation: exactly one stream sync (to read nnz and the error flag);
- * the remaining compaction is enqueued on `stream` when the call returns. */
+ *              col_idx int32[2M] (rows ascending, columns strictly ascending); the
+ *              column arrays are allocated for the 2*num_edges directed entries before
+ *              deduplication (no host round trip is needed to size them).
+ * Errors: any index outside [0, N) -> IGP_ERR_INPUT (detected on the device; the
+ * offending edges are skipped).
+ * Synchronisation: every kernel is enqueued first, then the call waits once for the
+ * build to complete (to report the error flag and nnz).  With IGP_BUILD_ASYNC it does
+ * not wait at all: see igp_graph_status. */
 IGP_API igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes,
                            igp_stream_t stream, igp_graph_t* out);
 
 #define IGP_BUILD_DEFAULT 0u
 #define IGP_BUILD_NO_REORDER 1u /* keep the original node order for the filter steps (no degree-sorted
                                    relabelling; results differ only by fp32 summation order) */
+#define IGP_BUILD_ASYNC 2u      /* fully asynchronous build (and later igp_graph_add_edges): the call
+                                   returns after enqueueing; a range error is reported by the first
+                                   igp_graph_status / igp_graph_info / igp_graph_copy_csr call, which
+                                   waits for the build.  Embeds may be enqueued behind it right away. */
 
-/* As igp_build_graph; `flags` selects the filter steps' row order.  By default the
- * handle also holds a relabelled copy of the CSR with rows by descending degree (ties by
- * ascending id), which the embed kernels traverse; IGP_BUILD_NO_REORDER skips it.  Unknown
- * flags -> IGP_ERR_INPUT. */
+/* As igp_build_graph; `flags` selects the filter steps' row order and the synchronisation.
+ * By default the handle also holds a relabelled copy of the CSR with rows by descending
+ * degree (ties by ascending id), which the embed kernels traverse; IGP_BUILD_NO_REORDER
+ * skips it.  Unknown flags -> IGP_ERR_INPUT. */
 IGP_API igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes, uint32_t flags,
                                       igp_stream_t stream, igp_graph_t* out);
 
 /* Streaming update (Alg. 2 l.1): merge a batch of new edges (same rules as
  * igp_build_graph, node ids in [0, N)) into the graph in place, on the device: the result
  * is the canonical CSR of the union, as if built from all edges at once, with the row
- * order (relabelling) recomputed.  One host sync; the previous CSR is released in stream
- * order.  On error the graph is unchanged.  Not safe concurrently with an embed of g. */
+ * order (relabelling) recomputed.  The previous CSR is released in stream order.  Waits
+ * once for the merge, and on a range error leaves the graph unchanged; a graph built with
+ * IGP_BUILD_ASYNC does not wait, skips the bad edges and reports IGP_ERR_INPUT from
+ * igp_graph_status.  Not safe concurrently with an embed of g on another stream. */
 IGP_API igp_status igp_graph_add_edges(igp_graph_t g, const int32_t* d_edges, int64_t num_edges,
                                        igp_stream_t stream);
 
-/* Query a graph: N, nnz = 2M (directed CSR entries) and M.  Any output pointer may be NULL. */
+/* Query a graph: N, nnz = 2M (directed CSR entries) and M.  Any output pointer may be NULL.
+ * Waits for an outstanding IGP_BUILD_ASYNC build/merge; returns its range error, if any. */
 IGP_API igp_status igp_graph_info(igp_graph_t g, int32_t* num_nodes, int64_t* nnz, int64_t* num_undirected_edges);
+
+/* Wait for the graph's build / last merge and return IGP_OK or IGP_ERR_INPUT (an edge
+ * index outside [0, N) was skipped).  Immediate for graphs built without IGP_BUILD_ASYNC. */
+IGP_API igp_status igp_graph_status(igp_graph_t g);
 
 /* Copy the canonical CSR (original node ids) into caller-owned device buffers
  * d_row_ptr int32[N+1] and d_col_idx int32[nnz]; asynchronous on `stream`. */
@@ -106,6 +120,11 @@ IGP_API igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t
 
 /* Release a graph (synchronises the device before freeing).  NULL is a no-op. */
 IGP_API igp_status igp_destroy_graph(igp_graph_t g);
+
+/* Release a graph in stream order on `stream` without any host synchronisation: all
+ * work that reads g must be on `stream` or ordered before it (e.g. by events).
+ * NULL g is a no-op. */
+IGP_API igp_status igp_destroy_graph_async(igp_graph_t g, igp_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * Embedding  (Alg. 1 lines 1-6)
@@ -115,8 +134,8 @@ IGP_API igp_status igp_destroy_graph(igp_graph_t g);
 #define IGP_MODE_PRE_SIGMOID 1 /* Z^(L) (column z-scored), debug/test      */
 #define IGP_MODE_LINEAR 2      /* Z^(l) = phi * Z^(l-1): no tanh/ZNorm/sigmoid, debug/test */
 
-#define IGP_FLAG_TIME_LAYERS 1u /* record CUDA events around the L filter-step launches
-                                   (igp_last_layer_time_ms); makes the call mutate the handle */
+#define IGP_FLAG_TIME_LAYERS 1u /* record CUDA events on `stream` around each slice's L filter-step
+                                   launches into the process-wide layer timer (igp_layer_timer_*) */
 
 typedef struct {
     float tau;            /* degree correction tau (Eq. (1) for tau < 0; D + tau I otherwise); finite */
@@ -156,9 +175,12 @@ IGP_API igp_status igp_embed_ex(igp_graph_t g, const igp_embed_opts* opts, float
 IGP_API igp_status igp_embed_host(const int32_t* h_edges, int64_t num_edges, int32_t num_nodes,
                           const igp_embed_opts* opts, float* h_out, igp_stream_t stream);
 
-/* After an igp_embed_ex with IGP_FLAG_TIME_LAYERS has completed (caller synced):
- * total device time of the L filter-step launches and the launch count. */
-IGP_API igp_status igp_last_layer_time_ms(igp_graph_t g, float* total_ms, int32_t* launches);
+/* Process-wide filter-step timer fed by embeds with IGP_FLAG_TIME_LAYERS (thread safe).
+ * reset: forget all recorded intervals.  read: wait for the recorded intervals to
+ * complete and return their summed device time (ms) and the number of filter-step
+ * launches they bracket.  Recording adds no host synchronisation to an embed. */
+IGP_API igp_status igp_layer_timer_reset(void);
+IGP_API igp_status igp_layer_timer_read(float* total_ms, int64_t* launches);
 
 /* ---------------------------------------------------------------------------
  * Random input (test / inspection entry points)

@@ -52,13 +52,16 @@ SIGNATURES = {
     "igp_build_graph_ex": (ctypes.c_int, [_P, _i64, _i32, ctypes.c_uint32, _P, ctypes.POINTER(_P)]),
     "igp_graph_add_edges": (ctypes.c_int, [_P, _P, _i64, _P]),
     "igp_graph_info": (ctypes.c_int, [_P, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "igp_graph_status": (ctypes.c_int, [_P]),
     "igp_graph_copy_csr": (ctypes.c_int, [_P, _P, _P, _P]),
     "igp_destroy_graph": (ctypes.c_int, [_P]),
+    "igp_destroy_graph_async": (ctypes.c_int, [_P, _P]),
     "igp_embed_opts_default": (None, [ctypes.POINTER(EmbedOpts)]),
     "igp_embed": (ctypes.c_int, [_P, _f32, _i32, _i32, _u64, _P, _P]),
     "igp_embed_ex": (ctypes.c_int, [_P, ctypes.POINTER(EmbedOpts), _P, _P]),
     "igp_embed_host": (ctypes.c_int, [_P, _i64, _i32, ctypes.POINTER(EmbedOpts), _P, _P]),
-    "igp_last_layer_time_ms": (ctypes.c_int, [_P, ctypes.POINTER(_f32), ctypes.POINTER(_i32)]),
+    "igp_layer_timer_reset": (ctypes.c_int, []),
+    "igp_layer_timer_read": (ctypes.c_int, [ctypes.POINTER(_f32), ctypes.POINTER(_i64)]),
     "igp_philox_bits": (ctypes.c_int, [_u64, _u64, _i64, _P, _P]),
     "igp_philox_normal": (ctypes.c_int, [_u64, _u64, _i64, _P, _P]),
     "igp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -100,20 +103,41 @@ def _require_cuda(t: torch.Tensor, dtype, name: str):
 
 
 class Graph:
-    """Device CSR handle (igp_graph_t).  Owns row_ptr / col_idx on the device."""
+    """Device CSR handle (igp_graph_t).  Owns row_ptr / col_idx on the device.
 
-    def __init__(self, handle: ctypes.c_void_p, device: torch.device):
+    ``nnz`` / ``num_edges`` are read lazily (igp_graph_info): for a graph built with
+    ``async_build=True`` the first access waits for the build and raises on a range error."""
+
+    def __init__(self, handle: ctypes.c_void_p, device: torch.device, num_nodes: int):
         self._h = handle
         self.device = device
-        n, nnz, m = _i32(), _i64(), _i64()
-        _check(_lib.igp_graph_info(handle, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(m)))
-        self.num_nodes, self.nnz, self.num_edges = n.value, nnz.value, m.value
+        self.num_nodes = int(num_nodes)
+        self._nnz = None
 
     @property
     def handle(self):
         if self._h is None:
             raise ValueError("graph was destroyed")
         return self._h
+
+    def _info(self):
+        if self._nnz is None:
+            n, nnz, m = _i32(), _i64(), _i64()
+            _check(_lib.igp_graph_info(self.handle, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(m)))
+            self._nnz = nnz.value
+        return self._nnz
+
+    @property
+    def nnz(self) -> int:
+        return self._info()
+
+    @property
+    def num_edges(self) -> int:
+        return self._info() // 2
+
+    def status(self):
+        """igp_graph_status: wait for the build / last merge; raises IGPError on a range error."""
+        _check(_lib.igp_graph_status(self.handle))
 
     def csr(self, stream=None):
         """(row_ptr int32[N+1], col_idx int32[nnz]) copies on the graph's device."""
@@ -129,19 +153,19 @@ class Graph:
         with torch.cuda.device(self.device):
             _check(_lib.igp_graph_add_edges(self.handle, ctypes.c_void_p(edges.data_ptr()), edges.shape[0],
                                             _stream_ptr(stream)))
-        n, nnz, m = _i32(), _i64(), _i64()
-        _check(_lib.igp_graph_info(self.handle, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(m)))
-        self.nnz, self.num_edges = nnz.value, m.value
+        self._nnz = None
         return self
 
-    def last_layer_time_ms(self):
-        ms, n = _f32(), _i32()
-        _check(_lib.igp_last_layer_time_ms(self.handle, ctypes.byref(ms), ctypes.byref(n)))
-        return ms.value, n.value
-
-    def close(self):
+    def close(self, stream=None):
+        """Destroy the handle: with ``stream`` in stream order (igp_destroy_graph_async, no host
+        sync; all work on the graph must be on / ordered before that stream), else after a
+        device sync (igp_destroy_graph)."""
         if self._h is not None:
-            _lib.igp_destroy_graph(self._h)
+            if stream is None:
+                _lib.igp_destroy_graph(self._h)
+            else:
+                with torch.cuda.device(self.device):
+                    _lib.igp_destroy_graph_async(self._h, _stream_ptr(stream))
             self._h = None
 
     def __del__(self):
@@ -158,21 +182,39 @@ class Graph:
 
 
 BUILD_NO_REORDER = 1
+BUILD_ASYNC = 2
 
 
-def build_graph(edges: torch.Tensor, num_nodes: int, stream=None, reorder: bool = True) -> Graph:
+def build_graph(edges: torch.Tensor, num_nodes: int, stream=None, reorder: bool = True,
+                async_build: bool = False) -> Graph:
     """igp_build_graph_ex: canonical CSR of the undirected simple graph.
 
     ``edges``: CUDA int32 tensor [E, 2] (duplicates / both orientations / self loops allowed).
-    ``reorder=False`` keeps the original row order for the filter steps (IGP_BUILD_NO_REORDER)."""
+    ``reorder=False`` keeps the original row order for the filter steps (IGP_BUILD_NO_REORDER).
+    ``async_build=True`` returns without any host sync (IGP_BUILD_ASYNC); range errors surface
+    from ``Graph.status()`` / ``nnz``."""
     _require_cuda(edges, torch.int32, "edges")
     if edges.dim() != 2 or edges.shape[1] != 2:
         raise ValueError("edges must have shape [E, 2]")
     h = _P()
+    flags = (0 if reorder else BUILD_NO_REORDER) | (BUILD_ASYNC if async_build else 0)
     with torch.cuda.device(edges.device):
         _check(_lib.igp_build_graph_ex(ctypes.c_void_p(edges.data_ptr()), edges.shape[0], int(num_nodes),
-                                       0 if reorder else BUILD_NO_REORDER, _stream_ptr(stream), ctypes.byref(h)))
-    return Graph(h, edges.device)
+                                       flags, _stream_ptr(stream), ctypes.byref(h)))
+    return Graph(h, edges.device, num_nodes)
+
+
+def layer_timer_reset():
+    """igp_layer_timer_reset: forget the filter-step intervals recorded so far."""
+    _check(_lib.igp_layer_timer_reset())
+
+
+def layer_timer_read():
+    """igp_layer_timer_read: (total ms, launches) of the filter-step intervals recorded by
+    embeds with ``time_layers=True`` since the last reset (waits for them to complete)."""
+    ms, n = _f32(), _i64()
+    _check(_lib.igp_layer_timer_read(ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value
 
 
 def make_opts(tau: float, d: int, steps: int, seed: int = 0, *, subsequence: int = 0, theta: float = 0.1,

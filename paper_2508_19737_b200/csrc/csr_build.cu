@@ -16,7 +16,9 @@
 //                   1024 < len <= 16384:  one block per row, bitonic sort in shared memory
 //                   len > 16384:          one block per row, N-bit bitmap in global scratch
 //   B5 scan+compact  row_ptr = scan(unique counts); col_idx = compacted rows
-// The only host synchronisation reads nnz = row_ptr[N] and the error flag.
+// No host synchronisation: the column arrays are sized by the 2E directed entries
+// before deduplication; nnz = row_ptr[N] and the range-error flag stay on the device
+// until the caller asks (igp_api.cu).
 #include <climits>
 #include <cstdio>
 
@@ -40,7 +42,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 // ---------------------------------------------------------------- B1 / B3
 __global__ void count_kernel(const int32_t* __restrict__ edges, int64_t E, int32_t n,
-                             int32_t* __restrict__ cnt, int32_t* __restrict__ err) {
+                             int32_t* __restrict__ cnt, int32_t* __restrict__ err) {  // err: CsrDevice::meta[0]
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += stride) {
         const int32_t u = __ldg(edges + 2 * e), v = __ldg(edges + 2 * e + 1);
@@ -490,12 +492,23 @@ __global__ void iota_kernel(int32_t* __restrict__ a, int32_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) a[i] = (int32_t)i;
 }
 
+void free_csr(const CsrDevice& c, cudaStream_t s) {
+    free_async(c.row_ptr, s);
+    free_async(c.col_idx, s);
+    free_async(c.order, s);
+    free_async(c.meta, s);
+    if (!c.perm_alias) {
+        free_async(c.rp_perm, s);
+        free_async(c.col_perm, s);
+    }
+}
+
 igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder, cudaStream_t s, CsrDevice* out,
                      const CsrDevice* base) {
     DeviceInfo di;
     if (!device_info(&di)) return IGP_ERR_CUDA;
     // both orientations of the new edges (before dedup / self-loop removal), plus the base rows
-    const int64_t raw = 2 * E + (base ? base->nnz : 0);
+    const int64_t raw = 2 * E + (base ? base->cap : 0);
     if (raw > (int64_t)INT32_MAX) {
         set_error("edge count exceeds the int32 CSR index range");
         return IGP_ERR_UNSUPPORTED;
@@ -530,24 +543,26 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder,
     int32_t* inv = (int32_t*)(ws + o_inv);
     int32_t* degp = (int32_t*)(ws + o_degp);
     int32_t* tmp = (int32_t*)(ws + o_tmp);
-    SortScratch sc{(int32_t*)(ws + o_big), (int32_t*)(ws + o_giant), flags + 1, (uint32_t*)(ws + o_bitmap)};
+    SortScratch sc{(int32_t*)(ws + o_big), (int32_t*)(ws + o_giant), flags, (uint32_t*)(ws + o_bitmap)};
 
     CsrDevice c;
     c.n = n;
+    c.cap = raw;
+    // the column arrays are sized by the entries before deduplication, so nothing on the
+    // host waits for nnz; vector index loads may read up to kColPad entries past a row
+    const size_t cbytes = sizeof(int32_t) * (size_t)(raw + kColPad);
     igp_status st = cuda_status(alloc_async((void**)&c.row_ptr, sizeof(int32_t) * ((size_t)n + 1), s), "alloc");
     if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.order, sizeof(int32_t) * (size_t)n, s), "alloc");
+    if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.meta, 4 * sizeof(int32_t), s), "alloc");
+    if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.col_idx, cbytes, s), "col_idx alloc");
     // rp_perm padded by 4 entries: 16-byte bulk copies of a row-pointer slice may overrun the end
     if (st == IGP_OK && reorder)
         st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 5), s), "alloc");
+    if (st == IGP_OK && reorder) st = cuda_status(alloc_async((void**)&c.col_perm, cbytes, s), "col_perm alloc");
+    if (!reorder) c.perm_alias = true;
     auto fail = [&](igp_status e) {
         free_async(ws, s);
-        free_async(c.row_ptr, s);
-        free_async(c.order, s);
-        free_async(c.col_idx, s);
-        if (reorder) {
-            free_async(c.rp_perm, s);
-            free_async(c.col_perm, s);
-        }
+        free_csr(c, s);
         return e;
     };
     if (st != IGP_OK) return fail(st);
@@ -557,6 +572,14 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder,
         if (_s != IGP_OK) return fail(_s);              \
     } while (0)
     IGP_STEP(cuda_status(cudaMemsetAsync(flags, 0, 4 * sizeof(int32_t), s), "memset"));
+    // range-error flag: a merge inherits the base graph's (asynchronous builds report it lazily)
+    if (base)
+        IGP_STEP(cuda_status(cudaMemcpyAsync(c.meta, base->meta, 4 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s),
+                             "meta copy"));
+    else
+        IGP_STEP(cuda_status(cudaMemsetAsync(c.meta, 0, 4 * sizeof(int32_t), s), "memset"));
+    IGP_STEP(cuda_status(cudaMemsetAsync(c.col_idx + raw, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
+    if (reorder) IGP_STEP(cuda_status(cudaMemsetAsync(c.col_perm + raw, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
     // B1-B3: count, scan, scatter both orientations into row buckets (behind the base rows)
     if (base) {
         base_degree_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(base->row_ptr, n, cnt);
@@ -566,13 +589,13 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder,
     }
     const int eg = grid_for(E, 256, di.num_sms, 16);
     if (E > 0) {
-        count_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, cnt, flags);
+        count_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, cnt, c.meta);
         IGP_STEP(launch_status("count_kernel"));
     }
     IGP_STEP(scan_exclusive(cnt, off, n, s));
-    const int rg0 = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
+    const int rg = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
     if (base) {
-        base_copy_kernel<<<rg0, 256, 0, s>>>(base->row_ptr, base->col_idx, n, off, tmp);
+        base_copy_kernel<<<rg, 256, 0, s>>>(base->row_ptr, base->col_idx, n, off, tmp);
         IGP_STEP(launch_status("base_copy_kernel"));
         base_degree_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(base->row_ptr, n, cnt);
         IGP_STEP(launch_status("base_degree_kernel"));
@@ -583,61 +606,38 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder,
         scatter_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, off, cnt, tmp);
         IGP_STEP(launch_status("scatter_kernel"));
     }
-    // B4-B5: per-row sort + dedup, row pointers
+    // B4-B5: per-row sort + dedup, row pointers, compaction
     IGP_STEP(segmented_sort(off, tmp, ucnt, n, raw, n, sc, s, di));
     IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
-    if (reorder) {
-        // B6a: degree-descending order (counting sort by degree, then ascending id per bucket)
-        IGP_STEP(cuda_status(cudaMemsetAsync(hist, 0, sizeof(int32_t) * kDegBuckets, s), "memset"));
-        degree_hist_kernel<<<grid_for(n, 256, di.num_sms, 4), 256, 0, s>>>(c.row_ptr, n, hist);
-        IGP_STEP(launch_status("degree_hist_kernel"));
-        IGP_STEP(scan_exclusive(hist, boff, kDegBuckets, s));
-        IGP_STEP(cuda_status(
-            cudaMemcpyAsync(fill, boff, sizeof(int32_t) * (kDegBuckets + 1), cudaMemcpyDeviceToDevice, s), "copy"));
-        degree_scatter_kernel<<<(n + kSchedTile - 1) / kSchedTile, 256, 0, s>>>(c.row_ptr, n, fill, c.order);
-        IGP_STEP(launch_status("degree_scatter_kernel"));
-        IGP_STEP(segmented_sort(boff, c.order, hist, kDegBuckets, n, n, sc, s, di));
-    } else {
-        iota_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n);  // identity labelling
-        IGP_STEP(launch_status("iota_kernel"));
-    }
-    // the build's single host synchronisation: nnz and the error flag
-    int32_t host_vals[2] = {0, 0};
-    IGP_STEP(cuda_status(cudaMemcpyAsync(&host_vals[0], c.row_ptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
-                         "nnz readback"));
-    IGP_STEP(cuda_status(cudaMemcpyAsync(&host_vals[1], flags, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
-                         "flag readback"));
-    IGP_STEP(cuda_status(cudaStreamSynchronize(s), "build sync"));
-    if (host_vals[1] != 0) {
-        set_error("igp_build_graph: edge index outside [0, num_nodes)");
-        return fail(IGP_ERR_INPUT);
-    }
-    c.nnz = host_vals[0];
-    const size_t cbytes = sizeof(int32_t) * (size_t)(c.nnz + kColPad);
-    IGP_STEP(cuda_status(alloc_async((void**)&c.col_idx, cbytes, s), "col_idx alloc"));
-    if (reorder) IGP_STEP(cuda_status(alloc_async((void**)&c.col_perm, cbytes, s), "col_perm alloc"));
-    IGP_STEP(cuda_status(cudaMemsetAsync(c.col_idx + c.nnz, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
-    if (reorder)
-        IGP_STEP(cuda_status(cudaMemsetAsync(c.col_perm + c.nnz, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
-    const int rg = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
-    if (c.nnz > 0) {
+    if (raw > 0) {
         compact_kernel<<<rg, 256, 0, s>>>(off, tmp, c.row_ptr, c.col_idx, n);
         IGP_STEP(launch_status("compact_kernel"));
     }
     if (!reorder) {  // the filter steps run on the canonical CSR itself
+        iota_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n);  // identity labelling
+        IGP_STEP(launch_status("iota_kernel"));
         c.rp_perm = c.row_ptr;
         c.col_perm = c.col_idx;
-        c.perm_alias = true;
         free_async(ws, s);
         *out = c;
         return IGP_OK;
     }
+    // B6a: degree-descending order (counting sort by degree, then ascending id per bucket)
+    IGP_STEP(cuda_status(cudaMemsetAsync(hist, 0, sizeof(int32_t) * kDegBuckets, s), "memset"));
+    degree_hist_kernel<<<grid_for(n, 256, di.num_sms, 4), 256, 0, s>>>(c.row_ptr, n, hist);
+    IGP_STEP(launch_status("degree_hist_kernel"));
+    IGP_STEP(scan_exclusive(hist, boff, kDegBuckets, s));
+    IGP_STEP(cuda_status(
+        cudaMemcpyAsync(fill, boff, sizeof(int32_t) * (kDegBuckets + 1), cudaMemcpyDeviceToDevice, s), "copy"));
+    degree_scatter_kernel<<<(n + kSchedTile - 1) / kSchedTile, 256, 0, s>>>(c.row_ptr, n, fill, c.order);
+    IGP_STEP(launch_status("degree_scatter_kernel"));
+    IGP_STEP(segmented_sort(boff, c.order, hist, kDegBuckets, n, n, sc, s, di));
     // B6b: the relabelled CSR the filter steps run on (rows by descending degree)
     inverse_perm_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n, inv, c.row_ptr, degp);
     IGP_STEP(launch_status("inverse_perm_kernel"));
     IGP_STEP(scan_exclusive(degp, c.rp_perm, n, s));
     IGP_STEP(cuda_status(cudaMemsetAsync(c.rp_perm + n + 1, 0, 4 * sizeof(int32_t), s), "pad memset"));
-    if (c.nnz > 0) {
+    if (raw > 0) {
         perm_scatter_kernel<<<rg, 256, 0, s>>>(c.order, inv, c.row_ptr, c.col_idx, c.rp_perm, c.col_perm, n);
         IGP_STEP(launch_status("perm_scatter_kernel"));
         IGP_STEP(segmented_sort(c.rp_perm, c.col_perm, ucnt, n, raw, n, sc, s, di));

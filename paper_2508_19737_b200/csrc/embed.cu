@@ -545,7 +545,7 @@ int choose_width(int d, int32_t n, int64_t nnz) {
 
 template <int W, int MB>
 igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s,
-                       EmbedTiming* timing, const DeviceInfo& di) {
+                       const DeviceInfo& di) {
     const int32_t n = g.n;
     const int L = o.steps, d = o.d, nslices = d / W;
     const int grid = layer_grid<W, MB>(n, di);
@@ -573,7 +573,7 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     if (const char* e = getenv("IGP_ST_EF")) st_ef = (float)atof(e);
 
     igp_status rc = IGP_OK;
-    const bool timed = (o.flags & IGP_FLAG_TIME_LAYERS) && timing;
+    const bool timed = (o.flags & IGP_FLAG_TIME_LAYERS) != 0;
     do {
         // all filter-step work runs on the relabelled CSR (rows by descending degree)
         scale_kernel<<<simple_grid(n, 256, di), 256, 0, s>>>(g.rp_perm, n, (double)o.tau, (double)o.eps, node);
@@ -589,10 +589,14 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
             input_kernel<W><<<simple_grid((int64_t)n * (W / 4), 256, di), 256, 0, s>>>(o.seed, o.subsequence, n, d,
                                                                                       col0, g.order, node, ybuf[0]);
             if ((rc = launch_status("input_kernel")) != IGP_OK) break;
-            if (timed) {
-                if (!timing->ev0[k]) cudaEventCreate(&timing->ev0[k]);
-                if (!timing->ev1[k]) cudaEventCreate(&timing->ev1[k]);
-                cudaEventRecord(timing->ev0[k], s);
+            TimerSlot* ts = nullptr;
+            if (timed && L > 0) {
+                if (!(ts = timer_acquire(L))) {
+                    rc = IGP_ERR_CUDA;
+                    set_error("layer timer: event creation failed");
+                    break;
+                }
+                cudaEventRecord(ts->ev0, s);
             }
             for (int l = 1; l <= L; ++l) {
                 LayerArgs a;
@@ -614,16 +618,11 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 if ((rc = launch_status("layer_kernel")) != IGP_OK) break;
             }
             if (rc != IGP_OK) break;
-            if (timed) cudaEventRecord(timing->ev1[k], s);
+            if (ts) cudaEventRecord(ts->ev1, s);
             const double* sfin = (linear || L == 0) ? nullptr : sk + (size_t)L * 2 * W;
             output_kernel<W><<<simple_grid((int64_t)n * (W / 4), 256, di), 256, 0, s>>>(ybuf[L & 1], node, sfin, g.order, n,
                                                                                         d, col0, o.mode, out);
             if ((rc = launch_status("output_kernel")) != IGP_OK) break;
-        }
-        if (rc == IGP_OK && timed) {
-            timing->slices = nslices;
-            timing->launches = L * nslices;
-            timing->valid = true;
         }
     } while (0);
     free_async(ws, s);
@@ -632,21 +631,20 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
 
 }  // namespace
 
-igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s, EmbedTiming* timing) {
+igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s) {
     DeviceInfo di;
     if (!device_info(&di)) return IGP_ERR_CUDA;
     if (o.d != 16 && o.d != 32 && o.d != 64 && o.d != 128) {
         set_error("igp_embed: d must be one of 16, 32, 64, 128");
         return IGP_ERR_UNSUPPORTED;
     }
-    if (timing) timing->valid = false;
     const char* occ_env = getenv("IGP_LAYER_OCC");  // development knob: 2 or 3 blocks per SM
     const int occ = occ_env ? atoi(occ_env) : kDefaultOcc;
 #define IGP_W_CASE(WW)                                                      \
     case WW:                                                                \
-        if (occ == 3) return run_embed_w<WW, 3>(g, o, out, s, timing, di); \
-        return run_embed_w<WW, 2>(g, o, out, s, timing, di);
-    switch (choose_width(o.d, g.n, g.nnz)) {
+        if (occ == 3) return run_embed_w<WW, 3>(g, o, out, s, di); \
+        return run_embed_w<WW, 2>(g, o, out, s, di);
+    switch (choose_width(o.d, g.n, g.cap)) {  // a heuristic: cap ~ nnz (the output does not depend on W)
         IGP_W_CASE(16)
         IGP_W_CASE(32)
         IGP_W_CASE(64)

@@ -6,6 +6,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "igp_internal.cuh"
 
@@ -62,6 +63,90 @@ cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s) {
 
 void free_async(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
+}
+
+// ---------------------------------------------------------------- layer timer
+namespace {
+struct TimerEntry {
+    TimerSlot slot;
+    int device = -1;
+    int64_t launches = 0;
+};
+std::mutex g_timer_mu;
+std::vector<TimerEntry*> g_timer;  // entries [0, g_timer_used) are recorded intervals
+size_t g_timer_used = 0;
+}  // namespace
+
+TimerSlot* timer_acquire(int64_t launches) {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(g_timer_mu);
+    // reuse a free entry of this device, else create one
+    for (size_t k = g_timer_used; k < g_timer.size(); ++k) {
+        if (g_timer[k]->device == dev) {
+            std::swap(g_timer[k], g_timer[g_timer_used]);
+            TimerEntry* e = g_timer[g_timer_used++];
+            e->launches = launches;
+            return &e->slot;
+        }
+    }
+    TimerEntry* e = new (std::nothrow) TimerEntry();
+    if (!e) return nullptr;
+    if (cudaEventCreate(&e->slot.ev0) != cudaSuccess || cudaEventCreate(&e->slot.ev1) != cudaSuccess) {
+        if (e->slot.ev0) cudaEventDestroy(e->slot.ev0);
+        delete e;
+        return nullptr;
+    }
+    e->device = dev;
+    e->launches = launches;
+    g_timer.push_back(e);
+    std::swap(g_timer.back(), g_timer[g_timer_used]);
+    return &g_timer[g_timer_used++]->slot;
+}
+
+// ---------------------------------------------------------------- lazy graph status
+// a private non-blocking stream per device for the few-byte status reads (so a query does not
+// serialise behind unrelated work on the legacy default stream)
+static cudaStream_t status_stream(int dev) {
+    static std::mutex mu;
+    static cudaStream_t st[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    cudaStream_t& x = st[dev & 63];
+    if (!x) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+    return x;
+}
+
+// wait for g's last build / merge and read nnz = row_ptr[N] and the range-error flag
+igp_status resolve_graph(igp_graph_s* g) {
+    if (g->resolved) return IGP_OK;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != g->device) cudaSetDevice(g->device);
+    igp_status st = cuda_status(cudaEventSynchronize(g->ready), "graph build");
+    int32_t vals[2] = {0, 0};
+    if (st == IGP_OK) {
+        cudaStream_t ps = status_stream(g->device);
+        st = cuda_status(cudaMemcpyAsync(&vals[0], g->csr.row_ptr + g->csr.n, sizeof(int32_t), cudaMemcpyDeviceToHost, ps),
+                         "nnz readback");
+        if (st == IGP_OK)
+            st = cuda_status(cudaMemcpyAsync(&vals[1], g->csr.meta, sizeof(int32_t), cudaMemcpyDeviceToHost, ps),
+                             "flag readback");
+        if (st == IGP_OK) st = cuda_status(cudaStreamSynchronize(ps), "status sync");
+    }
+    if (prev != g->device && prev >= 0) cudaSetDevice(prev);
+    if (st != IGP_OK) return st;
+    g->nnz = vals[0];
+    g->err = vals[1];
+    g->resolved = true;
+    return IGP_OK;
+}
+
+igp_status graph_error(const igp_graph_s* g) {
+    if (g->err) {
+        set_error("edge index outside [0, num_nodes) (the offending edges were skipped)");
+        return IGP_ERR_INPUT;
+    }
+    return IGP_OK;
 }
 
 }  // namespace igp
@@ -124,7 +209,7 @@ igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, int32_t nu
 igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes, uint32_t flags,
                               igp_stream_t stream, igp_graph_t* out) {
     set_error("");
-    if (flags & ~(uint32_t)IGP_BUILD_NO_REORDER) {
+    if (flags & ~(uint32_t)(IGP_BUILD_NO_REORDER | IGP_BUILD_ASYNC)) {
         if (out) *out = nullptr;
         set_error("unknown build flags");
         return IGP_ERR_INPUT;
@@ -148,14 +233,28 @@ igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t
     }
     igp_graph_s* g = new (std::nothrow) igp_graph_s();
     if (!g) return IGP_ERR_OOM;
-    igp_status st = build_csr(d_edges, num_edges, num_nodes, (flags & IGP_BUILD_NO_REORDER) == 0,
-                              (cudaStream_t)stream, &g->csr);
+    cudaStream_t s = (cudaStream_t)stream;
+    g->reorder = (flags & IGP_BUILD_NO_REORDER) == 0;
+    g->async = (flags & IGP_BUILD_ASYNC) != 0;
+    igp_status st = cuda_status(cudaGetDevice(&g->device), "cudaGetDevice");
+    if (st == IGP_OK) st = cuda_status(cudaEventCreateWithFlags(&g->ready, cudaEventDisableTiming), "event");
+    if (st == IGP_OK) st = build_csr(d_edges, num_edges, num_nodes, g->reorder, s, &g->csr);
     if (st != IGP_OK) {
+        if (g->ready) cudaEventDestroy(g->ready);
         delete g;
         return st;
     }
-    g->m = g->csr.nnz / 2;
-    g->reorder = (flags & IGP_BUILD_NO_REORDER) == 0;
+    st = cuda_status(cudaEventRecord(g->ready, s), "event record");
+    if (st == IGP_OK && !g->async) {
+        st = resolve_graph(g);
+        if (st == IGP_OK) st = graph_error(g);
+    }
+    if (st != IGP_OK) {
+        std::string msg = igp_last_error_message();
+        igp_destroy_graph_async(g, stream);
+        set_error(msg);
+        return st;
+    }
     *out = g;
     return IGP_OK;
 }
@@ -170,63 +269,82 @@ igp_status igp_graph_add_edges(igp_graph_t g, const int32_t* d_edges, int64_t nu
         set_error("num_edges must be >= 0 and d_edges non-NULL when num_edges > 0");
         return IGP_ERR_INPUT;
     }
+    if (num_edges > ((int64_t)INT32_MAX - g->csr.cap) / 2) {
+        set_error("merged edge count exceeds the int32 CSR index range");
+        return IGP_ERR_UNSUPPORTED;
+    }
     cudaStream_t s = (cudaStream_t)stream;
+    // the merge reads the current CSR: order it behind the build / merge that wrote it
+    IGP_CUDA(cudaStreamWaitEvent(s, g->ready, 0), "stream wait");
     CsrDevice merged;
     IGP_TRY(build_csr(d_edges, num_edges, g->csr.n, g->reorder, s, &merged, &g->csr));
-    // the old CSR is released in stream order behind the merge that read it
-    CsrDevice old = g->csr;
-    free_async(old.row_ptr, s);
-    free_async(old.col_idx, s);
-    free_async(old.order, s);
-    if (!old.perm_alias) {
-        free_async(old.rp_perm, s);
-        free_async(old.col_perm, s);
+    IGP_CUDA(cudaEventRecord(g->ready, s), "event record");
+    if (!g->async) {
+        // check the merge before replacing the graph: on a range error g stays as it was
+        igp_graph_s tmp;
+        tmp.csr = merged;
+        tmp.device = g->device;
+        tmp.ready = g->ready;
+        igp_status st = resolve_graph(&tmp);
+        if (st == IGP_OK) st = graph_error(&tmp);
+        tmp.ready = nullptr;
+        if (st != IGP_OK) {
+            free_csr(merged, s);
+            return st;
+        }
+        g->nnz = tmp.nnz;
+        g->err = 0;
+        g->resolved = true;
+    } else {
+        g->resolved = false;
     }
+    // the old CSR is released in stream order behind the merge that read it
+    free_csr(g->csr, s);
     g->csr = merged;
-    g->m = merged.nnz / 2;
     return IGP_OK;
 }
 
-igp_status igp_graph_info(igp_graph_t g, int32_t* num_nodes, int64_t* nnz, int64_t* m) {
+igp_status igp_graph_status(igp_graph_t g) {
     if (!g) {
         set_error("graph is NULL");
         return IGP_ERR_INPUT;
     }
+    IGP_TRY(resolve_graph(g));
+    return graph_error(g);
+}
+
+igp_status igp_graph_info(igp_graph_t g, int32_t* num_nodes, int64_t* nnz, int64_t* m) {
+    IGP_TRY(igp_graph_status(g));
     if (num_nodes) *num_nodes = g->csr.n;
-    if (nnz) *nnz = g->csr.nnz;
-    if (m) *m = g->m;
+    if (nnz) *nnz = g->nnz;
+    if (m) *m = g->nnz / 2;
     return IGP_OK;
 }
 
 igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t* d_col_idx, igp_stream_t stream) {
-    if (!g || !d_row_ptr || (g->csr.nnz > 0 && !d_col_idx)) {
+    if (!g || !d_row_ptr) {
         set_error("graph or output pointer is NULL");
+        return IGP_ERR_INPUT;
+    }
+    IGP_TRY(igp_graph_status(g));
+    if (g->nnz > 0 && !d_col_idx) {
+        set_error("d_col_idx is NULL");
         return IGP_ERR_INPUT;
     }
     cudaStream_t s = (cudaStream_t)stream;
     IGP_CUDA(cudaMemcpyAsync(d_row_ptr, g->csr.row_ptr, sizeof(int32_t) * ((size_t)g->csr.n + 1),
                              cudaMemcpyDeviceToDevice, s),
              "copy row_ptr");
-    if (g->csr.nnz > 0)
-        IGP_CUDA(cudaMemcpyAsync(d_col_idx, g->csr.col_idx, sizeof(int32_t) * (size_t)g->csr.nnz,
+    if (g->nnz > 0)
+        IGP_CUDA(cudaMemcpyAsync(d_col_idx, g->csr.col_idx, sizeof(int32_t) * (size_t)g->nnz,
                                  cudaMemcpyDeviceToDevice, s),
                  "copy col_idx");
     return IGP_OK;
 }
 
 static void release_graph(igp_graph_t g, cudaStream_t s) {
-    // the CSR lives in the stream-ordered pool; callers have drained all work on it
-    free_async(g->csr.row_ptr, s);
-    free_async(g->csr.col_idx, s);
-    free_async(g->csr.order, s);
-    if (!g->csr.perm_alias) {
-        free_async(g->csr.rp_perm, s);
-        free_async(g->csr.col_perm, s);
-    }
-    for (int k = 0; k < kMaxSlices; ++k) {
-        if (g->timing.ev0[k]) cudaEventDestroy(g->timing.ev0[k]);
-        if (g->timing.ev1[k]) cudaEventDestroy(g->timing.ev1[k]);
-    }
+    free_csr(g->csr, s);
+    if (g->ready) cudaEventDestroy(g->ready);  // deferred by the runtime until the event completes
     delete g;
 }
 
@@ -234,6 +352,14 @@ igp_status igp_destroy_graph(igp_graph_t g) {
     if (!g) return IGP_OK;
     cudaDeviceSynchronize();  // no stream may still read the CSR
     release_graph(g, (cudaStream_t)0);
+    return IGP_OK;
+}
+
+igp_status igp_destroy_graph_async(igp_graph_t g, igp_stream_t stream) {
+    if (!g) return IGP_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaStreamWaitEvent(s, g->ready, 0);  // never free under an unfinished build / merge
+    release_graph(g, s);
     return IGP_OK;
 }
 
@@ -253,7 +379,10 @@ igp_status igp_embed_ex(igp_graph_t g, const igp_embed_opts* opts, float* d_out,
         return IGP_ERR_INPUT;
     }
     IGP_TRY(check_opts(opts));
-    return run_embed(g->csr, *opts, d_out, (cudaStream_t)stream, &g->timing);
+    cudaStream_t s = (cudaStream_t)stream;
+    // order the embed behind the build / merge (a no-op wait when it is on the same stream)
+    IGP_CUDA(cudaStreamWaitEvent(s, g->ready, 0), "stream wait");
+    return run_embed(g->csr, *opts, d_out, s);
 }
 
 igp_status igp_embed(igp_graph_t g, float tau, int32_t d, int32_t steps, uint64_t seed, float* d_out,
@@ -267,19 +396,32 @@ igp_status igp_embed(igp_graph_t g, float tau, int32_t d, int32_t steps, uint64_
     return igp_embed_ex(g, &o, d_out, stream);
 }
 
-igp_status igp_last_layer_time_ms(igp_graph_t g, float* total_ms, int32_t* launches) {
-    if (!g || !g->timing.valid) {
-        set_error("no timed embed recorded on this graph");
-        return IGP_ERR_INPUT;
-    }
-    float ms = 0.0f;
-    for (int k = 0; k < g->timing.slices; ++k) {
+igp_status igp_layer_timer_reset(void) {
+    std::lock_guard<std::mutex> lock(g_timer_mu);
+    g_timer_used = 0;
+    return IGP_OK;
+}
+
+igp_status igp_layer_timer_read(float* total_ms, int64_t* launches) {
+    std::lock_guard<std::mutex> lock(g_timer_mu);
+    double ms = 0.0;
+    int64_t nl = 0;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    igp_status st = IGP_OK;
+    for (size_t k = 0; k < g_timer_used && st == IGP_OK; ++k) {
+        TimerEntry* e = g_timer[k];
+        if (e->device != prev) cudaSetDevice(e->device);
         float t = 0.0f;
-        IGP_CUDA(cudaEventElapsedTime(&t, g->timing.ev0[k], g->timing.ev1[k]), "cudaEventElapsedTime");
+        st = cuda_status(cudaEventSynchronize(e->slot.ev1), "cudaEventSynchronize");
+        if (st == IGP_OK) st = cuda_status(cudaEventElapsedTime(&t, e->slot.ev0, e->slot.ev1), "cudaEventElapsedTime");
+        if (e->device != prev && prev >= 0) cudaSetDevice(prev);
         ms += t;
+        nl += e->launches;
     }
-    if (total_ms) *total_ms = ms;
-    if (launches) *launches = g->timing.launches;
+    if (st != IGP_OK) return st;
+    if (total_ms) *total_ms = (float)ms;
+    if (launches) *launches = nl;
     return IGP_OK;
 }
 
@@ -298,17 +440,21 @@ igp_status igp_embed_host(const int32_t* h_edges, int64_t num_edges, int32_t num
     const size_t ob = sizeof(float) * (size_t)num_nodes * (size_t)opts->d;
     IGP_CUDA(alloc_async((void**)&d_edges, eb, s), "edges alloc");
     if (eb) IGP_CUDA(cudaMemcpyAsync(d_edges, h_edges, eb, cudaMemcpyHostToDevice, s), "edges H2D");
+    // everything is enqueued before the single wait at the end
     igp_graph_t g = nullptr;
-    igp_status st = igp_build_graph(d_edges, num_edges, num_nodes, stream, &g);
+    igp_status st = igp_build_graph_ex(d_edges, num_edges, num_nodes, IGP_BUILD_ASYNC, stream, &g);
     free_async(d_edges, s);
     if (st != IGP_OK) return st;
     st = cuda_status(alloc_async((void**)&d_out, ob, s), "out alloc");
     if (st == IGP_OK) st = igp_embed_ex(g, opts, d_out, stream);
     if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(h_out, d_out, ob, cudaMemcpyDeviceToHost, s), "out D2H");
     free_async(d_out, s);
+    // the range check ran with the build (early on `s`); its flag is read after the work is queued
+    if (st == IGP_OK) st = igp_graph_status(g);
+    std::string msg = igp_last_error_message();
+    igp_destroy_graph_async(g, stream);  // its only user is `s`
     igp_status st2 = cuda_status(cudaStreamSynchronize(s), "stream sync");
-    // release the graph without a device-wide sync (its only user, `s`, is drained)
-    release_graph(g, s);
+    if (st != IGP_OK) set_error(msg);
     return st != IGP_OK ? st : st2;
 }
 

@@ -58,14 +58,17 @@ inline igp_status launch_status(const char* what) {
 // ---------------------------------------------------------------------------
 struct CsrDevice {
     int32_t* row_ptr = nullptr;  // [N+1]
-    int32_t* col_idx = nullptr;  // [nnz + kColPad] (pad zero-filled: vector index loads may overrun a row)
+    int32_t* col_idx = nullptr;  // [cap + kColPad] (vector index loads may overrun a row's end)
     int32_t* order = nullptr;    // [N] order[r] = original id of relabelled row r (descending degree)
     int32_t* rp_perm = nullptr;  // [N+1] CSR of the relabelled graph (row r = node order[r]) ...
     int32_t* col_perm = nullptr; // [nnz + kColPad]  ... with relabelled, ascending column ids
+    int32_t* meta = nullptr;     // device [4]: [0] range-error flag (nnz is row_ptr[N])
     bool perm_alias = false;     // no relabelling: rp_perm/col_perm alias row_ptr/col_idx, order = identity
     int32_t n = 0;
-    int64_t nnz = 0;
+    int64_t cap = 0;             // allocated column entries (>= nnz; 2E + base entries before dedup)
 };
+// release every array of c in stream order on s
+void free_csr(const CsrDevice& c, cudaStream_t s);
 constexpr int kColPad = 16;
 // canonical CSR of the new edges, merged with `base` (an existing canonical CSR on the same
 // node set) when base != nullptr
@@ -85,20 +88,23 @@ igp_status launch_philox_normal(uint64_t seed, uint64_t sub, int64_t count, floa
 // embed.cu
 // ---------------------------------------------------------------------------
 constexpr int kMaxSlices = 8;
-struct EmbedTiming {
-    cudaEvent_t ev0[kMaxSlices] = {}, ev1[kMaxSlices] = {};  // around each slice's L filter-step launches
-    int32_t slices = 0;
-    int32_t launches = 0;
-    bool valid = false;
+// process-wide filter-step timer (igp_layer_timer_*): a pair of events per timed slice
+struct TimerSlot {
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
-igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s,
-                     EmbedTiming* timing);
+// an event pair (created on the current device) for `launches` filter steps; nullptr on failure
+TimerSlot* timer_acquire(int64_t launches);
+igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s);
 
 }  // namespace igp
 
 struct igp_graph_s {
     igp::CsrDevice csr;
     bool reorder = true;
-    int64_t m = 0;
-    igp::EmbedTiming timing;
+    bool async = false;        // IGP_BUILD_ASYNC: nnz / range errors resolved lazily
+    int device = 0;
+    cudaEvent_t ready = nullptr;  // recorded after the last build / merge
+    bool resolved = false;     // nnz / err below are valid
+    int64_t nnz = -1;
+    int32_t err = 0;
 };

@@ -332,3 +332,79 @@ def test_add_edges_errors_leave_graph_unchanged(igp):
     assert rp.cpu().tolist() == [0, 2, 4, 5, 6] and ci.cpu().tolist() == [1, 3, 0, 2, 1, 0]
     g.add_edges(torch.zeros((0, 2), dtype=torch.int32, device="cuda"))
     assert g.num_edges == 3
+
+
+# ------------------------------------------------------------------ asynchronous build / release, layer timer
+def test_async_build_same_csr_and_embed(igp):
+    """IGP_BUILD_ASYNC enqueues the whole build with no host sync: the CSR and the embed
+    behind it are identical to the synchronous build's."""
+    c = CONFIGS["medium"]
+    edges, _ = generate(c)
+    e = torch.from_numpy(edges).cuda()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ga = igp.build_graph(e, c.num_nodes, stream=s, async_build=True)
+        za = igp.embed(ga, c.tau, c.d, 5, 0, stream=s)
+        rpa, cia = ga.csr(stream=s)
+    s.synchronize()
+    gs = igp.build_graph(e, c.num_nodes)
+    zs = igp.embed(gs, c.tau, c.d, 5, 0)
+    rps, cis = gs.csr()
+    torch.cuda.synchronize()
+    assert ga.nnz == gs.nnz
+    assert torch.equal(rpa, rps) and torch.equal(cia, cis)
+    assert torch.equal(za, zs)  # bitwise: same kernels, same order
+    ga.close(stream=s)
+    gs.close()
+
+
+def test_async_build_reports_range_error_lazily(igp):
+    e = torch.tensor([[0, 1], [2, 7], [1, 2]], dtype=torch.int32, device="cuda")
+    g = igp.build_graph(e, 5, async_build=True)  # returns before the range check is read
+    with pytest.raises(igp.IGPError) as ei:
+        g.status()
+    assert ei.value.status == 2
+    with pytest.raises(igp.IGPError):
+        _ = g.nnz
+    g.close(stream=torch.cuda.current_stream())
+    # an asynchronous merge of a bad batch is reported the same way
+    g = igp.build_graph(torch.tensor([[0, 1]], dtype=torch.int32, device="cuda"), 4, async_build=True)
+    g.status()
+    g.add_edges(torch.tensor([[0, 9]], dtype=torch.int32, device="cuda"))
+    with pytest.raises(igp.IGPError):
+        g.status()
+    g.close()
+
+
+def test_async_streaming_merge_matches_oracle(igp):
+    """The streaming config's 10 merges, all asynchronous (no host sync until the end)."""
+    from synth.dcsbm import stream_batches
+    c = CONFIGS["streaming"]
+    edges, _ = generate(c)
+    batches = [torch.from_numpy(b).cuda() for b in stream_batches(edges, 10)]
+    g = igp.build_graph(batches[0], c.num_nodes, async_build=True)
+    for b in batches[1:]:
+        g.add_edges(b)
+    rp, ci = g.csr()
+    rp_o, ci_o, m_o = oracle.build_csr(edges, c.num_nodes)
+    assert g.num_edges == m_o
+    assert np.array_equal(rp.cpu().numpy(), rp_o) and np.array_equal(ci.cpu().numpy(), ci_o)
+    g.close()
+
+
+def test_layer_timer_accumulates_without_sync(igp):
+    c = CONFIGS["tiny"]
+    edges, _ = generate(c)
+    e = torch.from_numpy(edges).cuda()
+    igp.layer_timer_reset()
+    assert igp.layer_timer_read() == (0.0, 0)
+    s = torch.cuda.current_stream()
+    for k in range(3):
+        g = igp.build_graph(e, c.num_nodes, stream=s, async_build=True)
+        igp.embed(g, c.tau, c.d, c.steps, k, stream=s, time_layers=True)
+        g.close(stream=s)
+    ms, launches = igp.layer_timer_read()
+    assert launches % c.steps == 0  # L launches per timed column slice
+    assert launches >= 3 * c.steps and ms > 0.0
+    igp.layer_timer_reset()
+    assert igp.layer_timer_read() == (0.0, 0)

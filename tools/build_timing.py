@@ -45,10 +45,11 @@ for tl in (True, False, True):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     g = igp.build_graph(e, cfg.num_nodes)
+    igp.layer_timer_reset()
     igp.embed(g, cfg.tau, cfg.d, cfg.steps, 0, out=out, time_layers=tl)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     if tl:
-        print("layer ms", g.last_layer_time_ms())
+        print("layer ms", igp.layer_timer_read())
     g.close()
     print(f"[time_layers={tl}] step {1e3*(t1-t0):7.2f} ms")

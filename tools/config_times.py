@@ -29,12 +29,13 @@ for name in names:
         a.record()
         g = igp.build_graph(e, cfg.num_nodes)
         b.record()
+        igp.layer_timer_reset()
         igp.embed(g, cfg.tau, cfg.d, cfg.steps, 0, out=out, time_layers=True)
         c.record()
         torch.cuda.synchronize()
         bms.append(a.elapsed_time(b))
         ems.append(b.elapsed_time(c))
-        lms, nl = g.last_layer_time_ms()
+        lms, nl = igp.layer_timer_read()
         nnz = g.nnz
         g.close()
     em = sorted(ems)[len(ems) // 2]

@@ -39,9 +39,10 @@ for w, occ, env in [(w, o, e) for w in widths for o in occs for e in envs]:
     t1.record()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / reps
+    igp.layer_timer_reset()
     igp.embed(g, cfg.tau, cfg.d, cfg.steps, 0, out=out, time_layers=True)
     torch.cuda.synchronize()
-    lms, nl = g.last_layer_time_ms()
+    lms, nl = igp.layer_timer_read()
     if ref is None:
         ref = out.clone()
     diff = float((out - ref).abs().max())

@@ -11,6 +11,6 @@ for L, tl in ((60, False), (60, True), (60, False), (30, False), (10, False)):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); igp.embed(g, cfg.tau, cfg.d, L, 0, out=out, time_layers=tl); b.record(); torch.cuda.synchronize()
-    extra = g.last_layer_time_ms() if tl else ""
+    igp.layer_timer_reset(); a.record(); igp.embed(g, cfg.tau, cfg.d, L, 0, out=out, time_layers=tl); b.record(); torch.cuda.synchronize()
+    extra = igp.layer_timer_read() if tl else ""
     print("L", L, "timed", tl, "embed ms", a.elapsed_time(b), "wall", 1e3 * (time.perf_counter() - t0), extra, flush=True)
