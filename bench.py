@@ -242,11 +242,15 @@ def run_gpu(args, cfg):
     launches0 = igp.kernel_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev0.record(stream)
-    for _ in range(args.steps):
+    for k in range(args.steps):
         step(True)
+        step_ev[k].record(stream)
     ev1.record(stream)
     barrier()
+    log(f"[rank {rank}] per-step ms: " + " ".join(
+        f"{(ev0 if k == 0 else step_ev[k - 1]).elapsed_time(step_ev[k]):.2f}" for k in range(args.steps)))
     launches = igp.kernel_launch_count() - launches0
     clock_rec = clocks.stop()
     ms_total = ev0.elapsed_time(ev1)

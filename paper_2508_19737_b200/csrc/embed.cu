@@ -249,14 +249,16 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
     constexpr int NG = kWarps * G;            // row groups per block
     constexpr int OC = W >= 32 ? W / 32 : 1;  // statistics columns owned per lane
     constexpr int OR = W >= 32 ? G : G / 2;   // ... each over OR rows of the warp tile
-    __shared__ double2 st[W];                 // (mu, 1/sigma) of the previous step
-    __shared__ __align__(16) float stage[kWarps][G * W];
+    constexpr int TS = W + 4;                 // tile row stride (floats): conflict-free staging
+    __shared__ double2 st[W + W / 8];         // (mu, 1/sigma) of the previous step, column c at c + c/8
+    __shared__ __align__(16) float stage[kWarps][G * TS];
     extern __shared__ double dyn_smem[];
     double (*acc_f)[W] = reinterpret_cast<double (*)[W]>(dyn_smem);  // [NG][W] long-row partials
     for (int c = threadIdx.x; c < W; c += kThreads) {
         double m = 0.0, is = 1.0;
         if (p.sums_in) column_stats(p.sums_in, c, W, p.n, m, is);
-        st[c] = make_double2(m, is);
+        st[c + c / 8] = make_double2(m, is);  // one pad slot per 8 columns: the 8-column groups of the
+                                              // lanes of a row start in distinct banks
     }
     for (int t = threadIdx.x; t < NG * W; t += kThreads) (&acc_f[0][0])[t] = 0.0;
     __syncthreads();
@@ -277,18 +279,32 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
     for (int k = 0; k < OC; ++k) s1[k] = s2[k] = 0.0;
 
     const int64_t step = (int64_t)gridDim.x * NG;
+    // The row-pointer -> index -> gather chain of a row batch is started one batch ahead:
+    // the next batch's row pointers are loaded when a batch begins, and its first index
+    // chunk once the batch's first gathers are in flight (nbeg/nend/jfirst).
+    int64_t base = (int64_t)blockIdx.x * NG + warp * G;
+    int32_t nbeg = 0, nend = 0;
+    int jfirst[IPL];
+    if (base + g < p.n) {
+        nbeg = __ldg(p.rp + base + g);
+        nend = __ldg(p.rp + base + g + 1);
+    }
+    load_idx<IPL>(p.ci, nbeg & ~3, nend, q, pol_idx, jfirst);
     // warp-uniform batches of G consecutive rows of the relabelled (degree-sorted) CSR
-    for (int64_t base = (int64_t)blockIdx.x * NG + warp * G; base < p.n; base += step) {
+    for (; base < p.n; base += step) {
         const int32_t row = (int32_t)(base + g);
         const bool valid = row < p.n;
         float t8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        int32_t beg = 0, end = 0;
+        const int32_t beg = nbeg, end = nend;
         const uint64_t* own_ptr = yin + ((size_t)row * LPR + q) * 4;
         if (valid) {
-            beg = __ldg(p.rp + row);
-            end = __ldg(p.rp + row + 1);
             prefetch_l2(own_ptr);  // the row's own values are needed only after its gathers
             prefetch_l2(p.node + row);
+        }
+        nbeg = nend = 0;
+        if (base + step + g < p.n) {
+            nbeg = __ldg(p.rp + base + step + g);
+            nend = __ldg(p.rp + base + step + g + 1);
         }
         // neighbour sum: packed fp32 within up to kFoldChunks chunks, then folded into
         // fp64 partials in shared memory (only rows longer than 64 neighbours fold).
@@ -303,7 +319,9 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
         const int nch = end > beg ? (end - start + kChunk - 1) / kChunk : 0;
         const int max_nch = __reduce_max_sync(kFull, nch);
         int jr[IPL];
-        load_idx<IPL>(p.ci, start, end, q, pol_idx, jr);
+#pragma unroll
+        for (int k = 0; k < IPL; ++k) jr[k] = jfirst[k];
+        if (max_nch == 0) load_idx<IPL>(p.ci, nbeg & ~3, nend, q, pol_idx, jfirst);
         for (int c = 0; c < max_nch; ++c) {
             const int32_t e0 = start + c * kChunk, e1 = e0 + kChunk;
             int jn[IPL];
@@ -344,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
                         for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[t][k]);
                 }
             }
+            if (c == 0) load_idx<IPL>(p.ci, nbeg & ~3, nend, q, pol_idx, jfirst);  // next batch's first chunk
             if (++nc == kFoldChunks && e1 < end) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -384,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
                 float yy[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const double2 m = st[8 * q + 2 * k + h];
+                    const double2 m = st[9 * q + 2 * k + h];
                     const float tself = (h ? y.y : y.x) * nd.y;  // t_i = y_i / s_i
                     const double P =
                         ((double)p.theta * (double)tself + (double)p.alpha * si * ad[2 * k + h] - m.x * cc) * m.y;
@@ -398,16 +417,31 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
         }
         if (!p.linear) {
             // stage the warp's G x W tile of t (invalid rows contribute 0) and fold owned columns
-            *reinterpret_cast<float4*>(tile + g * W + 8 * q) = make_float4(t8[0], t8[1], t8[2], t8[3]);
-            *reinterpret_cast<float4*>(tile + g * W + 8 * q + 4) = make_float4(t8[4], t8[5], t8[6], t8[7]);
+            // lanes with (q & 4) store their upper half first, so each 8-lane store phase covers
+            // all 32 banks once (rows are TS = W + 4 floats apart)
+            const float4 lo4 = make_float4(t8[0], t8[1], t8[2], t8[3]), hi4 = make_float4(t8[4], t8[5], t8[6], t8[7]);
+            const bool swap = (q & 4) != 0;
+            *reinterpret_cast<float4*>(tile + g * TS + 8 * q + (swap ? 4 : 0)) = swap ? hi4 : lo4;
+            *reinterpret_cast<float4*>(tile + g * TS + 8 * q + (swap ? 0 : 4)) = swap ? lo4 : hi4;
             __syncwarp();
 #pragma unroll
             for (int r = 0; r < OR; ++r) {
+                float x[OC];
+                const float* src = tile + (or0 + r) * TS + oc0;
+                if constexpr (OC == 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(src);
+                    x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+                } else if constexpr (OC == 2) {
+                    const float2 v = *reinterpret_cast<const float2*>(src);
+                    x[0] = v.x, x[1] = v.y;
+                } else {
+                    x[0] = *src;
+                }
 #pragma unroll
                 for (int k = 0; k < OC; ++k) {
-                    const double x = (double)tile[(or0 + r) * W + oc0 + k];
-                    s1[k] += grid_round(x, p.grid_c);
-                    s2[k] += grid_round(x * x, p.grid_c);
+                    const double xd = (double)x[k];
+                    s1[k] += grid_round(xd, p.grid_c);
+                    s2[k] += grid_round(xd * xd, p.grid_c);
                 }
             }
             __syncwarp();
@@ -643,6 +677,7 @@ igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cu
 #define IGP_W_CASE(WW)                                                      \
     case WW:                                                                \
         if (occ == 3) return run_embed_w<WW, 3>(g, o, out, s, di); \
+        if (occ == 4) return run_embed_w<WW, 4>(g, o, out, s, di); \
         return run_embed_w<WW, 2>(g, o, out, s, di);
     switch (choose_width(o.d, g.n, g.cap)) {  // a heuristic: cap ~ nnz (the output does not depend on W)
         IGP_W_CASE(16)

@@ -15,6 +15,25 @@ from synth.dcsbm import CONFIGS, generate  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "headline"]
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+mode = sys.argv[3] if len(sys.argv) > 3 else ""  # "smi": nvidia-smi -lms 100 running; "nvml": pynvml polling
+if mode == "smi":
+    import subprocess
+    smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,clocks_event_reasons.active", "--format=csv",
+                            "-lms", "100", "-i", "0"], stdout=subprocess.DEVNULL)
+    time.sleep(1.0)
+elif mode == "nvml":
+    import threading
+    import pynvml
+    pynvml.nvmlInit()
+    hnd = pynvml.nvmlDeviceGetHandleByIndex(0)
+    stop = []
+
+    def poll():
+        while not stop:
+            pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(hnd)
+            time.sleep(0.1)
+    threading.Thread(target=poll, daemon=True).start()
 edges, _ = generate(cfg)
 e = torch.from_numpy(edges).cuda()
 N, d, L, tau = cfg.num_nodes, cfg.d, cfg.steps, cfg.tau
@@ -28,7 +47,7 @@ for k in range(steps):
     g = igp.build_graph(e, N, stream=s, async_build=True)
     t1 = time.perf_counter()
     ev[1].record(s)
-    igp.embed(g, tau, d, L, 0, out=out, stream=s)
+    igp.embed(g, tau, d, L, 0, out=out, stream=s, time_layers=(mode != ""))
     t2 = time.perf_counter()
     ev[2].record(s)
     g.close(stream=s)
