@@ -231,11 +231,14 @@ def test_headline_csr_bit_exact(igp, headline):
     check_csr(igp, edges, c.num_nodes)
 
 
-def test_headline_parity_reduced_steps(igp, headline):
-    """Full N / nnz / d, the same kernels and grid as bench.py; L reduced so the
-    fp64 oracle finishes in the test budget (IGP_FULL_PARITY=1 runs L = 60)."""
+QUICK = os.environ.get("IGP_QUICK") == "1"  # development runs: reduced L at the full sizes
+
+
+def test_headline_parity_full_steps(igp, headline):
+    """The bench workload itself: full N / nnz / d / L = 60, the same kernels and grid as
+    bench.py, element by element against the fp64 oracle (IGP_QUICK=1: L = 3)."""
     c, edges = headline
-    L = c.steps if os.environ.get("IGP_FULL_PARITY") == "1" else 3
+    L = 3 if QUICK else c.steps
     z, ref = run_parity(igp, edges, c.num_nodes, c.d, L, c.tau)
     err = row_rel_err(z, ref)
     record(f"headline_L{L}", err)
@@ -408,3 +411,52 @@ def test_layer_timer_accumulates_without_sync(igp):
     assert launches >= 3 * c.steps and ms > 0.0
     igp.layer_timer_reset()
     assert igp.layer_timer_read() == (0.0, 0)
+
+
+# ------------------------------------------------------------------ Large config (5M nodes, d = 128)
+@pytest.fixture(scope="module")
+def large(igp):
+    c = CONFIGS["large"]
+    edges, _ = generate(c)
+    return c, edges
+
+
+def test_large_csr_bit_exact(igp, large):
+    c, edges = large
+    check_csr(igp, edges, c.num_nodes)
+
+
+def test_large_parity_reduced_steps(igp, large):
+    """Full N = 5M / nnz ~ 200M / d = 128 with the bench's kernels and grid; L = 2 so the fp64
+    oracle (~10x the headline's work per layer) fits the test budget."""
+    c, edges = large
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, 2, c.tau)
+    err = row_rel_err(z, ref)
+    record("large_L2", err)
+    assert err <= TOL
+
+
+def test_large_full_steps_with_and_without_reordering(igp, large):
+    """L = 60 at full size, with and without the degree-sorted relabelling (config 5): both
+    runs are deterministic, in (0, 1), standardised before the sigmoid, and agree with each
+    other to the parity tolerance (they differ only in fp32 summation order)."""
+    c, edges = large
+    e = torch.from_numpy(edges).cuda()
+    zs = []
+    for reorder in (True, False):
+        g = igp.build_graph(e, c.num_nodes, reorder=reorder)
+        z1 = igp.embed(g, c.tau, c.d, c.steps, 0)
+        z2 = igp.embed(g, c.tau, c.d, c.steps, 0)
+        assert torch.equal(z1, z2)
+        assert float(z1.min()) > 0 and float(z1.max()) < 1
+        pre = igp.embed(g, c.tau, c.d, c.steps, 0, mode="pre_sigmoid").double()
+        assert torch.allclose(pre.mean(0), torch.zeros(c.d, dtype=torch.float64, device=pre.device), atol=1e-4)
+        assert torch.allclose(pre.std(0, unbiased=False), torch.ones(c.d, dtype=torch.float64, device=pre.device),
+                              atol=1e-4)
+        del pre
+        g.close()
+        zs.append(z1.cpu().numpy())
+        del z1, z2
+    err = row_rel_err(zs[1], zs[0].astype(np.float64))
+    record("large_L60_reorder_vs_not", err)
+    assert err <= TOL
