@@ -81,18 +81,26 @@ typedef enum {
 IGP_API igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes,
                            igp_stream_t stream, igp_graph_t* out);
 
-#define IGP_BUILD_DEFAULT 0u
-#define IGP_BUILD_NO_REORDER 1u /* keep the original node order for the filter steps (no degree-sorted
-                                   relabelling; results differ only by fp32 summation order) */
+#define IGP_BUILD_DEFAULT 0u    /* row order chosen by size: IGP_BUILD_REORDER_COMMUNITY when a 32-column
+                                   feature slice (N x 128 B) exceeds half the L2, else IGP_BUILD_REORDER_DEGREE */
+#define IGP_BUILD_NO_REORDER 1u /* keep the original node order for the filter steps (no relabelling;
+                                   results differ only by fp32 summation order) */
+#define IGP_BUILD_REORDER_DEGREE 8u /* rows by descending degree (ties by ascending id) */
+#define IGP_BUILD_REORDER_COMMUNITY 4u /* rows grouped by label-propagation communities (10 synchronous
+                                   sweeps, mode of <= 31 neighbour labels and the node's own, ties to the
+                                   smallest label), descending degree within a community: neighbour gathers
+                                   stay local in L2 on graphs whose feature slice exceeds it.
+                                   At most one of NO_REORDER / REORDER_DEGREE / REORDER_COMMUNITY. */
 #define IGP_BUILD_ASYNC 2u      /* fully asynchronous build (and later igp_graph_add_edges): the call
                                    returns after enqueueing; a range error is reported by the first
                                    igp_graph_status / igp_graph_info / igp_graph_copy_csr call, which
                                    waits for the build.  Embeds may be enqueued behind it right away. */
 
 /* As igp_build_graph; `flags` selects the filter steps' row order and the synchronisation.
- * By default the handle also holds a relabelled copy of the CSR with rows by descending
- * degree (ties by ascending id), which the embed kernels traverse; IGP_BUILD_NO_REORDER
- * skips it.  Unknown flags -> IGP_ERR_INPUT. */
+ * Unless IGP_BUILD_NO_REORDER is given, the handle also holds a relabelled copy of the CSR
+ * (rows in the chosen order, each row's neighbours in canonical order) which the embed kernels
+ * traverse; the canonical CSR, the output row order and the results' meaning do not change.
+ * Unknown or conflicting flags -> IGP_ERR_INPUT. */
 IGP_API igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes, uint32_t flags,
                                       igp_stream_t stream, igp_graph_t* out);
 

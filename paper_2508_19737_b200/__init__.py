@@ -183,21 +183,28 @@ class Graph:
 
 BUILD_NO_REORDER = 1
 BUILD_ASYNC = 2
+BUILD_REORDER_COMMUNITY = 4
+BUILD_REORDER_DEGREE = 8
+ORDERS = {"auto": 0, "none": BUILD_NO_REORDER, "degree": BUILD_REORDER_DEGREE, "community": BUILD_REORDER_COMMUNITY}
 
 
 def build_graph(edges: torch.Tensor, num_nodes: int, stream=None, reorder: bool = True,
-                async_build: bool = False) -> Graph:
+                async_build: bool = False, order: str | None = None) -> Graph:
     """igp_build_graph_ex: canonical CSR of the undirected simple graph.
 
     ``edges``: CUDA int32 tensor [E, 2] (duplicates / both orientations / self loops allowed).
-    ``reorder=False`` keeps the original row order for the filter steps (IGP_BUILD_NO_REORDER).
+    ``order``: row order of the filter steps: "auto" (default: "community" once N x 128 B
+    exceeds half the L2, else "degree"), "degree" (IGP_BUILD_REORDER_DEGREE), "community"
+    (IGP_BUILD_REORDER_COMMUNITY) or "none" (IGP_BUILD_NO_REORDER; also ``reorder=False``).
     ``async_build=True`` returns without any host sync (IGP_BUILD_ASYNC); range errors surface
     from ``Graph.status()`` / ``nnz``."""
     _require_cuda(edges, torch.int32, "edges")
     if edges.dim() != 2 or edges.shape[1] != 2:
         raise ValueError("edges must have shape [E, 2]")
     h = _P()
-    flags = (0 if reorder else BUILD_NO_REORDER) | (BUILD_ASYNC if async_build else 0)
+    if order is None:
+        order = "auto" if reorder else "none"
+    flags = ORDERS[order] | (BUILD_ASYNC if async_build else 0)
     with torch.cuda.device(edges.device):
         _check(_lib.igp_build_graph_ex(ctypes.c_void_p(edges.data_ptr()), edges.shape[0], int(num_nodes),
                                        flags, _stream_ptr(stream), ctypes.byref(h)))

@@ -492,6 +492,60 @@ __global__ void iota_kernel(int32_t* __restrict__ a, int32_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) a[i] = (int32_t)i;
 }
 
+// ---------------------------------------------------------------- B7 community row order (optional)
+// Label propagation, one warp per row: the new label of row r is the most frequent label among
+// its first (up to) 31 neighbours (canonical order) and r itself, ties to the smallest label.
+// Synchronous sweeps (lin -> lout) make the result independent of scheduling.
+__global__ void __launch_bounds__(256) label_prop_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                         int32_t n, const int32_t* __restrict__ lin,
+                                                         int32_t* __restrict__ lout) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
+        const int32_t beg = rp[r];
+        const int len = min(rp[r + 1] - beg, 31);
+        const bool act = lane <= len;
+        int32_t lab = INT_MAX;
+        if (lane < len) lab = lin[ci[beg + lane]];
+        else if (lane == len) lab = lin[r];
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        int cnt = 0;
+        if (act) cnt = __popc(__match_any_sync(am, lab));
+        const int best = __reduce_max_sync(0xffffffffu, cnt);
+        const int32_t l = __reduce_min_sync(0xffffffffu, (act && cnt == best) ? lab : INT_MAX);
+        if (lane == 0) lout[r] = l;
+    }
+}
+
+// bucket nodes by label; the bucket entries are the nodes' ranks in the degree order
+__global__ void label_count_kernel(const int32_t* __restrict__ lab, int32_t n, int32_t* __restrict__ cnt) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(cnt + lab[i], 1);
+}
+
+__global__ void label_scatter_kernel(const int32_t* __restrict__ lab, const int32_t* __restrict__ rank, int32_t n,
+                                     const int32_t* __restrict__ off, int32_t* __restrict__ fill,
+                                     int32_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int32_t l = lab[i];
+        out[off[l] + atomicAdd(fill + l, 1)] = rank[i];
+    }
+}
+
+// order[k] = deg_order[sorted rank k]: communities by label, descending degree within each
+__global__ void gather_order_kernel(const int32_t* __restrict__ deg_order, const int32_t* __restrict__ ranks, int32_t n,
+                                    int32_t* __restrict__ order) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += stride) order[k] = deg_order[ranks[k]];
+}
+
+// rank[order[r]] = r
+__global__ void rank_kernel(const int32_t* __restrict__ order, int32_t n, int32_t* __restrict__ rank) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += stride) rank[order[r]] = (int32_t)r;
+}
+
 void free_csr(const CsrDevice& c, cudaStream_t s) {
     free_async(c.row_ptr, s);
     free_async(c.col_idx, s);
@@ -503,8 +557,10 @@ void free_csr(const CsrDevice& c, cudaStream_t s) {
     }
 }
 
-igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder, cudaStream_t s, CsrDevice* out,
-                     const CsrDevice* base) {
+igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_order, cudaStream_t s,
+                     CsrDevice* out, const CsrDevice* base) {
+    const bool reorder = row_order != kOrderNone;
+    const bool community = row_order == kOrderCommunity;
     DeviceInfo di;
     if (!device_info(&di)) return IGP_ERR_CUDA;
     // both orientations of the new edges (before dedup / self-loop removal), plus the base rows
@@ -530,7 +586,10 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder,
     size_t o_degp = al(o_inv + sizeof(int32_t) * (size_t)n);
     size_t o_bitmap = al(o_degp + sizeof(int32_t) * (size_t)n);
     size_t o_tmp = al(o_bitmap + sizeof(uint32_t) * (size_t)words * kGiantBlocks);
-    size_t total = o_tmp + sizeof(int32_t) * (size_t)(raw > 0 ? raw : 1);
+    size_t o_comm = al(o_tmp + sizeof(int32_t) * (size_t)(raw > 0 ? raw : 1));
+    // community order: two label buffers, label bucket offsets / fill, bucketed ranks, degree order
+    const size_t comm_bytes = community ? al(sizeof(int32_t) * (size_t)n) * 5 + al(sizeof(int32_t) * ((size_t)n + 1)) : 0;
+    size_t total = o_comm + comm_bytes;
     char* ws = nullptr;
     IGP_CUDA(alloc_async((void**)&ws, total, s), "build workspace alloc");
     int32_t* cnt = (int32_t*)(ws + o_cnt);
@@ -632,15 +691,52 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, bool reorder,
     degree_scatter_kernel<<<(n + kSchedTile - 1) / kSchedTile, 256, 0, s>>>(c.row_ptr, n, fill, c.order);
     IGP_STEP(launch_status("degree_scatter_kernel"));
     IGP_STEP(segmented_sort(boff, c.order, hist, kDegBuckets, n, n, sc, s, di));
-    // B6b: the relabelled CSR the filter steps run on (rows by descending degree)
+    if (community) {
+        // B7: label-propagation communities, rows grouped by label (descending degree within)
+        const size_t nb = al(sizeof(int32_t) * (size_t)n);
+        int32_t* lab0 = (int32_t*)(ws + o_comm);
+        int32_t* lab1 = (int32_t*)(ws + o_comm + nb);
+        int32_t* lfill = (int32_t*)(ws + o_comm + 2 * nb);
+        int32_t* lranks = (int32_t*)(ws + o_comm + 3 * nb);
+        int32_t* dorder = (int32_t*)(ws + o_comm + 4 * nb);
+        int32_t* loff = (int32_t*)(ws + o_comm + 5 * nb);
+        const int ng = grid_for(n, 256, di.num_sms, 8);
+        iota_kernel<<<ng, 256, 0, s>>>(lab0, n);
+        IGP_STEP(launch_status("iota_kernel"));
+        for (int it = 0; it < kLabelPropIters; ++it) {
+            label_prop_kernel<<<grid_for((int64_t)n * 32, 256, di.num_sms, 8), 256, 0, s>>>(c.row_ptr, c.col_idx, n,
+                                                                                            lab0, lab1);
+            IGP_STEP(launch_status("label_prop_kernel"));
+            int32_t* t = lab0;
+            lab0 = lab1;
+            lab1 = t;
+        }
+        rank_kernel<<<ng, 256, 0, s>>>(c.order, n, inv);  // rank in the degree order
+        IGP_STEP(launch_status("rank_kernel"));
+        IGP_STEP(cuda_status(cudaMemsetAsync(lab1, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
+        label_count_kernel<<<ng, 256, 0, s>>>(lab0, n, lab1);
+        IGP_STEP(launch_status("label_count_kernel"));
+        IGP_STEP(scan_exclusive(lab1, loff, n, s));
+        IGP_STEP(cuda_status(cudaMemsetAsync(lfill, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
+        label_scatter_kernel<<<ng, 256, 0, s>>>(lab0, inv, n, loff, lfill, lranks);
+        IGP_STEP(launch_status("label_scatter_kernel"));
+        IGP_STEP(segmented_sort(loff, lranks, lab1, n, n, n, sc, s, di));  // ranks unique: no entry dropped
+        IGP_STEP(cuda_status(cudaMemcpyAsync(dorder, c.order, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s),
+                             "copy"));
+        gather_order_kernel<<<ng, 256, 0, s>>>(dorder, lranks, n, c.order);
+        IGP_STEP(launch_status("gather_order_kernel"));
+    }
+    // B6b: the relabelled CSR the filter steps run on (rows by descending degree, or by community)
     inverse_perm_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n, inv, c.row_ptr, degp);
     IGP_STEP(launch_status("inverse_perm_kernel"));
     IGP_STEP(scan_exclusive(degp, c.rp_perm, n, s));
     IGP_STEP(cuda_status(cudaMemsetAsync(c.rp_perm + n + 1, 0, 4 * sizeof(int32_t), s), "pad memset"));
     if (raw > 0) {
+        // each relabelled row keeps its canonical neighbour order (ascending original id), so a
+        // row's summation order is the same under any permutation (up to where the 64-neighbour
+        // fp64 folds of rows longer than 60 fall); no re-sort is needed
         perm_scatter_kernel<<<rg, 256, 0, s>>>(c.order, inv, c.row_ptr, c.col_idx, c.rp_perm, c.col_perm, n);
         IGP_STEP(launch_status("perm_scatter_kernel"));
-        IGP_STEP(segmented_sort(c.rp_perm, c.col_perm, ucnt, n, raw, n, sc, s, di));
     }
 #undef IGP_STEP
     free_async(ws, s);

@@ -209,9 +209,12 @@ igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, int32_t nu
 igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t num_nodes, uint32_t flags,
                               igp_stream_t stream, igp_graph_t* out) {
     set_error("");
-    if (flags & ~(uint32_t)(IGP_BUILD_NO_REORDER | IGP_BUILD_ASYNC)) {
+    const uint32_t order_flags = flags & (IGP_BUILD_NO_REORDER | IGP_BUILD_REORDER_DEGREE | IGP_BUILD_REORDER_COMMUNITY);
+    if ((flags & ~(uint32_t)(IGP_BUILD_NO_REORDER | IGP_BUILD_ASYNC | IGP_BUILD_REORDER_COMMUNITY |
+                             IGP_BUILD_REORDER_DEGREE)) ||
+        (order_flags & (order_flags - 1))) {
         if (out) *out = nullptr;
-        set_error("unknown build flags");
+        set_error("unknown or conflicting build flags");
         return IGP_ERR_INPUT;
     }
     if (!out) {
@@ -234,11 +237,26 @@ igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t
     igp_graph_s* g = new (std::nothrow) igp_graph_s();
     if (!g) return IGP_ERR_OOM;
     cudaStream_t s = (cudaStream_t)stream;
-    g->reorder = (flags & IGP_BUILD_NO_REORDER) == 0;
+    if (flags & IGP_BUILD_NO_REORDER) {
+        g->order = kOrderNone;
+    } else if (flags & IGP_BUILD_REORDER_COMMUNITY) {
+        g->order = kOrderCommunity;
+    } else if (flags & IGP_BUILD_REORDER_DEGREE) {
+        g->order = kOrderDegree;
+    } else {
+        // default: communities once a 32-column slice of the features no longer fits half the L2
+        // (measured: headline +2%, Large +20% per step incl. the build)
+        DeviceInfo di;
+        if (!device_info(&di)) {
+            delete g;
+            return IGP_ERR_CUDA;
+        }
+        g->order = (double)num_nodes * 128.0 > 0.5 * (double)di.l2_bytes ? kOrderCommunity : kOrderDegree;
+    }
     g->async = (flags & IGP_BUILD_ASYNC) != 0;
     igp_status st = cuda_status(cudaGetDevice(&g->device), "cudaGetDevice");
     if (st == IGP_OK) st = cuda_status(cudaEventCreateWithFlags(&g->ready, cudaEventDisableTiming), "event");
-    if (st == IGP_OK) st = build_csr(d_edges, num_edges, num_nodes, g->reorder, s, &g->csr);
+    if (st == IGP_OK) st = build_csr(d_edges, num_edges, num_nodes, g->order, s, &g->csr);
     if (st != IGP_OK) {
         if (g->ready) cudaEventDestroy(g->ready);
         delete g;
@@ -277,7 +295,7 @@ igp_status igp_graph_add_edges(igp_graph_t g, const int32_t* d_edges, int64_t nu
     // the merge reads the current CSR: order it behind the build / merge that wrote it
     IGP_CUDA(cudaStreamWaitEvent(s, g->ready, 0), "stream wait");
     CsrDevice merged;
-    IGP_TRY(build_csr(d_edges, num_edges, g->csr.n, g->reorder, s, &merged, &g->csr));
+    IGP_TRY(build_csr(d_edges, num_edges, g->csr.n, g->order, s, &merged, &g->csr));
     IGP_CUDA(cudaEventRecord(g->ready, s), "event record");
     if (!g->async) {
         // check the merge before replacing the graph: on a range error g stays as it was

@@ -70,9 +70,12 @@ struct CsrDevice {
 // release every array of c in stream order on s
 void free_csr(const CsrDevice& c, cudaStream_t s);
 constexpr int kColPad = 16;
+// row order of the relabelled CSR the filter steps traverse
+enum RowOrder { kOrderNone = 0, kOrderDegree = 1, kOrderCommunity = 2 };
+constexpr int kLabelPropIters = 10;  // label-propagation sweeps of the community order
 // canonical CSR of the new edges, merged with `base` (an existing canonical CSR on the same
 // node set) when base != nullptr
-igp_status build_csr(const int32_t* d_edges, int64_t num_edges, int32_t n, bool reorder, cudaStream_t s,
+igp_status build_csr(const int32_t* d_edges, int64_t num_edges, int32_t n, RowOrder order, cudaStream_t s,
                      CsrDevice* out, const CsrDevice* base = nullptr);
 
 // exclusive scan of n int32 counts: out[0..n], out[n] = total (int32 range checked by caller)
@@ -100,7 +103,7 @@ igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cu
 
 struct igp_graph_s {
     igp::CsrDevice csr;
-    bool reorder = true;
+    igp::RowOrder order = igp::kOrderDegree;
     bool async = false;        // IGP_BUILD_ASYNC: nnz / range errors resolved lazily
     int device = 0;
     cudaEvent_t ready = nullptr;  // recorded after the last build / merge

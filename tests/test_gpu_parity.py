@@ -260,6 +260,36 @@ def test_headline_full_steps_properties(igp, headline):
                           atol=1e-4)
 
 
+# ------------------------------------------------------------------ community row order (IGP_BUILD_REORDER_COMMUNITY)
+@pytest.mark.parametrize("cfg", ["tiny", "medium"])
+def test_embed_community_order(igp, cfg):
+    """The label-propagation row order changes only where rows sit (and so fp32 summation
+    order): the canonical CSR is unchanged and the embedding matches the oracle."""
+    c = CONFIGS[cfg]
+    edges, _ = generate(c)
+    e = torch.from_numpy(edges).cuda()
+    g = igp.build_graph(e, c.num_nodes, order="community")
+    rp, ci = g.csr()
+    rp_o, ci_o, _ = oracle.build_csr(edges, c.num_nodes)
+    assert np.array_equal(rp.cpu().numpy(), rp_o) and np.array_equal(ci.cpu().numpy(), ci_o)
+    z = igp.embed(g, c.tau, c.d, c.steps, 0).cpu().numpy()
+    z2 = igp.embed(igp.build_graph(e, c.num_nodes, order="community"), c.tau, c.d, c.steps, 0).cpu().numpy()
+    assert np.array_equal(z, z2)  # the order (and so the output) is deterministic
+    ref = oracle.embed(rp_o, ci_o, c.num_nodes, c.d, c.steps, c.tau, seed=0, nthreads=NTHREADS)
+    err = row_rel_err(z, ref)
+    record(f"{cfg}_community_order", err)
+    assert err <= TOL
+
+
+def test_community_order_flag_conflict(igp):
+    import ctypes
+    h = ctypes.c_void_p()
+    e = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+    st = igp.lib().igp_build_graph_ex(ctypes.c_void_p(e.data_ptr()), 1, 2, igp.BUILD_NO_REORDER |
+                                      igp.BUILD_REORDER_COMMUNITY, None, ctypes.byref(h))
+    assert st == 2
+
+
 # ------------------------------------------------------------------ row order (IGP_BUILD_NO_REORDER)
 @pytest.mark.parametrize("cfg", ["tiny", "medium"])
 def test_embed_without_relabelling(igp, cfg):
@@ -437,14 +467,15 @@ def test_large_parity_reduced_steps(igp, large):
 
 
 def test_large_full_steps_with_and_without_reordering(igp, large):
-    """L = 60 at full size, with and without the degree-sorted relabelling (config 5): both
-    runs are deterministic, in (0, 1), standardised before the sigmoid, and agree with each
-    other to the parity tolerance (they differ only in fp32 summation order)."""
+    """L = 60 at full size with the community order (the default here), the degree-sorted
+    relabelling and no relabelling (config 5): every run is deterministic, in (0, 1),
+    standardised before the sigmoid, and they agree with each other to the parity tolerance
+    (they differ only in fp32 summation order)."""
     c, edges = large
     e = torch.from_numpy(edges).cuda()
     zs = []
-    for reorder in (True, False):
-        g = igp.build_graph(e, c.num_nodes, reorder=reorder)
+    for order in ("community", "degree", "none"):
+        g = igp.build_graph(e, c.num_nodes, order=order)
         z1 = igp.embed(g, c.tau, c.d, c.steps, 0)
         z2 = igp.embed(g, c.tau, c.d, c.steps, 0)
         assert torch.equal(z1, z2)
@@ -457,6 +488,7 @@ def test_large_full_steps_with_and_without_reordering(igp, large):
         g.close()
         zs.append(z1.cpu().numpy())
         del z1, z2
-    err = row_rel_err(zs[1], zs[0].astype(np.float64))
-    record("large_L60_reorder_vs_not", err)
-    assert err <= TOL
+    for name, z in (("degree", zs[1]), ("none", zs[2])):
+        err = row_rel_err(z, zs[0].astype(np.float64))
+        record(f"large_L60_{name}_vs_community", err)
+        assert err <= TOL
