@@ -36,7 +36,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synth.dcsbm import CONFIGS, generate  # noqa: E402
+from synth.dcsbm import ALL_CONFIGS as CONFIGS, generate  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 

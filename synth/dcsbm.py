@@ -44,6 +44,21 @@ CONFIGS = {
     "large": DCSBMConfig("large", 5_000_000, 220, 1.5, 100_000_000, 128, -1.0, 60),
 }
 
+# The paper's own settings (Table II: tau, L, d per N) on DC-SBM graphs with
+# Table I's shape (K, M ~ 20 N): SURVEY.md §8(f) rank 3.  Parity cases and
+# throughput reports, not bench lines.
+PAPER_CONFIGS = {
+    "paper_5k": DCSBMConfig("paper_5k", 5_000, 19, 2.5, 100_000, 64, -6.0, 10),
+    "paper_10k": DCSBMConfig("paper_10k", 10_000, 25, 2.5, 200_000, 64, -3.0, 9),
+    "paper_50k": DCSBMConfig("paper_50k", 50_000, 44, 2.5, 1_000_000, 32, -80.0, 40),
+    "paper_100k": DCSBMConfig("paper_100k", 100_000, 56, 2.5, 2_000_000, 32, -80.0, 60),
+    "paper_500k": DCSBMConfig("paper_500k", 500_000, 98, 2.5, 10_000_000, 32, -80.0, 70),
+    "paper_1m": DCSBMConfig("paper_1m", 1_000_000, 125, 2.5, 20_000_000, 32, -80.0, 60),
+    "paper_stream_100k": DCSBMConfig("paper_stream_100k", 100_000, 56, 2.5, 2_000_000, 32, -100.0, 20),
+    "paper_stream_1m": DCSBMConfig("paper_stream_1m", 1_000_000, 125, 2.5, 20_000_000, 16, -100.0, 20),
+}
+ALL_CONFIGS = {**CONFIGS, **PAPER_CONFIGS}
+
 
 def block_sizes(rng: np.random.Generator, n: int, k: int, min_size: int = 10) -> np.ndarray:
     """Block sizes ~ Dirichlet(2·1_K)·N, each >= min_size, repaired to sum to N."""

@@ -14,7 +14,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2508_19737_b200 as igp  # noqa: E402
-from synth.dcsbm import CONFIGS, generate, stream_batches  # noqa: E402
+from synth.dcsbm import ALL_CONFIGS as CONFIGS, generate, stream_batches  # noqa: E402
 
 argv = sys.argv[1:]
 out_json = None
