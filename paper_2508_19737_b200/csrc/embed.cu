@@ -579,7 +579,7 @@ int choose_width(int d, int32_t n, int64_t nnz) {
 
 template <int W, int MB>
 igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s,
-                       const DeviceInfo& di) {
+                       const DeviceInfo& di, HostCopy* hc) {
     const int32_t n = g.n;
     const int L = o.steps, d = o.d, nslices = d / W;
     const int grid = layer_grid<W, MB>(n, di);
@@ -657,6 +657,14 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
             output_kernel<W><<<simple_grid((int64_t)n * (W / 4), 256, di), 256, 0, s>>>(ybuf[L & 1], node, sfin, g.order, n,
                                                                                         d, col0, o.mode, out);
             if ((rc = launch_status("output_kernel")) != IGP_OK) break;
+            if (hc) {  // this slice's columns are final: copy them out behind the remaining slices
+                if ((rc = cuda_status(cudaEventRecord(hc->ev[k], s), "event record")) != IGP_OK) break;
+                if ((rc = cuda_status(cudaStreamWaitEvent(hc->cs, hc->ev[k], 0), "stream wait")) != IGP_OK) break;
+                rc = cuda_status(cudaMemcpy2DAsync(hc->h_out + col0, sizeof(float) * d, out + col0, sizeof(float) * d,
+                                                   sizeof(float) * W, n, cudaMemcpyDeviceToHost, hc->cs),
+                                 "slice D2H");
+                if (rc != IGP_OK) break;
+            }
         }
     } while (0);
     free_async(ws, s);
@@ -665,7 +673,7 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
 
 }  // namespace
 
-igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s) {
+igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s, HostCopy* hc) {
     DeviceInfo di;
     if (!device_info(&di)) return IGP_ERR_CUDA;
     if (o.d != 16 && o.d != 32 && o.d != 64 && o.d != 128) {
@@ -676,9 +684,9 @@ igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cu
     const int occ = occ_env ? atoi(occ_env) : kDefaultOcc;
 #define IGP_W_CASE(WW)                                                      \
     case WW:                                                                \
-        if (occ == 3) return run_embed_w<WW, 3>(g, o, out, s, di); \
-        if (occ == 4) return run_embed_w<WW, 4>(g, o, out, s, di); \
-        return run_embed_w<WW, 2>(g, o, out, s, di);
+        if (occ == 3) return run_embed_w<WW, 3>(g, o, out, s, di, hc); \
+        if (occ == 4) return run_embed_w<WW, 4>(g, o, out, s, di, hc); \
+        return run_embed_w<WW, 2>(g, o, out, s, di, hc);
     switch (choose_width(o.d, g.n, g.cap)) {  // a heuristic: cap ~ nnz (the output does not depend on W)
         IGP_W_CASE(16)
         IGP_W_CASE(32)

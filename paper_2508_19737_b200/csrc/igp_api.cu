@@ -463,15 +463,31 @@ igp_status igp_embed_host(const int32_t* h_edges, int64_t num_edges, int32_t num
     igp_status st = igp_build_graph_ex(d_edges, num_edges, num_nodes, IGP_BUILD_ASYNC, stream, &g);
     free_async(d_edges, s);
     if (st != IGP_OK) return st;
-    st = cuda_status(alloc_async((void**)&d_out, ob, s), "out alloc");
-    if (st == IGP_OK) st = igp_embed_ex(g, opts, d_out, stream);
-    if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(h_out, d_out, ob, cudaMemcpyDeviceToHost, s), "out D2H");
+    // each column slice is copied to h_out on a second stream as soon as it is final, so all
+    // but the last slice's device->host transfer overlaps the remaining filter steps
+    HostCopy hc;
+    hc.h_out = h_out;
+    st = cuda_status(cudaStreamCreateWithFlags(&hc.cs, cudaStreamNonBlocking), "copy stream");
+    for (int k = 0; k < kMaxSlices && st == IGP_OK; ++k)
+        st = cuda_status(cudaEventCreateWithFlags(&hc.ev[k], cudaEventDisableTiming), "event");
+    if (st == IGP_OK) st = cuda_status(alloc_async((void**)&d_out, ob, s), "out alloc");
+    if (st == IGP_OK) st = cuda_status(cudaStreamWaitEvent(s, g->ready, 0), "stream wait");
+    if (st == IGP_OK) st = run_embed(g->csr, *opts, d_out, s, &hc);
+    cudaEvent_t copied = nullptr;
+    if (st == IGP_OK) st = cuda_status(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming), "event");
+    if (st == IGP_OK) st = cuda_status(cudaEventRecord(copied, hc.cs), "event record");
+    if (st == IGP_OK) st = cuda_status(cudaStreamWaitEvent(s, copied, 0), "stream wait");  // d_out freed after
     free_async(d_out, s);
     // the range check ran with the build (early on `s`); its flag is read after the work is queued
     if (st == IGP_OK) st = igp_graph_status(g);
     std::string msg = igp_last_error_message();
     igp_destroy_graph_async(g, stream);  // its only user is `s`
     igp_status st2 = cuda_status(cudaStreamSynchronize(s), "stream sync");
+    if (hc.cs) cudaStreamSynchronize(hc.cs);
+    if (copied) cudaEventDestroy(copied);
+    for (int k = 0; k < kMaxSlices; ++k)
+        if (hc.ev[k]) cudaEventDestroy(hc.ev[k]);
+    if (hc.cs) cudaStreamDestroy(hc.cs);
     if (st != IGP_OK) set_error(msg);
     return st != IGP_OK ? st : st2;
 }

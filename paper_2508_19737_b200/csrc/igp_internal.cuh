@@ -97,7 +97,15 @@ struct TimerSlot {
 };
 // an event pair (created on the current device) for `launches` filter steps; nullptr on failure
 TimerSlot* timer_acquire(int64_t launches);
-igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s);
+// optional device->host copy of each column slice as soon as it is final (igp_embed_host):
+// slice k's columns go to h_out on stream cs while slice k+1 computes
+struct HostCopy {
+    float* h_out = nullptr;  // host [N][d]
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[kMaxSlices] = {};
+};
+igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s,
+                     HostCopy* hc = nullptr);
 
 }  // namespace igp
 
