@@ -86,7 +86,7 @@ IGP_API igp_status igp_build_graph(const int32_t* d_edges, int64_t num_edges, in
 #define IGP_BUILD_NO_REORDER 1u /* keep the original node order for the filter steps (no relabelling;
                                    results differ only by fp32 summation order) */
 #define IGP_BUILD_REORDER_DEGREE 8u /* rows by descending degree (ties by ascending id) */
-#define IGP_BUILD_REORDER_COMMUNITY 4u /* rows grouped by label-propagation communities (10 synchronous
+#define IGP_BUILD_REORDER_COMMUNITY 4u /* rows grouped by label-propagation communities (8 synchronous
                                    sweeps, mode of <= 31 neighbour labels and the node's own, ties to the
                                    smallest label), descending degree within a community: neighbour gathers
                                    stay local in L2 on graphs whose feature slice exceeds it.

@@ -21,6 +21,7 @@
 // until the caller asks (igp_api.cu).
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "igp_internal.cuh"
 

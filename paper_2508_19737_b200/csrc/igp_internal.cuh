@@ -72,7 +72,8 @@ void free_csr(const CsrDevice& c, cudaStream_t s);
 constexpr int kColPad = 16;
 // row order of the relabelled CSR the filter steps traverse
 enum RowOrder { kOrderNone = 0, kOrderDegree = 1, kOrderCommunity = 2 };
-constexpr int kLabelPropIters = 10;  // label-propagation sweeps of the community order
+constexpr int kLabelPropIters = 8;  // label-propagation sweeps of the community order (measured best of
+                                    // 4-14 on headline and Large: profiles/r01b/lp_sweep.txt)
 // canonical CSR of the new edges, merged with `base` (an existing canonical CSR on the same
 // node set) when base != nullptr
 igp_status build_csr(const int32_t* d_edges, int64_t num_edges, int32_t n, RowOrder order, cudaStream_t s,

@@ -590,6 +590,82 @@ __global__ void __launch_bounds__(256, 4) flat_rw(const int* __restrict__ rp, co
   }
 }
 
+// The product structure with chunked dynamic row scheduling: a block grabs K consecutive row
+// batches (K x 64 rows) at a time from a global counter, so consecutive batches of a community
+// run on one SM (L1 reuse of shared neighbours) while the grid stays balanced.
+__device__ int g_chunk_counter;
+template <int K>
+__global__ void __launch_bounds__(256, 2) lab_chunk(const int* __restrict__ rp, const int* __restrict__ ci,
+                                                     const float* __restrict__ s, const float* __restrict__ yin,
+                                                     float* __restrict__ yout, int n) {
+  constexpr int LPR = 4, G = 8, IPL = 4, NV = 4, NG = 8 * G, BATCH = 8;
+  __shared__ int chunk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane % LPR, g = lane / LPR;
+  const uint64_t* Y = reinterpret_cast<const uint64_t*>(yin);
+  uint64_t* O = reinterpret_cast<uint64_t*>(yout);
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) chunk = atomicAdd(&g_chunk_counter, 1);
+    __syncthreads();
+    const long c0 = (long)chunk * K * NG;
+    if (c0 >= n) break;
+    for (int k = 0; k < K; ++k) {
+      const long base = c0 + (long)k * NG + warp * G;
+      if (base >= n) break;
+      const int row = (int)(base + g);
+      const bool valid = row < n;
+      int beg = 0, end = 0;
+      if (valid) { beg = __ldg(rp + row); end = __ldg(rp + row + 1); }
+      uint64_t acc[NV] = {0ull, 0ull, 0ull, 0ull};
+      const int start = beg & ~3;
+      const int nch = end > beg ? (end - start + 15) / 16 : 0;
+      const int max_nch = __reduce_max_sync(kFull, nch);
+      int jr[IPL];
+      load_idx<IPL>(ci, start, end, q, jr);
+      for (int c = 0; c < max_nch; ++c) {
+        const int e0 = start + c * 16, e1 = e0 + 16;
+        int jn[IPL];
+        load_idx<IPL>(ci, e1, end, q, jn);
+        const int lo = beg > e0 ? beg - e0 : 0;
+        int hi = end - e0;
+        hi = hi < 0 ? 0 : (hi > 16 ? 16 : hi);
+        const bool full = __all_sync(kFull, lo == 0 && hi == 16);
+#pragma unroll
+        for (int u0 = 0; u0 < 16; u0 += BATCH) {
+          uint64_t v[BATCH][NV];
+#pragma unroll
+          for (int t = 0; t < BATCH; ++t) {
+            const int u = u0 + t;
+            const int j = __shfl_sync(kFull, jr[u % IPL], u / IPL, LPR);
+            if (full || (u >= lo && u < hi)) ldg256(Y + ((size_t)j * LPR + q) * NV, v[t]);
+            else v[t][0] = v[t][1] = v[t][2] = v[t][3] = 0ull;
+          }
+#pragma unroll
+          for (int t = 0; t < BATCH; ++t)
+#pragma unroll
+            for (int kk = 0; kk < NV; ++kk) acc[kk] = fadd2(acc[kk], v[t][kk]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < IPL; ++kk) jr[kk] = jn[kk];
+      }
+      if (valid) {
+        const float si = s[row];
+        const uint64_t* own = Y + ((size_t)row * LPR + q) * NV;
+        uint64_t o[NV];
+#pragma unroll
+        for (int kk = 0; kk < NV; ++kk) {
+          const float2 y = unpack2(own[kk]);
+          const float2 a = unpack2(acc[kk]);
+          o[kk] = pack2(si * tanhf(0.1f * y.x + si * a.x), si * tanhf(0.1f * y.y + si * a.y));
+        }
+#pragma unroll
+        for (int kk = 0; kk < NV; ++kk) O[((size_t)row * LPR + q) * NV + kk] = o[kk];
+      }
+    }
+  }
+}
+
 template <typename K>
 float timeit(K kern, int grid, const int* rp, const int* ci, const float* s, float* y0, float* y1, int n, int reps,
              int* regs) {
@@ -657,6 +733,31 @@ int main(int argc, char** argv) {
            gbytes / ms * 1e3, cudaGetErrorString(cudaGetLastError()));                                             \
   }
   RUN("flat VB32 B4 occ4", (flat<32, 4, 4>), 4);
+#define RUNC(NAME, KK)                                                                                             \
+  {                                                                                                                \
+    cudaEvent_t a0, b0;                                                                                            \
+    cudaEventCreate(&a0);                                                                                          \
+    cudaEventCreate(&b0);                                                                                          \
+    int zero = 0;                                                                                                  \
+    float tot = 0;                                                                                                 \
+    for (int r = 0; r < reps + 1; ++r) {                                                                           \
+      cudaMemcpyToSymbol(g_chunk_counter, &zero, sizeof(int));                                                    \
+      cudaEventRecord(a0);                                                                                         \
+      lab_chunk<KK><<<sms * 2, 256>>>(rp, ci, s, (r & 1) ? y1 : y0, (r & 1) ? y0 : y1, n);                         \
+      cudaEventRecord(b0);                                                                                         \
+      cudaEventSynchronize(b0);                                                                                    \
+      float ms;                                                                                                    \
+      cudaEventElapsedTime(&ms, a0, b0);                                                                           \
+      if (r) tot += ms;                                                                                            \
+    }                                                                                                              \
+    printf("%-44s                          : %8.1f us  gather %7.0f GB/s  %s\n", NAME, tot / reps * 1e3,            \
+           gbytes / (tot / reps) * 1e3, cudaGetErrorString(cudaGetLastError()));                                   \
+  }
+  RUNC("chunk K=1 (dynamic)", 1);
+  RUNC("chunk K=2", 2);
+  RUNC("chunk K=4", 4);
+  RUNC("chunk K=8", 8);
+  RUNC("chunk K=16", 16);
   RUN("flat + own/store stream", (flat_rw<0>), 4);
   RUN("flat + own/store stream (store evict_first)", (flat_rw<1>), 4);
   RUN("base VB32 B8 (product structure)", (lab<32, 8, 0, 0, 2>), 0);
