@@ -191,6 +191,60 @@ __device__ __forceinline__ void warp_bitonic(int32_t* buf, int P, int lane) {
     }
 }
 
+// Sort + dedup seg[0..len) (len <= 32*E) in place with one warp; returns the unique count.
+// Element i = h*32 + lane lives in a[h]; bitonic stages with partner distance j < 32 use
+// shuffles, j >= 32 exchange registers within the lane.  All lanes must call it (converged).
+template <int E>
+__device__ __forceinline__ int warp_sort_dedup(int32_t* seg, int len, int lane) {
+    int32_t a[E];
+#pragma unroll
+    for (int h = 0; h < E; ++h) a[h] = h * 32 + lane < len ? seg[h * 32 + lane] : INT_MAX;
+    int P = 32;
+    while (P < len) P <<= 1;
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+        if (k > P) break;
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int hj = j >> 5;
+#pragma unroll
+                for (int h = 0; h < E; ++h) {
+                    if (h & hj) continue;  // (h, h | hj) pairs, handled from the lower index
+                    const int i = h * 32 + lane;
+                    const bool up = (i & k) == 0;
+                    const int32_t x = a[h], y = a[h | hj];
+                    a[h] = up ? min(x, y) : max(x, y);
+                    a[h | hj] = up ? max(x, y) : min(x, y);
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < E; ++h) {
+                    const int i = h * 32 + lane;
+                    const int32_t b = __shfl_xor_sync(0xffffffffu, a[h], j);
+                    const bool up = (i & k) == 0, lower = (i & j) == 0;
+                    a[h] = (lower == up) ? min(a[h], b) : max(a[h], b);
+                }
+            }
+        }
+    }
+    // dedup: keep the first of each run of equal values, compact in order
+    int base = 0;
+    int32_t carry = 0;  // last element of the previous register row
+#pragma unroll
+    for (int h = 0; h < E; ++h) {
+        const int i = h * 32 + lane;
+        int32_t prev = __shfl_up_sync(0xffffffffu, a[h], 1);
+        if (lane == 0) prev = carry;
+        carry = __shfl_sync(0xffffffffu, a[h], 31);
+        const bool keep = i < len && (i == 0 || a[h] != prev);
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) seg[base + __popc(m & lanemask_lt())] = a[h];
+        base += __popc(m);
+    }
+    return base;
+}
+
 __global__ void __launch_bounds__(256) sort_rows_warp_kernel(const int32_t* __restrict__ off, int32_t* __restrict__ tmp,
                                                              int32_t* __restrict__ ucnt, int32_t n,
                                                              int32_t* __restrict__ big_list, int32_t* __restrict__ big_count,
@@ -212,6 +266,12 @@ __global__ void __launch_bounds__(256) sort_rows_warp_kernel(const int32_t* __re
         }
         if (len <= 1) {
             if (lane == 0) ucnt[r] = len;
+            continue;
+        }
+        if (len <= 64) {  // registers: two elements per lane, bitonic network over shuffles (measured:
+                          // faster than shared memory here, slower for 4-8 elements per lane)
+            const int u = warp_sort_dedup<2>(tmp + o, len, lane);  // converged: all lanes shuffle
+            if (lane == 0) ucnt[r] = u;
             continue;
         }
         const int P = next_pow2(len);
@@ -518,19 +578,39 @@ __global__ void __launch_bounds__(256) label_prop_kernel(const int32_t* __restri
     }
 }
 
-// bucket nodes by label; the bucket entries are the nodes' ranks in the degree order
+// bucket nodes by label; the bucket entries are the nodes' ranks in the degree order.  After
+// label propagation a few hundred labels cover all nodes, so the atomics are warp-aggregated
+// (one per distinct label per warp).
 __global__ void label_count_kernel(const int32_t* __restrict__ lab, int32_t n, int32_t* __restrict__ cnt) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(cnt + lab[i], 1);
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool act = i < n;
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        if (!act) continue;
+        const int32_t l = lab[i];
+        const unsigned peers = __match_any_sync(am, l);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + l, __popc(peers));
+    }
 }
 
 __global__ void label_scatter_kernel(const int32_t* __restrict__ lab, const int32_t* __restrict__ rank, int32_t n,
                                      const int32_t* __restrict__ off, int32_t* __restrict__ fill,
                                      int32_t* __restrict__ out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool act = i < n;
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        if (!act) continue;
         const int32_t l = lab[i];
-        out[off[l] + atomicAdd(fill + l, 1)] = rank[i];
+        const unsigned peers = __match_any_sync(am, l);
+        const int leader = __ffs(peers) - 1;
+        int32_t b = 0;
+        if (lane == leader) b = atomicAdd(fill + l, __popc(peers));
+        b = __shfl_sync(peers, b, leader);
+        out[off[l] + b + __popc(peers & lanemask_lt())] = rank[i];
     }
 }
 

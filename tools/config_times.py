@@ -22,7 +22,8 @@ if "--json" in argv:
     k = argv.index("--json")
     out_json = argv[k + 1]
     del argv[k:k + 2]
-names = argv[0].split(",") if argv else ["tiny", "medium", "headline", "streaming", "large", "large_noreorder"]
+names = argv[0].split(",") if argv else ["tiny", "medium", "headline", "headline_degree", "streaming", "large",
+                                         "large_degree", "large_noreorder"]
 results = {}
 
 
@@ -32,7 +33,7 @@ def ev():
 
 def static(name):
     base, _, suffix = name.partition("_")
-    order = {"": "degree", "noreorder": "none", "community": "community"}[suffix]
+    order = {"": "auto", "degree": "degree", "noreorder": "none", "community": "community"}[suffix]
     reorder = order != "none"
     cfg = CONFIGS[base]
     edges, _ = generate(cfg)
