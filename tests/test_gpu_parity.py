@@ -546,3 +546,26 @@ def test_paper_settings_chaotic_tau_layerwise(igp, cfg):
     assert torch.allclose(pre.std(0, unbiased=False), torch.ones(c.d, dtype=torch.float64, device=pre.device),
                           atol=1e-4)
     g.close()
+
+
+# ------------------------------------------------------------------ downstream sanity report (not a gate)
+@pytest.mark.parametrize("cfg", ["medium", "paper_5k"])
+def test_birch_sanity_report(igp, cfg):
+    """north_star: 'as a sanity report only, both embeddings fed to the same CPU BIRCH must give
+    an equal NMI against the planted blocks' (Alg. 1 l.7; sklearn Birch, K-agnostic,
+    threshold 1.0 -- the paper does not state its threshold).  BIRCH's threshold
+    decisions can flip on 1e-5 perturbations, so 'equal' is checked to 0.02 and both recorded."""
+    from sklearn.cluster import Birch
+    from sklearn.metrics import adjusted_rand_score, normalized_mutual_info_score
+    from synth.dcsbm import ALL_CONFIGS
+    c = ALL_CONFIGS[cfg]
+    edges, labels = generate(c)
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, c.steps, c.tau)
+    scores = {}
+    for name, emb in (("gpu", z.astype(np.float64)), ("oracle", ref)):
+        pred = Birch(n_clusters=None, threshold=1.0).fit_predict(emb)
+        scores[name] = (normalized_mutual_info_score(labels, pred), adjusted_rand_score(labels, pred))
+        record(f"{cfg}_birch_{name}_nmi", scores[name][0])
+        record(f"{cfg}_birch_{name}_ari", scores[name][1])
+    assert scores["oracle"][0] > 0.5  # the embedding carries the planted blocks at all
+    assert abs(scores["gpu"][0] - scores["oracle"][0]) <= 0.02
