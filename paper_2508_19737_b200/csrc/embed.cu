@@ -28,6 +28,7 @@
 // are independent of summation order: blocks combine them with plain atomics,
 // the row schedule is free, and the output is still bitwise deterministic.  The
 // rounding perturbs mu and sigma by < 2^-g (~1e-9), far below fp32 resolution.
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 
@@ -518,8 +519,9 @@ constexpr size_t layer_smem() {
 
 template <int W, int MB>
 int layer_grid(int32_t n, const DeviceInfo& di) {
-    static int occ_cache[64] = {0};
-    int& occ = occ_cache[di.device & 63];
+    // per device: the smem attribute is set (idempotently) before the occupancy is published
+    static std::atomic<int> occ_cache[64];
+    int occ = occ_cache[di.device & 63].load(std::memory_order_acquire);
     if (occ == 0) {
         cudaFuncSetAttribute(layer_kernel<W, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)layer_smem<W>());
         int o = 0;
@@ -528,6 +530,7 @@ int layer_grid(int32_t n, const DeviceInfo& di) {
             o < 1)
             o = 1;
         occ = o;
+        occ_cache[di.device & 63].store(o, std::memory_order_release);
     }
     const int64_t rows_per_block = (int64_t)kWarps * (32 / (W / 8));
     const int64_t want = (n + rows_per_block - 1) / rows_per_block;

@@ -569,3 +569,41 @@ def test_birch_sanity_report(igp, cfg):
         record(f"{cfg}_birch_{name}_ari", scores[name][1])
     assert scores["oracle"][0] > 0.5  # the embedding carries the planted blocks at all
     assert abs(scores["gpu"][0] - scores["oracle"][0]) <= 0.02
+
+
+def test_concurrent_host_threads(igp):
+    """Two host threads, each with its own stream, build and embed different graphs at the same
+    time (thread-safe handles, pools, caches and error strings): results equal the sequential run."""
+    import threading
+    cfgs = [CONFIGS["tiny"], CONFIGS["medium"]]
+    inputs = [torch.from_numpy(generate(c)[0]).cuda() for c in cfgs]
+    seq = []
+    for c, e in zip(cfgs, inputs):
+        g = igp.build_graph(e, c.num_nodes)
+        seq.append(igp.embed(g, c.tau, c.d, c.steps, 3).cpu())
+        g.close()
+    out = [None, None]
+    errs = []
+
+    def work(k):
+        try:
+            c, e = cfgs[k], inputs[k]
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    g = igp.build_graph(e, c.num_nodes, stream=s, async_build=True)
+                    z = igp.embed(g, c.tau, c.d, c.steps, 3, stream=s)
+                    g.close(stream=s)
+                s.synchronize()
+                out[k] = z.cpu()
+        except Exception as ex:  # surfaced below
+            errs.append(ex)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for k in range(2):
+        assert torch.equal(out[k], seq[k])
