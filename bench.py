@@ -70,6 +70,11 @@ def step_bytes(n, nnz, d):
     return 4 * (n + 1) + 4 * nnz + 4 * n + 8 * n * d
 
 
+def embed_bytes(n, nnz, d, L):
+    """B_embed = L B_step + (4(N+1) + 4 nnz + 12 N) [a4] + (4Nd + 4N) [a5] + (8Nd + 4N) [a8]."""
+    return L * step_bytes(n, nnz, d) + (4 * (n + 1) + 4 * nnz + 12 * n) + (4 * n * d + 4 * n) + (8 * n * d + 4 * n)
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
 
@@ -298,7 +303,11 @@ def run_gpu(args, cfg):
             "per": "filter step (all d columns)", "algorithmic_bytes": b_step,
             "step_us": step_s * 1e6, "avg_launch_us": avg_launch_s * 1e6, "peak_source": peak_src,
             "gather_bytes_per_step": 4 * nnz * d, "gather_GBps": 4 * nnz * d / step_s / 1e9,
-            "share_of_step": tot_layer_ms / ms_total}
+            "share_of_step": tot_layer_ms / ms_total,
+            # whole-embed compulsory bytes over the embed time (SURVEY.md §8(d) "B_embed/(t HBM)")
+            "embed_algorithmic_bytes": embed_bytes(N, nnz, d, L),
+            "embed_frac": embed_bytes(N, nnz, d, L) / (embed_ms / 1e3) / 1e9 / peak,
+            "embed_frac_8TBs": embed_bytes(N, nnz, d, L) / (embed_ms / 1e3) / 8e12}
 
     line = {"metric": "FFP embed throughput (GEdge·feat/s)", "value": value, "unit": "GEdge·feat/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
