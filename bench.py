@@ -131,6 +131,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def load_gather_ceiling(config_name):
+    """Measured random-gather ceiling (GB/s) of this workload's index stream, if profiled."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            v = json.load(f).get(config_name) or {}
+        return v.get("gather_ceiling_GBps")
+    except Exception:
+        return None
+
+
 def load_traffic(config_name):
     """DRAM bytes (read + write) of one filter step, from the committed ncu --set full
     capture of one slice launch (profiles/ncu_traffic.json) times the launches per step."""
@@ -303,6 +313,7 @@ def run_gpu(args, cfg):
             "per": "filter step (all d columns)", "algorithmic_bytes": b_step,
             "step_us": step_s * 1e6, "avg_launch_us": avg_launch_s * 1e6, "peak_source": peak_src,
             "gather_bytes_per_step": 4 * nnz * d, "gather_GBps": 4 * nnz * d / step_s / 1e9,
+            "gather_ceiling_GBps": load_gather_ceiling(cfg.name),
             "share_of_step": tot_layer_ms / ms_total,
             # whole-embed compulsory bytes over the embed time (SURVEY.md §8(d) "B_embed/(t HBM)")
             "embed_algorithmic_bytes": embed_bytes(N, nnz, d, L),
