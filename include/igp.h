@@ -142,6 +142,9 @@ IGP_API igp_status igp_destroy_graph_async(igp_graph_t g, igp_stream_t stream);
 #define IGP_MODE_PRE_SIGMOID 1 /* Z^(L) (column z-scored), debug/test      */
 #define IGP_MODE_LINEAR 2      /* Z^(l) = phi * Z^(l-1): no tanh/ZNorm/sigmoid, debug/test */
 
+#define IGP_FLAG_ROW_L2 2u      /* post-op, NOT part of the paper's method (Eq. (4) ends with the sigmoid):
+                                   each output row scaled to unit L2 norm (fp64 norm), zero rows unchanged;
+                                   for consumers that want the north star's "rows normalised" reading (A12) */
 #define IGP_FLAG_TIME_LAYERS 1u /* record CUDA events on `stream` around each slice's L filter-step
                                    launches into the process-wide layer timer (igp_layer_timer_*) */
 

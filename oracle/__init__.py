@@ -68,6 +68,8 @@ def _load():
     lib.oracle_propagate.restype = None
     lib.oracle_zscore_columns.argtypes = [P, i32, i32]
     lib.oracle_zscore_columns.restype = None
+    lib.oracle_row_l2.argtypes = [P, i32, i32]
+    lib.oracle_row_l2.restype = None
     lib.oracle_embed.argtypes = [P, P, i32, i32, i32, f64, f64, f64, f64, P, u64, u64, i32, i32, P]
     lib.oracle_embed.restype = ctypes.c_int
     _lib = lib
@@ -162,6 +164,16 @@ def zscore_columns(T) -> np.ndarray:
         T = T[:, None]
     lib.oracle_zscore_columns(_ptr(T), T.shape[0], T.shape[1])
     return T
+
+
+def row_l2(Z) -> np.ndarray:
+    """Optional post-op (not in the paper, reading A12): rows scaled to unit L2 norm."""
+    lib = _load()
+    Z = np.array(Z, dtype=np.float64, order="C", copy=True)
+    if Z.ndim == 1:
+        Z = Z[None, :]
+    lib.oracle_row_l2(_ptr(Z), Z.shape[0], Z.shape[1])
+    return Z
 
 
 def embed(row_ptr, col_idx, num_nodes: int, d: int, steps: int, tau: float, seed: int = 0,

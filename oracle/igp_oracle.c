@@ -249,6 +249,22 @@ void oracle_zscore_columns(double* T, int32_t N, int32_t d) {
     }
 }
 
+/* Optional row L2 normalisation of an output (NOT part of the paper's method: Eq. (4),
+ * PAPER.md:164-166, ends with the sigmoid; the north star's wording "the rows are normalised
+ * into the embedding" / "(4) a fused row L2-normalise / output kernel" is served by an
+ * off-by-default library flag, reading A12).  Definition: z_i <- z_i / ||z_i||_2,
+ * rows with ||z_i||_2 = 0 unchanged.  In place on Z (N x d, row-major). */
+void oracle_row_l2(double* Z, int32_t N, int32_t d) {
+    for (int32_t i = 0; i < N; ++i) {
+        double* z = &Z[(int64_t)i * d];
+        double ss = 0.0;
+        for (int32_t c = 0; c < d; ++c) ss += z[c] * z[c];
+        double nrm = sqrt(ss);
+        if (nrm > 0.0)
+            for (int32_t c = 0; c < d; ++c) z[c] /= nrm;
+    }
+}
+
 /* modes for oracle_embed */
 #define ORACLE_MODE_FULL 0        /* Z~ = sigmoid(Z^(L))                        */
 #define ORACLE_MODE_PRE_SIGMOID 1 /* Z^(L)                                      */

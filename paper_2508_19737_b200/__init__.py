@@ -26,6 +26,7 @@ LIB_PATH = os.path.join(_PKG, "libigp.so")
 
 MODES = {"full": 0, "pre_sigmoid": 1, "linear": 2}
 FLAG_TIME_LAYERS = 1
+FLAG_ROW_L2 = 2
 
 IGP_OK = 0
 _STATUS = {0: "IGP_OK", 2: "IGP_ERR_INPUT", 4: "IGP_ERR_NUMERICAL", 5: "IGP_ERR_CUDA", 6: "IGP_ERR_OOM",
@@ -225,12 +226,13 @@ def layer_timer_read():
 
 
 def make_opts(tau: float, d: int, steps: int, seed: int = 0, *, subsequence: int = 0, theta: float = 0.1,
-              alpha: float = 1.0, eps: float = 1e-3, mode: str = "full", time_layers: bool = False) -> EmbedOpts:
+              alpha: float = 1.0, eps: float = 1e-3, mode: str = "full", time_layers: bool = False,
+              row_l2: bool = False) -> EmbedOpts:
     o = EmbedOpts()
     _lib.igp_embed_opts_default(ctypes.byref(o))
     o.tau, o.d, o.steps, o.seed, o.subsequence = float(tau), int(d), int(steps), int(seed), int(subsequence)
     o.theta, o.alpha, o.eps, o.mode = float(theta), float(alpha), float(eps), MODES[mode]
-    o.flags = FLAG_TIME_LAYERS if time_layers else 0
+    o.flags = (FLAG_TIME_LAYERS if time_layers else 0) | (FLAG_ROW_L2 if row_l2 else 0)
     return o
 
 

@@ -506,6 +506,24 @@ __global__ void output_kernel(const float4* __restrict__ y, const float4* __rest
     }
 }
 
+// optional post-op (IGP_FLAG_ROW_L2, reading A12): z_i <- z_i / ||z_i||_2, one warp per row,
+// fp64 sum of squares; rows with zero norm are left unchanged
+__global__ void row_l2_kernel(float* __restrict__ out, int32_t n, int d) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        float* z = out + i * d;
+        double ss = 0.0;
+        for (int c = lane; c < d; c += 32) ss += (double)z[c] * (double)z[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
+        if (ss > 0.0) {
+            const double inv = 1.0 / sqrt(ss);
+            for (int c = lane; c < d; c += 32) z[c] = (float)((double)z[c] * inv);
+        }
+    }
+}
+
 int simple_grid(int64_t items, int threads, const DeviceInfo& di, int per_sm = 8) {
     int64_t g = (items + threads - 1) / threads;
     int64_t cap = (int64_t)di.num_sms * per_sm;
@@ -660,13 +678,25 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
             output_kernel<W><<<simple_grid((int64_t)n * (W / 4), 256, di), 256, 0, s>>>(ybuf[L & 1], node, sfin, g.order, n,
                                                                                         d, col0, o.mode, out);
             if ((rc = launch_status("output_kernel")) != IGP_OK) break;
-            if (hc) {  // this slice's columns are final: copy them out behind the remaining slices
+            if (hc && !(o.flags & IGP_FLAG_ROW_L2)) {  // this slice's columns are final: copy them
+                                                          // out behind the remaining slices
                 if ((rc = cuda_status(cudaEventRecord(hc->ev[k], s), "event record")) != IGP_OK) break;
                 if ((rc = cuda_status(cudaStreamWaitEvent(hc->cs, hc->ev[k], 0), "stream wait")) != IGP_OK) break;
                 rc = cuda_status(cudaMemcpy2DAsync(hc->h_out + col0, sizeof(float) * d, out + col0, sizeof(float) * d,
                                                    sizeof(float) * W, n, cudaMemcpyDeviceToHost, hc->cs),
                                  "slice D2H");
                 if (rc != IGP_OK) break;
+            }
+        }
+        if (rc == IGP_OK && (o.flags & IGP_FLAG_ROW_L2)) {  // needs every slice: after the last one
+            row_l2_kernel<<<simple_grid((int64_t)n * 32, 256, di), 256, 0, s>>>(out, n, d);
+            if ((rc = launch_status("row_l2_kernel")) != IGP_OK) break;
+            if (hc) {
+                if ((rc = cuda_status(cudaEventRecord(hc->ev[0], s), "event record")) != IGP_OK) break;
+                if ((rc = cuda_status(cudaStreamWaitEvent(hc->cs, hc->ev[0], 0), "stream wait")) != IGP_OK) break;
+                rc = cuda_status(cudaMemcpyAsync(hc->h_out, out, sizeof(float) * (size_t)n * d, cudaMemcpyDeviceToHost,
+                                                 hc->cs),
+                                 "D2H");
             }
         }
     } while (0);

@@ -170,6 +170,10 @@ static igp_status check_opts(const igp_embed_opts* o) {
         set_error("steps must be >= 0");
         return IGP_ERR_INPUT;
     }
+    if (o->flags & ~(uint32_t)(IGP_FLAG_TIME_LAYERS | IGP_FLAG_ROW_L2)) {
+        set_error("unknown embed flags");
+        return IGP_ERR_INPUT;
+    }
     if (o->mode != IGP_MODE_FULL && o->mode != IGP_MODE_PRE_SIGMOID && o->mode != IGP_MODE_LINEAR) {
         set_error("unknown mode");
         return IGP_ERR_INPUT;

@@ -607,3 +607,33 @@ def test_concurrent_host_threads(igp):
     assert not errs, errs
     for k in range(2):
         assert torch.equal(out[k], seq[k])
+
+
+# ------------------------------------------------------------------ optional row-L2 post-op (IGP_FLAG_ROW_L2, reading A12)
+@pytest.mark.parametrize("cfg,d", [("tiny", 16), ("tiny", 128), ("medium", 64)])
+def test_row_l2_flag(igp, cfg, d):
+    """Off by default (the paper ends with the sigmoid); with the flag each output row is the
+    oracle's sigmoid row scaled to unit L2 norm.  Also through the host-buffer path."""
+    c = CONFIGS[cfg]
+    edges, _ = generate(c)
+    g = gpu_graph(igp, edges, c.num_nodes)
+    z = igp.embed(g, c.tau, d, c.steps, 0, row_l2=True).cpu().numpy()
+    rp, ci, _ = oracle.build_csr(edges, c.num_nodes)
+    ref = oracle.row_l2(oracle.embed(rp, ci, c.num_nodes, d, c.steps, c.tau, seed=0, nthreads=NTHREADS))
+    err = row_rel_err(z, ref)
+    record(f"{cfg}_d{d}_row_l2", err)
+    assert err <= TOL
+    assert np.allclose(np.linalg.norm(z.astype(np.float64), axis=1), 1.0, atol=1e-6)
+    if cfg == "tiny":
+        host = igp.embed_host(torch.from_numpy(edges).pin_memory(), c.num_nodes, c.tau, d, c.steps, 0,
+                              row_l2=True).numpy()
+        assert np.array_equal(host, z)
+
+
+def test_embed_unknown_flags_rejected(igp):
+    import ctypes
+    g = gpu_graph(igp, np.array([[0, 1]], np.int32), 2)
+    o = igp.make_opts(-1.0, 16, 2)
+    o.flags = 0x100
+    out = torch.empty((2, 16), device="cuda")
+    assert igp.lib().igp_embed_ex(g.handle, ctypes.byref(o), ctypes.c_void_p(out.data_ptr()), None) == 2

@@ -117,3 +117,22 @@ def test_negative_tau_changes_the_embedding():
     a = oracle.embed(rp, ci, n, 16, 5, -1.0, seed=0)
     b = oracle.embed(rp, ci, n, 16, 5, 0.0, seed=0)
     assert np.abs(a - b).max() > 1e-3
+
+
+# ------------------------------------------------------------------ optional row-L2 post-op (reading A12)
+def test_row_l2_closed_forms():
+    """Pythagorean rows have exact unit-norm images; zero rows are unchanged."""
+    Z = np.array([[3.0, 4.0], [0.0, 0.0], [5.0, 12.0], [-8.0, 15.0]])
+    out = oracle.row_l2(Z)
+    assert np.array_equal(out, np.array([[0.6, 0.8], [0.0, 0.0], [5 / 13, 12 / 13], [-8 / 17, 15 / 17]]))
+
+
+def test_row_l2_unit_norm_and_direction():
+    rng = np.random.default_rng(5)
+    Z = rng.random((300, 64)) + 1e-3  # sigmoid outputs are positive
+    out = oracle.row_l2(Z)
+    assert np.allclose(np.linalg.norm(out, axis=1), 1.0, atol=1e-14)
+    # each row is a positive multiple of its input: out_i * ||Z_i|| == Z_i
+    assert np.allclose(out * np.linalg.norm(Z, axis=1, keepdims=True), Z, rtol=1e-14, atol=0)
+    # idempotent
+    assert np.allclose(oracle.row_l2(out), out, atol=1e-15)
