@@ -637,3 +637,15 @@ def test_embed_unknown_flags_rejected(igp):
     o.flags = 0x100
     out = torch.empty((2, 16), device="cuda")
     assert igp.lib().igp_embed_ex(g.handle, ctypes.byref(o), ctypes.c_void_p(out.data_ptr()), None) == 2
+
+
+@pytest.mark.parametrize("L", [0, 1])
+def test_embed_zero_and_one_step(igp, L):
+    """L = 0: the output is sigmoid(Theta) (Alg. 1 with an empty layer loop); L = 1: one layer."""
+    c = CONFIGS["tiny"]
+    edges, _ = generate(c)
+    for mode in ("full", "pre_sigmoid", "linear"):
+        z, ref = run_parity(igp, edges, c.num_nodes, 32, L, c.tau, seed=11, mode=mode)
+        err = row_rel_err(z, ref)
+        record(f"tiny_L{L}_{mode}", err)
+        assert err <= TOL, mode
