@@ -255,14 +255,11 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
     __shared__ __align__(16) float stage[kWarps][G * TS];
     extern __shared__ double dyn_smem[];
     double (*acc_f)[W] = reinterpret_cast<double (*)[W]>(dyn_smem);  // [NG][W] long-row partials
-    for (int c = threadIdx.x; c < W; c += kThreads) {
-        double m = 0.0, is = 1.0;
-        if (p.sums_in) column_stats(p.sums_in, c, W, p.n, m, is);
-        st[c + c / 8] = make_double2(m, is);  // one pad slot per 8 columns: the 8-column groups of the
-                                              // lanes of a row start in distinct banks
-    }
+    // Programmatic dependent launch: the next filter step may be scheduled onto SMs as this
+    // grid's blocks retire; everything up to griddepcontrol.wait (shared-memory setup, the first
+    // row batch's row pointers and indices -- static CSR data) overlaps this grid's tail.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int t = threadIdx.x; t < NG * W; t += kThreads) (&acc_f[0][0])[t] = 0.0;
-    __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q = lane % LPR, g = lane / LPR;
@@ -291,6 +288,15 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
         nend = __ldg(p.rp + base + g + 1);
     }
     load_idx<IPL>(p.ci, nbeg & ~3, nend, q, pol_idx, jfirst);
+    // the previous step's output (yin) and column sums (sums_in) are read only after this point
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int c = threadIdx.x; c < W; c += kThreads) {
+        double m = 0.0, is = 1.0;
+        if (p.sums_in) column_stats(p.sums_in, c, W, p.n, m, is);
+        st[c + c / 8] = make_double2(m, is);  // one pad slot per 8 columns: the 8-column groups of the
+                                              // lanes of a row start in distinct banks
+    }
+    __syncthreads();
     // warp-uniform batches of G consecutive rows of the relabelled (degree-sorted) CSR
     for (; base < p.n; base += step) {
         const int32_t row = (int32_t)(base + g);
@@ -669,7 +675,19 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 a.grid_c = grid_c;
                 a.idx_ef = idx_ef;
                 a.st_ef = st_ef;
-                layer_kernel<W, MB><<<grid, kThreads, layer_smem<W>(), s>>>(a);
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(grid);
+                cfg.blockDim = dim3(kThreads);
+                cfg.dynamicSmemBytes = layer_smem<W>();
+                cfg.stream = s;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                if ((rc = cuda_status(cudaLaunchKernelEx(&cfg, layer_kernel<W, MB>, a), "layer_kernel launch")) !=
+                    IGP_OK)
+                    break;
                 if ((rc = launch_status("layer_kernel")) != IGP_OK) break;
             }
             if (rc != IGP_OK) break;
