@@ -29,6 +29,10 @@
  *     igp_last_error_message() gives a thread-local detail string.
  *   - The library never falls back to the CPU: with no usable CUDA device every
  *     call returns IGP_ERR_CUDA.
+ *   - Development knobs (read from the environment at each embed; measurement tooling
+ *     only, results are bitwise independent of all of them): IGP_SLICE_WIDTH (16/32/64/128
+ *     columns per slice), IGP_LAYER_OCC (2/3/4 blocks per SM), IGP_IDX_EF / IGP_ST_EF
+ *     (fraction of index loads / output stores marked L2 evict_first).
  */
 #ifndef IGP_H_
 #define IGP_H_
