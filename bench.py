@@ -250,11 +250,12 @@ def run_gpu(args, cfg):
     for _ in range(args.warmup):
         step(True)  # same calls as the timed steps (the timer's events are created here)
     torch.cuda.synchronize(dev)
-    igp.layer_timer_reset()
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
+    step(True)  # the GPU idled while the sampler started: one more untimed step brings it back up
+    igp.layer_timer_reset()
     launches0 = igp.kernel_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
