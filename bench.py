@@ -165,6 +165,17 @@ def oracle_sample(cfg, edges, layers, nthreads):
     return time.perf_counter() - t0, int(ci.size)
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -205,7 +216,7 @@ def run_reference(args, cfg):
                        "L": cfg.steps, "L_sampled": layers},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "GEdge·feat/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": "GEdge·feat/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -360,7 +371,7 @@ def run_gpu(args, cfg):
         cores = cpu_cores()
         secs, onnz = oracle_sample(cfg, edges_np, args.cpu_layers, cores)
         line["cpu_baseline"] = {"value": onnz * d * args.cpu_layers / secs / 1e9, "unit": "GEdge·feat/s",
-                                "cores": cores, "kind": "oracle",
+                                "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                                 "sample": f"{cfg.name} graph, {args.cpu_layers} of L={L} filter steps "
                                           f"(+ Philox input, sigmoid), fp64, {secs:.1f} s"}
     if rank == 0:

@@ -64,3 +64,30 @@ def test_host_side_calls_without_device(igp):
     assert lib.igp_embed_ex(None, ctypes.byref(o), None, None) == 2
     assert lib.igp_destroy_graph(None) == 0
     assert lib.igp_kernel_launch_count() == 0
+
+
+def test_more_host_validated_errors(igp):
+    """Argument errors that return before any device work (no GPU needed)."""
+    lib = igp.lib()
+    h = ctypes.c_void_p()
+    assert lib.igp_build_graph_ex(None, 0, 5, 0x80, None, ctypes.byref(h)) == 2          # unknown flag
+    assert lib.igp_build_graph_ex(None, 0, 5, 1 | 4, None, ctypes.byref(h)) == 2         # conflicting orders
+    assert lib.igp_build_graph_ex(None, 0, 5, 4 | 8, None, ctypes.byref(h)) == 2
+    assert lib.igp_build_graph_ex(None, 0, 5, 0, None, None) == 2                        # no out handle
+    assert lib.igp_build_graph_ex(None, 3, 5, 0, None, ctypes.byref(h)) == 2             # edges NULL, E > 0
+    assert lib.igp_graph_add_edges(None, None, 0, None) == 2
+    assert lib.igp_graph_status(None) == 2
+    assert lib.igp_graph_info(None, None, None, None) == 2
+    assert lib.igp_graph_copy_csr(None, None, None, None) == 2
+    assert lib.igp_destroy_graph_async(None, None) == 0
+    assert lib.igp_philox_bits(0, 0, -1, None, None) == 2
+    assert lib.igp_philox_normal(0, 0, 6, None, None) == 2                               # not a multiple of 4
+    o = igp.make_opts(-1.0, 64, 3)
+    o.flags = 0x40
+    assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o), None, None) == 2              # NULL h_out first
+    out = (ctypes.c_float * 256)()
+    assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o), out, None) == 2               # unknown embed flag
+    o.flags = 0
+    o.eps = 0.0
+    assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o), out, None) == 2               # eps must be > 0
+    assert lib.igp_kernel_launch_count() == 0
