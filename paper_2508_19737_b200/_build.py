@@ -56,5 +56,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+EXAMPLE_SRC = os.path.join(ROOT, "examples", "embed_c.c")
+EXAMPLE_BIN = os.path.join(ROOT, "examples", "embed_c")
+
+
+def build_example(force: bool = False) -> str:
+    """The plain-C consumer of the ABI (examples/embed_c.c), linked against libigp.so."""
+    lib = build()
+    if force or _stale(EXAMPLE_BIN, [EXAMPLE_SRC, lib, os.path.join(ROOT, "include", "igp.h")]):
+        cuda_home = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+        tmp = EXAMPLE_BIN + f".tmp{os.getpid()}"
+        cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-I" + os.path.join(ROOT, "include"),
+               "-I" + os.path.join(cuda_home, "include"), "-o", tmp, EXAMPLE_SRC, "-L" + PKG, "-ligp",
+               "-Wl,-rpath," + PKG, "-L" + os.path.join(cuda_home, "lib64"), "-lcudart", "-lm"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("example build failed: " + " ".join(cmd))
+        os.replace(tmp, EXAMPLE_BIN)
+    return EXAMPLE_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

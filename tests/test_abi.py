@@ -91,3 +91,13 @@ def test_more_host_validated_errors(igp):
     o.eps = 0.0
     assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o), out, None) == 2               # eps must be > 0
     assert lib.igp_kernel_launch_count() == 0
+
+
+def test_c_example_builds_against_the_header(igp):
+    """examples/embed_c.c uses only include/igp.h and links libigp.so (no Python, no torch)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("igp_build", os.path.join(ROOT, "paper_2508_19737_b200", "_build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    exe = b.build_example()
+    assert os.access(exe, os.X_OK)

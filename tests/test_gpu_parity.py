@@ -649,3 +649,14 @@ def test_embed_zero_and_one_step(igp, L):
         err = row_rel_err(z, ref)
         record(f"tiny_L{L}_{mode}", err)
         assert err <= TOL, mode
+
+
+def test_plain_c_consumer(igp):
+    """The C ABI used from C alone (examples/embed_c.c): host and device paths agree bitwise,
+    outputs in (0, 1), pre-sigmoid columns standardised."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "embed_c")
+    for args in (["3000", "30000", "64", "10"], ["777", "5000", "16", "3"], ["20000", "400000", "128", "5"]):
+        res = subprocess.run([exe, *args], capture_output=True, text=True, timeout=300)
+        assert res.returncode == 0, res.stderr
+        assert res.stdout.startswith("ok "), res.stdout
