@@ -47,6 +47,7 @@ __device__ __forceinline__ int2 ld_idx2(const int* p) {
   return v;
 }
 __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 template <int IPL>
 __device__ __forceinline__ void load_idx(const int* ci, int e0, int end, int q, int (&jr)[IPL]) {
@@ -100,10 +101,14 @@ __global__ void __launch_bounds__(256, MINB) lab(const int* __restrict__ rp, con
       const int e0 = start + c * 16, e1 = e0 + 16;
       int jn[IPL];
       load_idx<IPL>(ci, e1, end, q, jn);
-      if (PF) {
+      if (PF == 1) {
 #pragma unroll
         for (int k = 0; k < IPL; ++k)
           if (e1 + q * IPL + k < end) pf_l2(Y + (size_t)jn[k] * (W / 2));
+      } else if (PF == 2) {
+#pragma unroll
+        for (int k = 0; k < IPL; ++k)
+          if (e1 + q * IPL + k < end) pf_l1(Y + (size_t)jn[k] * (W / 2));
       }
       const int lo = beg > e0 ? beg - e0 : 0;
       int hi = end - e0;
@@ -733,6 +738,9 @@ int main(int argc, char** argv) {
            gbytes / ms * 1e3, cudaGetErrorString(cudaGetLastError()));                                             \
   }
   RUN("flat VB32 B4 occ4", (flat<32, 4, 4>), 4);
+  RUN("base VB32 B8 + L1 prefetch of next chunk", (lab<32, 8, 2, 0, 2>), 0);
+  RUN("base VB32 B4 + L1 prefetch of next chunk", (lab<32, 4, 2, 0, 2>), 0);
+  RUN("base VB32 B4 occ4 + L1 prefetch", (lab<32, 4, 2, 0, 4>), 0);
 #define RUNC(NAME, KK)                                                                                             \
   {                                                                                                                \
     cudaEvent_t a0, b0;                                                                                            \
