@@ -144,18 +144,6 @@ __device__ __forceinline__ void column_stats(const double* sums, int c, int W, i
 
 __device__ __forceinline__ double grid_round(double x, double c) { return __dsub_rn(__dadd_rn(x, c), c); }
 
-__device__ __forceinline__ int4 ld_idx4(const int32_t* p) {
-    int4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
-}
-__device__ __forceinline__ int2 ld_idx2(const int32_t* p) {
-    int2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
-    return v;
-}
 __device__ __forceinline__ int ld_idx1(const int32_t* p, uint64_t pol) {
     int v;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
@@ -264,7 +252,6 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q = lane % LPR, g = lane / LPR;
     const int grp = warp * G + g;
-    const unsigned gmask = ((LPR == 32) ? kFull : ((1u << LPR) - 1u)) << (g * LPR);
     const uint64_t* yin = reinterpret_cast<const uint64_t*>(p.yin);  // row j, lane q: yin + (j*LPR + q)*4
     uint64_t* yout = reinterpret_cast<uint64_t*>(p.yout);
     float* tile = stage[warp];
