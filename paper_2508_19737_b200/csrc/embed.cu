@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) 
                                               // lanes of a row start in distinct banks
     }
     __syncthreads();
-    // warp-uniform batches of G consecutive rows of the relabelled (degree-sorted) CSR
+    // warp-uniform batches of G consecutive rows of the relabelled CSR (degree-sorted, within
+    // communities for the community order: neighbouring rows have similar trip counts)
     for (; base < p.n; base += step) {
         const int32_t row = (int32_t)(base + g);
         const bool valid = row < p.n;
@@ -623,7 +624,7 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     igp_status rc = IGP_OK;
     const bool timed = (o.flags & IGP_FLAG_TIME_LAYERS) != 0;
     do {
-        // all filter-step work runs on the relabelled CSR (rows by descending degree)
+        // all filter-step work runs on the relabelled CSR (rows in the handle's degree / community order)
         scale_kernel<<<simple_grid(n, 256, di), 256, 0, s>>>(g.rp_perm, n, (double)o.tau, (double)o.eps, node);
         if ((rc = launch_status("scale_kernel")) != IGP_OK) break;
         affine_kernel<<<simple_grid((int64_t)n * 32, 256, di), 256, 0, s>>>(g.rp_perm, g.col_perm, n, o.theta,

@@ -59,9 +59,9 @@ inline igp_status launch_status(const char* what) {
 struct CsrDevice {
     int32_t* row_ptr = nullptr;  // [N+1]
     int32_t* col_idx = nullptr;  // [cap + kColPad] (vector index loads may overrun a row's end)
-    int32_t* order = nullptr;    // [N] order[r] = original id of relabelled row r (descending degree)
-    int32_t* rp_perm = nullptr;  // [N+1] CSR of the relabelled graph (row r = node order[r]) ...
-    int32_t* col_perm = nullptr; // [nnz + kColPad]  ... with relabelled, ascending column ids
+    int32_t* order = nullptr;    // [N] order[r] = original id of relabelled row r (degree or community order)
+    int32_t* rp_perm = nullptr;  // [N+5] CSR of the relabelled graph (row r = node order[r]) ...
+    int32_t* col_perm = nullptr; // [cap + kColPad]  ... neighbour ids relabelled, in canonical order
     int32_t* meta = nullptr;     // device [4]: [0] range-error flag (nnz is row_ptr[N])
     bool perm_alias = false;     // no relabelling: rp_perm/col_perm alias row_ptr/col_idx, order = identity
     int32_t n = 0;
