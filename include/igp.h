@@ -71,7 +71,7 @@ typedef enum {
  *              and self loops are allowed: self loops are dropped, each unordered pair
  *              {u, v}, u != v, becomes A_uv = A_vu = 1 once.
  *   num_edges  >= 0 (0 is valid: M = 0, all degrees 0); 2*num_edges must be
- *              <= INT32_MAX (else IGP_ERR_UNSUPPORTED).
+ *              <= INT32_MAX - 64 (int32 CSR offsets; else IGP_ERR_UNSUPPORTED).
  *   num_nodes  N >= 1 (else IGP_ERR_INPUT).
  *   out        receives a new handle owning device row_ptr int32[N+1] and
  *              col_idx int32[2M] (rows ascending, columns strictly ascending); the

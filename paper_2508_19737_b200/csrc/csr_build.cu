@@ -646,7 +646,7 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     if (!device_info(&di)) return IGP_ERR_CUDA;
     // both orientations of the new edges (before dedup / self-loop removal), plus the base rows
     const int64_t raw = 2 * E + (base ? base->cap : 0);
-    if (raw > (int64_t)INT32_MAX) {
+    if (raw > kMaxEntries) {
         set_error("edge count exceeds the int32 CSR index range");
         return IGP_ERR_UNSUPPORTED;
     }

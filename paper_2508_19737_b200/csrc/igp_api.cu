@@ -234,7 +234,7 @@ igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t
         set_error("num_edges must be >= 0 and d_edges non-NULL when num_edges > 0");
         return IGP_ERR_INPUT;
     }
-    if (num_edges > (int64_t)INT32_MAX / 2) {
+    if (num_edges > kMaxEntries / 2) {
         set_error("2*num_edges exceeds the int32 CSR index range");
         return IGP_ERR_UNSUPPORTED;
     }
@@ -291,7 +291,7 @@ igp_status igp_graph_add_edges(igp_graph_t g, const int32_t* d_edges, int64_t nu
         set_error("num_edges must be >= 0 and d_edges non-NULL when num_edges > 0");
         return IGP_ERR_INPUT;
     }
-    if (num_edges > ((int64_t)INT32_MAX - g->csr.cap) / 2) {
+    if (num_edges > (kMaxEntries - g->csr.cap) / 2) {
         set_error("merged edge count exceeds the int32 CSR index range");
         return IGP_ERR_UNSUPPORTED;
     }

@@ -70,6 +70,9 @@ struct CsrDevice {
 // release every array of c in stream order on s
 void free_csr(const CsrDevice& c, cudaStream_t s);
 constexpr int kColPad = 16;
+// largest CSR entry count (before dedup): int32 offsets with headroom for the kernels' chunk
+// arithmetic (a chunk start + 2 chunks of 16 must not overflow)
+constexpr int64_t kMaxEntries = (int64_t)INT32_MAX - 64;
 // row order of the relabelled CSR the filter steps traverse
 enum RowOrder { kOrderNone = 0, kOrderDegree = 1, kOrderCommunity = 2 };
 constexpr int kLabelPropIters = 8;  // label-propagation sweeps of the community order (measured best of
