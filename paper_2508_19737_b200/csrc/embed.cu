@@ -38,8 +38,6 @@
 namespace igp {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 16;      // neighbours per index chunk
 constexpr int kFoldChunks = 4;  // fp32 partial sums span at most 64 neighbours
 constexpr int kBatch = 8;       // gathers issued back to back per lane (full chunks)
@@ -230,8 +228,10 @@ __device__ __forceinline__ void load_idx(const int32_t* ci, int32_t e0, int32_t 
 //  - Column statistics: each warp stages its G x W tile of t in shared memory and every
 //    lane folds 8 of those values (OC whole columns) into fp64 registers, so the per-lane
 //    state is 2*OC doubles instead of 16.
-template <int W, int MB>
-__global__ void __launch_bounds__(kThreads, MB) layer_kernel(const LayerArgs p) {
+template <int W, int MB, int NW>
+__global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
+    constexpr int kWarps = NW;  // warps per block (8; 2 for graphs too small to fill the SMs)
+    constexpr int kThreads = NW * 32;
     constexpr int LPR = W / 8;
     constexpr int G = 32 / LPR;
     constexpr int IPL = kChunk / LPR;
@@ -524,27 +524,28 @@ int simple_grid(int64_t items, int threads, const DeviceInfo& di, int per_sm = 8
     return (int)(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
-template <int W>
+template <int W, int NW>
 constexpr size_t layer_smem() {
-    return sizeof(double) * (size_t)(kWarps * (256 / W)) * W;  // acc_f: NG x W doubles (>= kWarps x 2W)
+    return sizeof(double) * (size_t)(NW * (256 / W)) * W;  // acc_f: NG x W doubles (>= NW x 2W)
 }
 
-template <int W, int MB>
+template <int W, int MB, int NW>
 int layer_grid(int32_t n, const DeviceInfo& di) {
     // per device: the smem attribute is set (idempotently) before the occupancy is published
     static std::atomic<int> occ_cache[64];
     int occ = occ_cache[di.device & 63].load(std::memory_order_acquire);
     if (occ == 0) {
-        cudaFuncSetAttribute(layer_kernel<W, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)layer_smem<W>());
+        cudaFuncSetAttribute(layer_kernel<W, MB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)layer_smem<W, NW>());
         int o = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, layer_kernel<W, MB>, kThreads, layer_smem<W>()) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, layer_kernel<W, MB, NW>, NW * 32, layer_smem<W, NW>()) !=
                 cudaSuccess ||
             o < 1)
             o = 1;
         occ = o;
         occ_cache[di.device & 63].store(o, std::memory_order_release);
     }
-    const int64_t rows_per_block = (int64_t)kWarps * (32 / (W / 8));
+    const int64_t rows_per_block = (int64_t)NW * (32 / (W / 8));
     const int64_t want = (n + rows_per_block - 1) / rows_per_block;
     const int64_t cap = (int64_t)di.num_sms * occ;
     const int64_t g = want < cap ? want : cap;
@@ -597,7 +598,9 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                        const DeviceInfo& di, HostCopy* hc) {
     const int32_t n = g.n;
     const int L = o.steps, d = o.d, nslices = d / W;
-    const int grid = layer_grid<W, MB>(n, di);
+    // graphs too small to give every SM a block of 8 warps run 2-warp blocks (4x the blocks)
+    const bool small = (n + 8 * (256 / W) - 1) / (8 * (256 / W)) < di.num_sms;
+    const int grid = small ? layer_grid<W, MB, 2>(n, di) : layer_grid<W, MB, 8>(n, di);
     const size_t nw = (size_t)n * W;
     // workspace: node | y0 | y1 (N x W each) | sums [slices][L+1][2W]
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -665,17 +668,17 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 a.st_ef = st_ef;
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(grid);
-                cfg.blockDim = dim3(kThreads);
-                cfg.dynamicSmemBytes = layer_smem<W>();
+                cfg.blockDim = dim3(small ? 64 : 256);
+                cfg.dynamicSmemBytes = small ? layer_smem<W, 2>() : layer_smem<W, 8>();
                 cfg.stream = s;
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
                 attr[0].val.programmaticStreamSerializationAllowed = 1;
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
-                if ((rc = cuda_status(cudaLaunchKernelEx(&cfg, layer_kernel<W, MB>, a), "layer_kernel launch")) !=
-                    IGP_OK)
-                    break;
+                const cudaError_t le = small ? cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 2>, a)
+                                             : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 8>, a);
+                if ((rc = cuda_status(le, "layer_kernel launch")) != IGP_OK) break;
                 if ((rc = launch_status("layer_kernel")) != IGP_OK) break;
             }
             if (rc != IGP_OK) break;
