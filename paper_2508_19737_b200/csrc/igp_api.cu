@@ -118,6 +118,7 @@ static cudaStream_t status_stream(int dev) {
 
 // wait for g's last build / merge and read nnz = row_ptr[N] and the range-error flag
 igp_status resolve_graph(igp_graph_s* g) {
+    std::lock_guard<std::mutex> lock(g->mu);
     if (g->resolved) return IGP_OK;
     int prev = -1;
     cudaGetDevice(&prev);
@@ -372,8 +373,12 @@ static void release_graph(igp_graph_t g, cudaStream_t s) {
 
 igp_status igp_destroy_graph(igp_graph_t g) {
     if (!g) return IGP_OK;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != g->device) cudaSetDevice(g->device);
     cudaDeviceSynchronize();  // no stream may still read the CSR
     release_graph(g, (cudaStream_t)0);
+    if (prev >= 0) cudaSetDevice(prev);
     return IGP_OK;
 }
 

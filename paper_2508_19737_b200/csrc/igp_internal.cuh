@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 #include <string>
 
 #include "../../include/igp.h"
@@ -119,6 +120,7 @@ struct igp_graph_s {
     bool async = false;        // IGP_BUILD_ASYNC: nnz / range errors resolved lazily
     int device = 0;
     cudaEvent_t ready = nullptr;  // recorded after the last build / merge
+    std::mutex mu;             // guards the lazy resolution below (queries may race across threads)
     bool resolved = false;     // nnz / err below are valid
     int64_t nnz = -1;
     int32_t err = 0;
