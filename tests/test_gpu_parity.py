@@ -660,3 +660,23 @@ def test_plain_c_consumer(igp):
         res = subprocess.run([exe, *args], capture_output=True, text=True, timeout=300)
         assert res.returncode == 0, res.stderr
         assert res.stdout.startswith("ok "), res.stdout
+
+
+def test_bitwise_reproducible_across_processes(igp):
+    """Same graph, arguments and seed give bitwise-identical embeddings in a fresh process
+    (no dependence on allocation addresses, scheduling or atomics order)."""
+    import hashlib
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, hashlib, torch; sys.path.insert(0, %r); import paper_2508_19737_b200 as igp; "
+            "from synth.dcsbm import CONFIGS, generate; c = CONFIGS['medium']; "
+            "e = torch.from_numpy(generate(c)[0]).cuda(); g = igp.build_graph(e, c.num_nodes); "
+            "z = igp.embed(g, c.tau, c.d, 12, 5).cpu().numpy(); print(hashlib.sha256(z.tobytes()).hexdigest())" % root)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    c = CONFIGS["medium"]
+    e = torch.from_numpy(generate(c)[0]).cuda()
+    g = igp.build_graph(e, c.num_nodes)
+    z = igp.embed(g, c.tau, c.d, 12, 5).cpu().numpy()
+    assert hashlib.sha256(z.tobytes()).hexdigest() == out.stdout.strip()
