@@ -163,10 +163,14 @@ typedef struct {
     float eps;            /* Eq. (1) epsilon > 0, default 0.001 */
     int32_t mode;         /* IGP_MODE_* */
     uint32_t flags;       /* IGP_FLAG_* */
+    const float* d_z0;    /* NULL (default): Z^(0) = Theta from Philox (Alg. 1 l.2).  Otherwise a
+                             caller-owned device fp32 [N][d] row-major Z^(0) (row i = node id i) used
+                             instead of Theta: an inspection / verification hook (e.g. layer-by-layer
+                             checks from a given state, Alg. 1 l.3 "Z^(0) <- Theta" replaced) */
 } igp_embed_opts;
 
 /* Fill opts with the paper's defaults: theta 0.1, alpha 1, eps 1e-3, subsequence 0,
- * mode FULL, flags 0 (tau/d/steps/seed left at 0 for the caller to set). */
+ * mode FULL, flags 0, d_z0 NULL (tau/d/steps/seed left at 0 for the caller to set). */
 IGP_API void igp_embed_opts_default(igp_embed_opts* opts);
 
 /* Z~ for graph g written to d_out, device fp32 [N][d] row-major, caller-owned,

@@ -43,7 +43,7 @@ class EmbedOpts(ctypes.Structure):
     _fields_ = [("tau", ctypes.c_float), ("d", ctypes.c_int32), ("steps", ctypes.c_int32),
                 ("seed", ctypes.c_uint64), ("subsequence", ctypes.c_uint64), ("theta", ctypes.c_float),
                 ("alpha", ctypes.c_float), ("eps", ctypes.c_float), ("mode", ctypes.c_int32),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("d_z0", ctypes.c_void_p)]
 
 
 # name -> (restype, argtypes); mirrors include/igp.h
@@ -227,12 +227,15 @@ def layer_timer_read():
 
 def make_opts(tau: float, d: int, steps: int, seed: int = 0, *, subsequence: int = 0, theta: float = 0.1,
               alpha: float = 1.0, eps: float = 1e-3, mode: str = "full", time_layers: bool = False,
-              row_l2: bool = False) -> EmbedOpts:
+              row_l2: bool = False, z0: torch.Tensor | None = None) -> EmbedOpts:
     o = EmbedOpts()
     _lib.igp_embed_opts_default(ctypes.byref(o))
     o.tau, o.d, o.steps, o.seed, o.subsequence = float(tau), int(d), int(steps), int(seed), int(subsequence)
     o.theta, o.alpha, o.eps, o.mode = float(theta), float(alpha), float(eps), MODES[mode]
     o.flags = (FLAG_TIME_LAYERS if time_layers else 0) | (FLAG_ROW_L2 if row_l2 else 0)
+    if z0 is not None:  # caller-provided Z^(0) (CUDA float32 [N, d]) instead of Theta
+        _require_cuda(z0, torch.float32, "z0")
+        o.d_z0 = z0.data_ptr()
     return o
 
 
@@ -240,6 +243,9 @@ def embed(graph: Graph, tau: float, d: int, steps: int, seed: int = 0, *, out: t
           stream=None, **kw) -> torch.Tensor:
     """igp_embed_ex: Alg. 1 l.1-6; returns Z~ as CUDA float32 [N, d] (asynchronous on ``stream``)."""
     o = make_opts(tau, d, steps, seed, **kw)
+    z0 = kw.get("z0")
+    if z0 is not None and tuple(z0.shape) != (graph.num_nodes, int(d)):
+        raise ValueError("z0 must have shape [N, d]")
     if out is None:
         out = torch.empty((graph.num_nodes, int(d)), dtype=torch.float32, device=graph.device)
     _require_cuda(out, torch.float32, "out")

@@ -91,10 +91,11 @@ __global__ void affine_kernel(const int32_t* __restrict__ rp, const int32_t* __r
 
 // slice k of y0 = s_i * Theta_i, Theta = X / sqrt(d); element (i, c) of original node i is
 // draw k = i*d + c; relabelled row r holds original node order[r]
+// (or, with a caller-provided z0 [N][d], y0 = s_i * z0_i: the igp_embed_opts.d_z0 hook)
 template <int W>
 __global__ void input_kernel(uint64_t seed, uint64_t sub, int32_t n, int d, int col0,
                              const int32_t* __restrict__ order, const float4* __restrict__ node,
-                             float4* __restrict__ y0) {
+                             const float* __restrict__ z0, float4* __restrict__ y0) {
     constexpr int LPR = W / 4;
     const int64_t total = (int64_t)n * LPR;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -102,6 +103,12 @@ __global__ void input_kernel(uint64_t seed, uint64_t sub, int32_t n, int d, int 
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
         const int64_t i = idx / LPR;
         const int q = (int)(idx % LPR);
+        if (z0) {
+            const float4 z = *reinterpret_cast<const float4*>(z0 + (int64_t)order[i] * d + col0 + 4 * q);
+            const double s = (double)node[i].x;
+            y0[idx] = make_float4((float)(s * z.x), (float)(s * z.y), (float)(s * z.z), (float)(s * z.w));
+            continue;
+        }
         const uint64_t b = (uint64_t)(((int64_t)order[i] * d + col0) / 4 + q);  // draws of the ORIGINAL id
         const U4 r = philox_block(seed, sub, b);
         double x0, x1, x2, x3;
@@ -639,7 +646,8 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
             const int col0 = k * W;
             double* sk = sums + (size_t)k * (L + 1) * 2 * W;
             input_kernel<W><<<simple_grid((int64_t)n * (W / 4), 256, di), 256, 0, s>>>(o.seed, o.subsequence, n, d,
-                                                                                      col0, g.order, node, ybuf[0]);
+                                                                                      col0, g.order, node, o.d_z0,
+                                                                                      ybuf[0]);
             if ((rc = launch_status("input_kernel")) != IGP_OK) break;
             TimerSlot* ts = nullptr;
             if (timed && L > 0) {

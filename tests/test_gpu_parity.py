@@ -516,9 +516,11 @@ def test_paper_settings_chaotic_tau_layerwise(igp, cfg):
     """Table II's tau = -80 / -100 clamp every node of degree <= |tau| to D = eps (Eq. (1)), so
     s^2 = 1/eps = 1000 and each layer amplifies fp32 rounding ~10^3 times: the fp32 and fp64
     trajectories separate after 2-3 layers (reading A16).  Checked instead: layer 1 from the
-    exact Philox input at the 1e-4 bar; each checked layer l recomputed by the oracle from the
-    GPU's own Z^(l-1) (isolating that layer's arithmetic) at 1e-3; full-L properties."""
+    exact Philox input at the 1e-4 bar; one layer from seeded layer states Z (synth/states.py,
+    generic and tanh-saturated shapes; the same fp32 values go to the CUDA path via d_z0 and to
+    the oracle via Z0) at 1e-3; full-L properties."""
     from synth.dcsbm import PAPER_CONFIGS
+    from synth.states import layer_state
     c = PAPER_CONFIGS[cfg]
     edges, _ = generate(c)
     e = torch.from_numpy(edges).cuda()
@@ -529,14 +531,15 @@ def test_paper_settings_chaotic_tau_layerwise(igp, cfg):
     err1 = row_rel_err(z1, ref1)
     record(f"{cfg}_L1", err1)
     assert err1 <= TOL
-    layers = [2, c.steps] if c.num_nodes >= 1_000_000 else [2, c.steps // 2, c.steps]
-    for l in layers:
-        zp = igp.embed(g, c.tau, c.d, l - 1, 0, mode="pre_sigmoid").cpu().numpy().astype(np.float64)
-        zl = igp.embed(g, c.tau, c.d, l, 0).cpu().numpy()
-        ref = oracle.embed(rp, ci, c.num_nodes, c.d, 1, c.tau, Z0=zp, nthreads=NTHREADS)
-        err = row_rel_err(zl, ref)
-        record(f"{cfg}_layer{l}_from_gpu_state", err)
-        assert err <= LAYER_TOL_CHAOTIC
+    for k, kind in enumerate(("normal", "bimodal")):
+        zs = layer_state(c.num_nodes, c.d, seed=100 + k, kind=kind)
+        for mode, om in (("full", oracle.MODE_FULL), ("pre_sigmoid", oracle.MODE_PRE_SIGMOID)):
+            zl = igp.embed(g, c.tau, c.d, 1, 0, mode=mode, z0=torch.from_numpy(zs).cuda()).cpu().numpy()
+            ref = oracle.embed(rp, ci, c.num_nodes, c.d, 1, c.tau, Z0=zs.astype(np.float64), mode=om,
+                               nthreads=NTHREADS)
+            err = row_rel_err(zl, ref)
+            record(f"{cfg}_one_layer_from_{kind}_state_{mode}", err)
+            assert err <= LAYER_TOL_CHAOTIC, (kind, mode)
     za = igp.embed(g, c.tau, c.d, c.steps, 0)
     zb = igp.embed(g, c.tau, c.d, c.steps, 0)
     assert torch.equal(za, zb)
@@ -680,3 +683,23 @@ def test_bitwise_reproducible_across_processes(igp):
     g = igp.build_graph(e, c.num_nodes)
     z = igp.embed(g, c.tau, c.d, 12, 5).cpu().numpy()
     assert hashlib.sha256(z.tobytes()).hexdigest() == out.stdout.strip()
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "medium"])
+def test_initial_state_hook(igp, cfg):
+    """igp_embed_opts.d_z0: a caller-provided Z^(0) (seeded, synth/states.py) replaces Theta;
+    row i of z0 is node id i whatever the internal row order.  Several layers at the 1e-4 bar."""
+    from synth.states import layer_state
+    c = CONFIGS[cfg]
+    edges, _ = generate(c)
+    zs = layer_state(c.num_nodes, c.d, seed=7)
+    rp, ci, _ = oracle.build_csr(edges, c.num_nodes)
+    e = torch.from_numpy(edges).cuda()
+    for order in ("degree", "community", "none"):
+        g = igp.build_graph(e, c.num_nodes, order=order)
+        z = igp.embed(g, c.tau, c.d, 5, 0, z0=torch.from_numpy(zs).cuda()).cpu().numpy()
+        ref = oracle.embed(rp, ci, c.num_nodes, c.d, 5, c.tau, Z0=zs.astype(np.float64), nthreads=NTHREADS)
+        err = row_rel_err(z, ref)
+        record(f"{cfg}_z0_{order}", err)
+        assert err <= TOL, order
+        g.close()

@@ -11,9 +11,9 @@ import oracle  # noqa: E402
 import paper_2508_19737_b200 as igp  # noqa: E402
 from synth.dcsbm import PAPER_CONFIGS, generate  # noqa: E402
 
-names = sys.argv[1].split(",") if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else ["paper_5k", "paper_10k", "paper_50k", "paper_100k"]
+names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["paper_5k", "paper_10k", "paper_50k", "paper_100k"]
 nt = len(os.sched_getaffinity(0))
-for name in ([] if "--layerwise" in sys.argv else names):
+for name in names:
     c = PAPER_CONFIGS[name]
     edges, _ = generate(c)
     e = torch.from_numpy(edges).cuda()
@@ -26,21 +26,3 @@ for name in ([] if "--layerwise" in sys.argv else names):
         err = float(np.max(np.abs(z - ref) / np.linalg.norm(ref, axis=1, keepdims=True)))
         print(f"{name} tau={c.tau} d={c.d} L={L:3d}: row-rel err {err:.3e}", flush=True)
     g.close()
-
-# layerwise: layer l of the GPU path from the GPU's own Z^(l-1) (pre-sigmoid output at l-1),
-# recomputed by the oracle in fp64 -- isolates one layer's arithmetic from the accumulated drift
-if "--layerwise" in sys.argv:
-    for name in names:
-        c = PAPER_CONFIGS[name]
-        edges, _ = generate(c)
-        e = torch.from_numpy(edges).cuda()
-        g = igp.build_graph(e, c.num_nodes)
-        rp, ci, _ = oracle.build_csr(edges, c.num_nodes)
-        for l in sorted({2, 3, c.steps // 2, c.steps}):
-            zp = igp.embed(g, c.tau, c.d, l - 1, 0, mode="pre_sigmoid").cpu().numpy().astype(np.float64)
-            for mode, om in (("pre_sigmoid", oracle.MODE_PRE_SIGMOID), ("full", oracle.MODE_FULL)):
-                zl = igp.embed(g, c.tau, c.d, l, 0, mode=mode).cpu().numpy().astype(np.float64)
-                ref = oracle.embed(rp, ci, c.num_nodes, c.d, 1, c.tau, Z0=zp, mode=om, nthreads=nt)
-                err = float(np.max(np.abs(zl - ref) / np.linalg.norm(ref, axis=1, keepdims=True)))
-                print(f"layerwise {name} tau={c.tau} layer {l:3d} {mode:11s}: row-rel err {err:.3e}", flush=True)
-        g.close()
