@@ -32,7 +32,10 @@ def ev():
 
 
 def static(name):
-    base, _, suffix = name.partition("_")
+    base, suffix = name, ""
+    for sfx in ("_degree", "_noreorder", "_community"):
+        if name.endswith(sfx):
+            base, suffix = name[: -len(sfx)], sfx[1:]
     order = {"": "auto", "degree": "degree", "noreorder": "none", "community": "community"}[suffix]
     reorder = order != "none"
     cfg = CONFIGS[base]
