@@ -12,10 +12,15 @@
 //   B2 scan       exclusive scan of row counts -> bucket offsets (3-phase scan)
 //   B3 scatter    both orientations into their row bucket        (order within a row arbitrary)
 //   B4 row sort   per-row sort + in-row dedup -> unique counts:
-//                   len <= 1024:          one warp per row, bitonic sort in shared memory
+//                   len <= 64:            one warp per row, bitonic network in registers (shuffles)
+//                   64 < len <= 1024:     one warp per row, bitonic sort in shared memory
 //                   1024 < len <= 16384:  one block per row, bitonic sort in shared memory
 //                   len > 16384:          one block per row, N-bit bitmap in global scratch
 //   B5 scan+compact  row_ptr = scan(unique counts); col_idx = compacted rows
+//   B6 row order  degree-descending (counting sort by degree, ascending id within a degree)
+//   B7 (optional) label-propagation communities, rows bucketed by label, degree order within
+//   B6b relabel   the CSR the filter steps traverse: rows in that order, each row's
+//                 neighbours relabelled and kept in canonical order
 // No host synchronisation: the column arrays are sized by the 2E directed entries
 // before deduplication; nnz = row_ptr[N] and the range-error flag stay on the device
 // until the caller asks (igp_api.cu).

@@ -9,6 +9,12 @@
 //                          gather y_j = s_j t_j (float4), Eq. (3) with the deferred column
 //                          z-score, tanh (Eq. (4)), store y' = s t', exact column sums
 //   E4  output_kernel<W>   Z~ = sigmoid((t - mu)/sigma)  (Eq. (4))
+//   E5  row_l2_kernel      optional post-op (IGP_FLAG_ROW_L2, not in the paper; reading A12)
+//
+// Launch structure.  E3 runs as a persistent grid (min(row batches, SMs x 2) blocks of 8
+// warps; 2-warp blocks when the graph cannot fill the SMs otherwise) and every filter step
+// is launched with programmatic dependent launch, so step l+1's setup and first CSR loads
+// overlap step l's tail.  The whole embed is enqueued without a host synchronisation.
 //
 // Column slicing.  Every step of the FFP acts on each column independently:
 // phi* mixes rows only, tanh/sigmoid are element-wise and ZNorm is per column
