@@ -27,6 +27,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "igp_internal.cuh"
 
@@ -449,6 +450,16 @@ __global__ void __launch_bounds__(256) degree_scatter_kernel(const int32_t* __re
         if (key[k] >= 0) order[base[key[k]] + rank[k]] = i0 + k * 256 + threadIdx.x;
 }
 
+// a non-blocking side stream per device for build work that overlaps the main stream
+cudaStream_t side_stream(int dev) {
+    static std::mutex mu;
+    static cudaStream_t st[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    cudaStream_t& x = st[dev & 63];
+    if (!x && cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) x = nullptr;
+    return x;
+}
+
 int grid_for(int64_t work, int threads, int num_sms, int per_sm) {
     int64_t g = (work + threads - 1) / threads;
     int64_t cap = (int64_t)num_sms * per_sm;
@@ -705,7 +716,11 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 5), s), "alloc");
     if (st == IGP_OK && reorder) st = cuda_status(alloc_async((void**)&c.col_perm, cbytes, s), "col_perm alloc");
     if (!reorder) c.perm_alias = true;
+    cudaEvent_t ev_csr = nullptr, ev_lp = nullptr;  // community order: side-stream fork / join
     auto fail = [&](igp_status e) {
+        if (ev_lp) cudaStreamWaitEvent(s, ev_lp, 0);  // never free under the side stream's work
+        if (ev_csr) cudaEventDestroy(ev_csr);
+        if (ev_lp) cudaEventDestroy(ev_lp);
         free_async(ws, s);
         free_csr(c, s);
         return e;
@@ -767,6 +782,39 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         *out = c;
         return IGP_OK;
     }
+    // B7 label propagation (community order) depends only on the canonical CSR: it runs on a
+    // side stream while B6a computes the degree order on `s` (LP is bound by the warp-match
+    // pipe, the degree sort by loads and ALU, so the two overlap)
+    const size_t nb = al(sizeof(int32_t) * (size_t)n);
+    int32_t* lab0 = (int32_t*)(ws + o_comm);
+    int32_t* lab1 = (int32_t*)(ws + o_comm + nb);
+    if (community) {
+        cudaStream_t ss = side_stream(di.device);
+        IGP_STEP(cuda_status(ss ? cudaSuccess : cudaErrorInvalidResourceHandle, "side stream"));
+        IGP_STEP(cuda_status(cudaEventCreateWithFlags(&ev_csr, cudaEventDisableTiming), "event"));
+        cudaEvent_t lp = nullptr;
+        IGP_STEP(cuda_status(cudaEventCreateWithFlags(&lp, cudaEventDisableTiming), "event"));
+        IGP_STEP(cuda_status(cudaEventRecord(ev_csr, s), "event record"));
+        IGP_STEP(cuda_status(cudaStreamWaitEvent(ss, ev_csr, 0), "stream wait"));
+        const int ng = grid_for(n, 256, di.num_sms, 8);
+        iota_kernel<<<ng, 256, 0, ss>>>(lab0, n);
+        igp_status lst = launch_status("iota_kernel");
+        for (int it = 0; it < kLabelPropIters && lst == IGP_OK; ++it) {
+            label_prop_kernel<<<grid_for((int64_t)n * 32, 256, di.num_sms, 8), 256, 0, ss>>>(c.row_ptr, c.col_idx, n,
+                                                                                             lab0, lab1);
+            lst = launch_status("label_prop_kernel");
+            int32_t* t = lab0;
+            lab0 = lab1;
+            lab1 = t;
+        }
+        if (lst == IGP_OK) lst = cuda_status(cudaEventRecord(lp, ss), "event record");
+        if (lst != IGP_OK) {  // drain what was enqueued on the side stream before freeing anything
+            cudaStreamSynchronize(ss);
+            cudaEventDestroy(lp);
+            return fail(lst);
+        }
+        ev_lp = lp;
+    }
     // B6a: degree-descending order (counting sort by degree, then ascending id per bucket)
     IGP_STEP(cuda_status(cudaMemsetAsync(hist, 0, sizeof(int32_t) * kDegBuckets, s), "memset"));
     degree_hist_kernel<<<grid_for(n, 256, di.num_sms, 4), 256, 0, s>>>(c.row_ptr, n, hist);
@@ -778,25 +826,17 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     IGP_STEP(launch_status("degree_scatter_kernel"));
     IGP_STEP(segmented_sort(boff, c.order, hist, kDegBuckets, n, n, sc, s, di));
     if (community) {
-        // B7: label-propagation communities, rows grouped by label (descending degree within)
-        const size_t nb = al(sizeof(int32_t) * (size_t)n);
-        int32_t* lab0 = (int32_t*)(ws + o_comm);
-        int32_t* lab1 = (int32_t*)(ws + o_comm + nb);
+        // B7 (continued): rows grouped by label (descending degree within), after the side
+        // stream's label propagation
+        IGP_STEP(cuda_status(cudaStreamWaitEvent(s, ev_lp, 0), "stream wait"));
+        cudaEventDestroy(ev_csr);  // released by the runtime once complete
+        cudaEventDestroy(ev_lp);
+        ev_csr = ev_lp = nullptr;
         int32_t* lfill = (int32_t*)(ws + o_comm + 2 * nb);
         int32_t* lranks = (int32_t*)(ws + o_comm + 3 * nb);
         int32_t* dorder = (int32_t*)(ws + o_comm + 4 * nb);
         int32_t* loff = (int32_t*)(ws + o_comm + 5 * nb);
         const int ng = grid_for(n, 256, di.num_sms, 8);
-        iota_kernel<<<ng, 256, 0, s>>>(lab0, n);
-        IGP_STEP(launch_status("iota_kernel"));
-        for (int it = 0; it < kLabelPropIters; ++it) {
-            label_prop_kernel<<<grid_for((int64_t)n * 32, 256, di.num_sms, 8), 256, 0, s>>>(c.row_ptr, c.col_idx, n,
-                                                                                            lab0, lab1);
-            IGP_STEP(launch_status("label_prop_kernel"));
-            int32_t* t = lab0;
-            lab0 = lab1;
-            lab1 = t;
-        }
         rank_kernel<<<ng, 256, 0, s>>>(c.order, n, inv);  // rank in the degree order
         IGP_STEP(launch_status("rank_kernel"));
         IGP_STEP(cuda_status(cudaMemsetAsync(lab1, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
