@@ -450,16 +450,6 @@ __global__ void __launch_bounds__(256) degree_scatter_kernel(const int32_t* __re
         if (key[k] >= 0) order[base[key[k]] + rank[k]] = i0 + k * 256 + threadIdx.x;
 }
 
-// a non-blocking side stream per device for build work that overlaps the main stream
-cudaStream_t side_stream(int dev) {
-    static std::mutex mu;
-    static cudaStream_t st[64] = {};
-    std::lock_guard<std::mutex> lock(mu);
-    cudaStream_t& x = st[dev & 63];
-    if (!x && cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) x = nullptr;
-    return x;
-}
-
 int grid_for(int64_t work, int threads, int num_sms, int per_sm) {
     int64_t g = (work + threads - 1) / threads;
     int64_t cap = (int64_t)num_sms * per_sm;

@@ -639,13 +639,29 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
 
     igp_status rc = IGP_OK;
     const bool timed = (o.flags & IGP_FLAG_TIME_LAYERS) != 0;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool joined = true;
     do {
         // all filter-step work runs on the relabelled CSR (rows in the handle's degree / community order)
         scale_kernel<<<simple_grid(n, 256, di), 256, 0, s>>>(g.rp_perm, n, (double)o.tau, (double)o.eps, node);
         if ((rc = launch_status("scale_kernel")) != IGP_OK) break;
-        affine_kernel<<<simple_grid((int64_t)n * 32, 256, di), 256, 0, s>>>(g.rp_perm, g.col_perm, n, o.theta,
-                                                                              o.alpha, node);
-        if ((rc = launch_status("affine_kernel")) != IGP_OK) break;
+        // c_i (needed from filter step 2 on: step 1 applies mu = 0) runs on a side stream beside
+        // the first slice's input and first filter step; joined before step 2 (or the slice end)
+        cudaStream_t ss = side_stream(di.device);
+        if ((rc = cuda_status(ss ? cudaSuccess : cudaErrorInvalidResourceHandle, "side stream")) != IGP_OK) break;
+        if ((rc = cuda_status(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event")) != IGP_OK) break;
+        if ((rc = cuda_status(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event")) != IGP_OK) break;
+        if ((rc = cuda_status(cudaEventRecord(ev_fork, s), "event record")) != IGP_OK) break;
+        if ((rc = cuda_status(cudaStreamWaitEvent(ss, ev_fork, 0), "stream wait")) != IGP_OK) break;
+        affine_kernel<<<simple_grid((int64_t)n * 32, 256, di), 256, 0, ss>>>(g.rp_perm, g.col_perm, n, o.theta,
+                                                                               o.alpha, node);
+        rc = launch_status("affine_kernel");
+        if (rc == IGP_OK) rc = cuda_status(cudaEventRecord(ev_join, ss), "event record");
+        if (rc != IGP_OK) {
+            cudaStreamSynchronize(ss);
+            break;
+        }
+        joined = false;
         if ((rc = cuda_status(cudaMemsetAsync(sums, 0, sums_bytes, s), "sums memset")) != IGP_OK) break;
         const int linear = (o.mode == IGP_MODE_LINEAR) ? 1 : 0;
         for (int k = 0; k < nslices && rc == IGP_OK; ++k) {
@@ -665,6 +681,10 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 cudaEventRecord(ts->ev0, s);
             }
             for (int l = 1; l <= L; ++l) {
+                if (l == 2 && !joined) {  // c_i from the side stream
+                    if ((rc = cuda_status(cudaStreamWaitEvent(s, ev_join, 0), "stream wait")) != IGP_OK) break;
+                    joined = true;
+                }
                 LayerArgs a;
                 a.rp = g.rp_perm;
                 a.ci = g.col_perm;
@@ -723,6 +743,9 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
             }
         }
     } while (0);
+    if (!joined) cudaStreamWaitEvent(s, ev_join, 0);  // the workspace is freed behind the side stream
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     free_async(ws, s);
     return rc;
 }

@@ -65,6 +65,15 @@ void free_async(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
+cudaStream_t side_stream(int dev) {
+    static std::mutex mu;
+    static cudaStream_t st[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    cudaStream_t& x = st[dev & 63];
+    if (!x && cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) x = nullptr;
+    return x;
+}
+
 // ---------------------------------------------------------------- layer timer
 namespace {
 struct TimerEntry {

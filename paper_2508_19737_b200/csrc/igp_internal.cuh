@@ -30,6 +30,10 @@ struct DeviceInfo {
 // cached per current device; returns false (and sets the error) if no device
 bool device_info(DeviceInfo* out);
 
+// a non-blocking side stream per device (library-internal fork/join of independent work;
+// every use joins back to the caller's stream before returning)
+cudaStream_t side_stream(int dev);
+
 // stream-ordered allocation helpers (default pool, release threshold raised once)
 cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s);
 void free_async(void* p, cudaStream_t s);
