@@ -11,9 +11,10 @@ Inputs (edge list 160 MB, feature buffers 256 MB at Headline) are larger than th
 
 value   = nnz * d * L * K * n_gpus / max-over-ranks device time   (GEdge·feat/s)
 e2e     = same metric through igp_embed_host (pinned host edges in, host Z~ out)
-roofline= the filter-step kernel: algorithmic bytes per launch (SURVEY.md §8(d)
-          B_step = 4(N+1) + 4 nnz + 4N + 8 N d) / its CUDA-event launch time, vs
-          the measured HBM copy bandwidth (MEASURED_PEAKS.json)
+roofline= the filter-step kernel, per launch: algorithmic bytes B_step / (column-slice launches
+          per step), SURVEY.md §8(d) B_step = 4(N+1) + 4 nnz + 4N + 8 N d, over its average
+          CUDA-event launch time, vs the measured HBM copy bandwidth (MEASURED_PEAKS.json);
+          traffic = ncu DRAM bytes of one launch (profiles/ncu_traffic.json)
 cpu_baseline = the fp64 oracle (oracle/, test infrastructure) on a bounded sample.
 
 --impl reference times the oracle itself as the reference arm (rank 0 only).
@@ -142,14 +143,14 @@ def load_gather_ceiling(config_name):
 
 
 def load_traffic(config_name):
-    """DRAM bytes (read + write) of one filter step, from the committed ncu --set full
-    capture of one slice launch (profiles/ncu_traffic.json) times the launches per step."""
+    """DRAM bytes (read + write) of one filter-step launch, from the committed ncu --set full
+    capture of the bench command (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             t = json.load(f)
         v = t.get(config_name)
-        return None if v is None else float(v["dram_bytes_per_launch"]) * int(v["launches_per_step"])
+        return None if v is None else float(v["dram_bytes_per_launch"])
     except Exception:
         return None
 
@@ -321,9 +322,13 @@ def run_gpu(args, cfg):
     peak, peak_src = hbm_peak()
     achieved = b_step / step_s / 1e9
     traffic = load_traffic(cfg.name)
+    # per launch (the contract's unit): one filter step is `slices` column-slice launches, so a
+    # launch's algorithmic bytes are B_step / slices and achieved = that / the average launch
+    # time (identical to B_step / step time); traffic is the ncu DRAM bytes of one launch
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": f"layer_kernel<{width}> x {slices} slice launches per filter step",
-            "per": "filter step (all d columns)", "algorithmic_bytes": b_step,
+            "traffic": traffic, "kernel": f"layer_kernel<{width}> ({slices} column-slice launches per filter step)",
+            "per": "launch", "algorithmic_bytes": b_step / slices, "algorithmic_bytes_per_step": b_step,
+            "traffic_per_step": None if traffic is None else traffic * slices,
             "step_us": step_s * 1e6, "avg_launch_us": avg_launch_s * 1e6, "peak_source": peak_src,
             "gather_bytes_per_step": 4 * nnz * d, "gather_GBps": 4 * nnz * d / step_s / 1e9,
             "gather_ceiling_GBps": load_gather_ceiling(cfg.name),
