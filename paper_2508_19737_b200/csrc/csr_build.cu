@@ -209,7 +209,7 @@ __device__ __forceinline__ int warp_sort_dedup(int32_t* seg, int len, int lane) 
     while (P < len) P <<= 1;
 #pragma unroll
     for (int k = 2; k <= 32 * E; k <<= 1) {
-        if (k > P) break;
+        if (k > P) continue;  // warp-uniform; `continue` keeps the loop fully unrolled (static indices)
 #pragma unroll
         for (int j = k >> 1; j > 0; j >>= 1) {
             if (j >= 32) {
@@ -274,9 +274,10 @@ __global__ void __launch_bounds__(256) sort_rows_warp_kernel(const int32_t* __re
             if (lane == 0) ucnt[r] = len;
             continue;
         }
-        if (len <= 64) {  // registers: two elements per lane, bitonic network over shuffles (measured:
-                          // faster than shared memory here, slower for 4-8 elements per lane)
-            const int u = warp_sort_dedup<2>(tmp + o, len, lane);  // converged: all lanes shuffle
+        if (len <= 256) {  // registers: up to 8 elements per lane, bitonic network over shuffles
+            const int u = len <= 64    ? warp_sort_dedup<2>(tmp + o, len, lane)
+                          : len <= 128 ? warp_sort_dedup<4>(tmp + o, len, lane)
+                                       : warp_sort_dedup<8>(tmp + o, len, lane);  // len is warp-uniform
             if (lane == 0) ucnt[r] = u;
             continue;
         }
