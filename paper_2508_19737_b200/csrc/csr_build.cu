@@ -404,51 +404,90 @@ __global__ void compact_kernel(const int32_t* __restrict__ off, const int32_t* _
 }
 
 // ---------------------------------------------------------------- row schedule (degree-descending order)
-// Bucket key = kDegBuckets-1-min(deg, kDegBuckets-1); a block-aggregated counting sort.
-// The order within a bucket is arbitrary: each row's result is independent of where it
-// is scheduled, and the layer statistics are exact sums (embed.cu), so outputs do not
-// depend on this order.
+// Bucket key = kDegBuckets-1-min(deg, kDegBuckets-1), sorted stably (ties by ascending id):
+// the order is deterministic, so the per-row summation order and the output are too.
 constexpr int kDegBuckets = 1024;
-constexpr int kSchedTile = 2048;
 
 __device__ __forceinline__ int deg_key(const int32_t* rp, int32_t i) {
     const int32_t deg = rp[i + 1] - rp[i];
     return kDegBuckets - 1 - (deg < kDegBuckets - 1 ? deg : kDegBuckets - 1);
 }
 
-__global__ void __launch_bounds__(256) degree_hist_kernel(const int32_t* __restrict__ rp, int32_t n,
-                                                          int32_t* __restrict__ hist) {
-    __shared__ int32_t sh[kDegBuckets];
-    for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x) sh[b] = 0;
-    __syncthreads();
+// ---------------------------------------------------------------- stable LSD counting-sort passes
+// Sort (key, val) pairs by key, stably (equal keys keep their input order), one 2^kDigitBits
+// digit per pass: per-tile digit histograms (key-major, so one exclusive scan gives every
+// (digit, tile) its output offset), then one warp per tile walks its elements in order and
+// ranks equal digits with __match_any_sync.  Used for the row orders (degree buckets; labels
+// over the degree order), which must be deterministic.
+constexpr int kDigitBits = 12;
+constexpr int kDigits = 1 << kDigitBits;
+constexpr int kSortTile = 4096;
+
+__global__ void degree_keys_kernel(const int32_t* __restrict__ rp, int32_t n, int32_t* __restrict__ keys,
+                                   int32_t* __restrict__ vals) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-        atomicAdd(&sh[deg_key(rp, (int32_t)i)], 1);
-    __syncthreads();
-    for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x)
-        if (sh[b]) atomicAdd(hist + b, sh[b]);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        keys[i] = deg_key(rp, (int32_t)i);
+        vals[i] = (int32_t)i;
+    }
 }
 
-__global__ void __launch_bounds__(256) degree_scatter_kernel(const int32_t* __restrict__ rp, int32_t n,
-                                                             int32_t* __restrict__ fill, int32_t* __restrict__ order) {
-    __shared__ int32_t cnt[kDegBuckets];
-    __shared__ int32_t base[kDegBuckets];
-    for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x) cnt[b] = 0;
-    __syncthreads();
-    const int32_t i0 = blockIdx.x * kSchedTile;
-    int key[kSchedTile / 256], rank[kSchedTile / 256];
-#pragma unroll
-    for (int k = 0; k < kSchedTile / 256; ++k) {
-        const int32_t i = i0 + k * 256 + threadIdx.x;
-        key[k] = i < n ? deg_key(rp, i) : -1;
-        rank[k] = key[k] >= 0 ? atomicAdd(&cnt[key[k]], 1) : 0;
+__global__ void label_keys_kernel(const int32_t* __restrict__ order, const int32_t* __restrict__ lab, int32_t n,
+                                  int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += stride) {
+        const int32_t v = order[k];
+        keys[k] = lab[v];
+        vals[k] = v;
     }
+}
+
+__global__ void __launch_bounds__(256) tile_digit_hist_kernel(const int32_t* __restrict__ keys, int32_t n, int shift,
+                                                              int32_t ntiles, int32_t* __restrict__ H) {
+    __shared__ int32_t h[kDigits];
+    for (int b = threadIdx.x; b < kDigits; b += blockDim.x) h[b] = 0;
     __syncthreads();
-    for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x) base[b] = cnt[b] ? atomicAdd(fill + b, cnt[b]) : 0;
+    const int64_t t0 = (int64_t)blockIdx.x * kSortTile;
+    for (int i = threadIdx.x; i < kSortTile; i += blockDim.x)
+        if (t0 + i < n) atomicAdd(&h[(keys[t0 + i] >> shift) & (kDigits - 1)], 1);
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kSchedTile / 256; ++k)
-        if (key[k] >= 0) order[base[key[k]] + rank[k]] = i0 + k * 256 + threadIdx.x;
+    for (int b = threadIdx.x; b < kDigits; b += blockDim.x) H[(int64_t)b * ntiles + blockIdx.x] = h[b];
+}
+
+__global__ void __launch_bounds__(32) tile_digit_scatter_kernel(const int32_t* __restrict__ keys,
+                                                                const int32_t* __restrict__ vals, int32_t n,
+                                                                int shift, int32_t ntiles,
+                                                                const int32_t* __restrict__ Hs,
+                                                                int32_t* __restrict__ okeys,
+                                                                int32_t* __restrict__ ovals) {
+    __shared__ int32_t cnt[kDigits];
+    const int lane = threadIdx.x;
+    for (int b = lane; b < kDigits; b += 32) cnt[b] = 0;
+    __syncwarp();
+    const int64_t t0 = (int64_t)blockIdx.x * kSortTile;
+    for (int c = 0; c < kSortTile; c += 32) {
+        const int64_t i = t0 + c + lane;
+        const bool act = i < n;
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        if (am == 0u) break;
+        int32_t key = 0, val = 0, dg = -1;
+        if (act) {
+            key = keys[i];
+            val = vals[i];
+            dg = (key >> shift) & (kDigits - 1);
+        }
+        if (act) {
+            const unsigned peers = __match_any_sync(am, dg);
+            const int leader = __ffs(peers) - 1;
+            const int32_t base = cnt[dg];  // read by all peers before the leader updates it
+            __syncwarp(am);
+            if (lane == leader) cnt[dg] = base + __popc(peers);
+            const int64_t pos = (int64_t)Hs[(int64_t)dg * ntiles + blockIdx.x] + base + __popc(peers & lanemask_lt());
+            okeys[pos] = key;
+            ovals[pos] = val;
+        }
+        __syncwarp();
+    }
 }
 
 int grid_for(int64_t work, int threads, int num_sms, int per_sm) {
@@ -538,6 +577,37 @@ igp_status segmented_sort(const int32_t* off, int32_t* data, int32_t* ucnt, int3
 
 }  // namespace
 
+namespace {
+
+struct PairSortScratch {
+    int32_t* keys[2];
+    int32_t* vals[2];
+    int32_t* H;   // kDigits x ntiles + 1
+    int32_t* Hs;  // exclusive scan of H
+};
+
+// stable sort of (keys, vals) (n pairs, in scratch keys[0]/vals[0]) by the low `key_bits` bits of
+// the key; the sorted values are written to `out` (which may be one of the scratch buffers)
+igp_status stable_sort_pairs(int32_t n, int key_bits, const PairSortScratch& sc, int32_t* out, cudaStream_t s,
+                             const DeviceInfo& di) {
+    const int32_t ntiles = (n + kSortTile - 1) / kSortTile;
+    int cur = 0;
+    for (int shift = 0; shift < key_bits; shift += kDigitBits) {
+        const bool last = shift + kDigitBits >= key_bits;
+        tile_digit_hist_kernel<<<ntiles, 256, 0, s>>>(sc.keys[cur], n, shift, ntiles, sc.H);
+        IGP_TRY(launch_status("tile_digit_hist_kernel"));
+        IGP_TRY(scan_exclusive(sc.H, sc.Hs, kDigits * ntiles, s));
+        int32_t* ov = last ? out : sc.vals[cur ^ 1];
+        tile_digit_scatter_kernel<<<ntiles, 32, 0, s>>>(sc.keys[cur], sc.vals[cur], n, shift, ntiles, sc.Hs,
+                                                        sc.keys[cur ^ 1], ov);
+        IGP_TRY(launch_status("tile_digit_scatter_kernel"));
+        cur ^= 1;
+    }
+    return IGP_OK;
+}
+
+}  // namespace
+
 // merge support: row counts start at the base graph's degrees, and the base rows are
 // copied into the front of each bucket before the new edges are scattered behind them
 __global__ void base_degree_kernel(const int32_t* __restrict__ rp, int32_t n, int32_t* __restrict__ cnt) {
@@ -585,55 +655,6 @@ __global__ void __launch_bounds__(256) label_prop_kernel(const int32_t* __restri
     }
 }
 
-// bucket nodes by label; the bucket entries are the nodes' ranks in the degree order.  After
-// label propagation a few hundred labels cover all nodes, so the atomics are warp-aggregated
-// (one per distinct label per warp).
-__global__ void label_count_kernel(const int32_t* __restrict__ lab, int32_t n, int32_t* __restrict__ cnt) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
-        const int64_t i = i0 + threadIdx.x;
-        const bool act = i < n;
-        const unsigned am = __ballot_sync(0xffffffffu, act);
-        if (!act) continue;
-        const int32_t l = lab[i];
-        const unsigned peers = __match_any_sync(am, l);
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + l, __popc(peers));
-    }
-}
-
-__global__ void label_scatter_kernel(const int32_t* __restrict__ lab, const int32_t* __restrict__ rank, int32_t n,
-                                     const int32_t* __restrict__ off, int32_t* __restrict__ fill,
-                                     int32_t* __restrict__ out) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int lane = threadIdx.x & 31;
-    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
-        const int64_t i = i0 + threadIdx.x;
-        const bool act = i < n;
-        const unsigned am = __ballot_sync(0xffffffffu, act);
-        if (!act) continue;
-        const int32_t l = lab[i];
-        const unsigned peers = __match_any_sync(am, l);
-        const int leader = __ffs(peers) - 1;
-        int32_t b = 0;
-        if (lane == leader) b = atomicAdd(fill + l, __popc(peers));
-        b = __shfl_sync(peers, b, leader);
-        out[off[l] + b + __popc(peers & lanemask_lt())] = rank[i];
-    }
-}
-
-// order[k] = deg_order[sorted rank k]: communities by label, descending degree within each
-__global__ void gather_order_kernel(const int32_t* __restrict__ deg_order, const int32_t* __restrict__ ranks, int32_t n,
-                                    int32_t* __restrict__ order) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += stride) order[k] = deg_order[ranks[k]];
-}
-
-// rank[order[r]] = r
-__global__ void rank_kernel(const int32_t* __restrict__ order, int32_t n, int32_t* __restrict__ rank) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += stride) rank[order[r]] = (int32_t)r;
-}
-
 void free_csr(const CsrDevice& c, cudaStream_t s) {
     free_async(c.row_ptr, s);
     free_async(c.col_idx, s);
@@ -667,16 +688,17 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     size_t o_big = al(o_ucnt + sizeof(int32_t) * (size_t)lists);
     size_t o_giant = al(o_big + sizeof(int32_t) * (size_t)lists);
     size_t o_flags = al(o_giant + sizeof(int32_t) * (size_t)lists);  // err, sort counters
-    size_t o_hist = al(o_flags + 4 * sizeof(int32_t));                // kDegBuckets
-    size_t o_boff = al(o_hist + sizeof(int32_t) * kDegBuckets);       // kDegBuckets + 1
-    size_t o_fill = al(o_boff + sizeof(int32_t) * (kDegBuckets + 1));  // kDegBuckets + 1
-    size_t o_inv = al(o_fill + sizeof(int32_t) * (kDegBuckets + 1));
+    size_t o_inv = al(o_flags + 4 * sizeof(int32_t));
     size_t o_degp = al(o_inv + sizeof(int32_t) * (size_t)n);
     size_t o_bitmap = al(o_degp + sizeof(int32_t) * (size_t)n);
     size_t o_tmp = al(o_bitmap + sizeof(uint32_t) * (size_t)words * kGiantBlocks);
-    size_t o_comm = al(o_tmp + sizeof(int32_t) * (size_t)(raw > 0 ? raw : 1));
+    // stable pair sorts of the row orders: keys / vals double buffers and tile digit histograms
+    const int32_t ntiles = (n + kSortTile - 1) / kSortTile;
+    const size_t hbytes = al(sizeof(int32_t) * ((size_t)kDigits * ntiles + 1));
+    size_t o_psort = al(o_tmp + sizeof(int32_t) * (size_t)(raw > 0 ? raw : 1));
+    size_t o_comm = o_psort + (reorder ? al(sizeof(int32_t) * (size_t)n) * 4 + 2 * hbytes : 0);
     // community order: two label buffers, label bucket offsets / fill, bucketed ranks, degree order
-    const size_t comm_bytes = community ? al(sizeof(int32_t) * (size_t)n) * 5 + al(sizeof(int32_t) * ((size_t)n + 1)) : 0;
+    const size_t comm_bytes = community ? al(sizeof(int32_t) * (size_t)n) * 2 : 0;  // two label buffers
     size_t total = o_comm + comm_bytes;
     char* ws = nullptr;
     IGP_CUDA(alloc_async((void**)&ws, total, s), "build workspace alloc");
@@ -684,13 +706,20 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     int32_t* off = (int32_t*)(ws + o_off);
     int32_t* ucnt = (int32_t*)(ws + o_ucnt);
     int32_t* flags = (int32_t*)(ws + o_flags);
-    int32_t* hist = (int32_t*)(ws + o_hist);
-    int32_t* boff = (int32_t*)(ws + o_boff);
-    int32_t* fill = (int32_t*)(ws + o_fill);
     int32_t* inv = (int32_t*)(ws + o_inv);
     int32_t* degp = (int32_t*)(ws + o_degp);
     int32_t* tmp = (int32_t*)(ws + o_tmp);
     SortScratch sc{(int32_t*)(ws + o_big), (int32_t*)(ws + o_giant), flags, (uint32_t*)(ws + o_bitmap)};
+    PairSortScratch psc{};
+    if (reorder) {
+        const size_t nb4 = al(sizeof(int32_t) * (size_t)n);
+        psc.keys[0] = (int32_t*)(ws + o_psort);
+        psc.vals[0] = (int32_t*)(ws + o_psort + nb4);
+        psc.keys[1] = (int32_t*)(ws + o_psort + 2 * nb4);
+        psc.vals[1] = (int32_t*)(ws + o_psort + 3 * nb4);
+        psc.H = (int32_t*)(ws + o_psort + 4 * nb4);
+        psc.Hs = (int32_t*)(ws + o_psort + 4 * nb4 + hbytes);
+    }
 
     CsrDevice c;
     c.n = n;
@@ -806,16 +835,12 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         }
         ev_lp = lp;
     }
-    // B6a: degree-descending order (counting sort by degree, then ascending id per bucket)
-    IGP_STEP(cuda_status(cudaMemsetAsync(hist, 0, sizeof(int32_t) * kDegBuckets, s), "memset"));
-    degree_hist_kernel<<<grid_for(n, 256, di.num_sms, 4), 256, 0, s>>>(c.row_ptr, n, hist);
-    IGP_STEP(launch_status("degree_hist_kernel"));
-    IGP_STEP(scan_exclusive(hist, boff, kDegBuckets, s));
-    IGP_STEP(cuda_status(
-        cudaMemcpyAsync(fill, boff, sizeof(int32_t) * (kDegBuckets + 1), cudaMemcpyDeviceToDevice, s), "copy"));
-    degree_scatter_kernel<<<(n + kSchedTile - 1) / kSchedTile, 256, 0, s>>>(c.row_ptr, n, fill, c.order);
-    IGP_STEP(launch_status("degree_scatter_kernel"));
-    IGP_STEP(segmented_sort(boff, c.order, hist, kDegBuckets, n, n, sc, s, di));
+    // B6a: degree-descending order, ties by ascending id: one stable counting-sort pass of the
+    // ids by degree bucket
+    const int ng = grid_for(n, 256, di.num_sms, 8);
+    degree_keys_kernel<<<ng, 256, 0, s>>>(c.row_ptr, n, psc.keys[0], psc.vals[0]);
+    IGP_STEP(launch_status("degree_keys_kernel"));
+    IGP_STEP(stable_sort_pairs(n, 10, psc, c.order, s, di));  // kDegBuckets = 2^10 keys
     if (community) {
         // B7 (continued): rows grouped by label (descending degree within), after the side
         // stream's label propagation
@@ -823,25 +848,13 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         cudaEventDestroy(ev_csr);  // released by the runtime once complete
         cudaEventDestroy(ev_lp);
         ev_csr = ev_lp = nullptr;
-        int32_t* lfill = (int32_t*)(ws + o_comm + 2 * nb);
-        int32_t* lranks = (int32_t*)(ws + o_comm + 3 * nb);
-        int32_t* dorder = (int32_t*)(ws + o_comm + 4 * nb);
-        int32_t* loff = (int32_t*)(ws + o_comm + 5 * nb);
-        const int ng = grid_for(n, 256, di.num_sms, 8);
-        rank_kernel<<<ng, 256, 0, s>>>(c.order, n, inv);  // rank in the degree order
-        IGP_STEP(launch_status("rank_kernel"));
-        IGP_STEP(cuda_status(cudaMemsetAsync(lab1, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
-        label_count_kernel<<<ng, 256, 0, s>>>(lab0, n, lab1);
-        IGP_STEP(launch_status("label_count_kernel"));
-        IGP_STEP(scan_exclusive(lab1, loff, n, s));
-        IGP_STEP(cuda_status(cudaMemsetAsync(lfill, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
-        label_scatter_kernel<<<ng, 256, 0, s>>>(lab0, inv, n, loff, lfill, lranks);
-        IGP_STEP(launch_status("label_scatter_kernel"));
-        IGP_STEP(segmented_sort(loff, lranks, lab1, n, n, n, sc, s, di));  // ranks unique: no entry dropped
-        IGP_STEP(cuda_status(cudaMemcpyAsync(dorder, c.order, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s),
-                             "copy"));
-        gather_order_kernel<<<ng, 256, 0, s>>>(dorder, lranks, n, c.order);
-        IGP_STEP(launch_status("gather_order_kernel"));
+        // stable sort of the degree-ordered node sequence by label: communities in label order,
+        // degree order (then id) inside each
+        label_keys_kernel<<<ng, 256, 0, s>>>(c.order, lab0, n, psc.keys[0], psc.vals[0]);
+        IGP_STEP(launch_status("label_keys_kernel"));
+        int lbits = 1;
+        while (lbits < 31 && ((int64_t)1 << lbits) < (int64_t)n) ++lbits;  // labels are node ids < n
+        IGP_STEP(stable_sort_pairs(n, lbits, psc, c.order, s, di));
     }
     // B6b: the relabelled CSR the filter steps run on (rows by descending degree, or by community)
     inverse_perm_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n, inv, c.row_ptr, degp);
