@@ -421,7 +421,7 @@ __device__ __forceinline__ int deg_key(const int32_t* rp, int32_t i) {
 // over the degree order), which must be deterministic.
 constexpr int kDigitBits = 12;
 constexpr int kDigits = 1 << kDigitBits;
-constexpr int kSortTile = 4096;
+constexpr int kSortTile = 2048;
 
 __global__ void degree_keys_kernel(const int32_t* __restrict__ rp, int32_t n, int32_t* __restrict__ keys,
                                    int32_t* __restrict__ vals) {
