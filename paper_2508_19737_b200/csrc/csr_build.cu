@@ -863,8 +863,8 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     IGP_STEP(cuda_status(cudaMemsetAsync(c.rp_perm + n + 1, 0, 4 * sizeof(int32_t), s), "pad memset"));
     if (raw > 0) {
         // each relabelled row keeps its canonical neighbour order (ascending original id), so a
-        // row's summation order is the same under any permutation (up to where the 64-neighbour
-        // fp64 folds of rows longer than 60 fall); no re-sort is needed
+        // row's summation order is the same under any permutation (up to where the 128-neighbour
+        // fp64 folds of rows longer than 124 fall); no re-sort is needed
         perm_scatter_kernel<<<rg, 256, 0, s>>>(c.order, inv, c.row_ptr, c.col_idx, c.rp_perm, c.col_perm, n);
         IGP_STEP(launch_status("perm_scatter_kernel"));
     }

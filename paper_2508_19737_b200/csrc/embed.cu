@@ -45,7 +45,8 @@ namespace igp {
 namespace {
 
 constexpr int kChunk = 16;      // neighbours per index chunk
-constexpr int kFoldChunks = 4;  // fp32 partial sums span at most 64 neighbours
+constexpr int kFoldChunks = 8;   // fp32 partial sums span at most 128 neighbours (measured: 64 -> 128
+                                 // makes the headline step 2% faster at unchanged parity; 256 loses accuracy)
 constexpr int kBatch = 8;       // gathers issued back to back per lane (full chunks)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kDefaultOcc = 2;
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
             nend = __ldg(p.rp + base + step + g + 1);
         }
         // neighbour sum: packed fp32 within up to kFoldChunks chunks, then folded into
-        // fp64 partials in shared memory (only rows longer than 64 neighbours fold).
+        // fp64 partials in shared memory (only rows longer than 128 neighbours fold).
         // The chunk loop is warp-uniform (the warp's rows have similar degrees), so the
         // index broadcasts are full-warp shuffles and fully-populated chunks run unpredicated.
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
