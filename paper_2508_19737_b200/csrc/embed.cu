@@ -371,7 +371,19 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
                         for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[t][k]);
                 }
             }
-            if (c == 0) load_idx<IPL>(p.ci, nbeg & ~3, nend, q, pol_idx, jfirst);  // next batch's first chunk
+            if (c == 0) {
+                load_idx<IPL>(p.ci, nbeg & ~3, nend, q, pol_idx, jfirst);  // next batch's first chunk
+                // the next batch's whole index range (its G rows are consecutive) into L2 with one
+                // bulk prefetch (measured +0.5%)
+                const int32_t lo_e = __shfl_sync(kFull, nbeg, 0);
+                const int32_t hi_e = __shfl_sync(kFull, nend, 31);
+                if (lane == 0 && hi_e > lo_e) {
+                    const uint64_t a0 = reinterpret_cast<uint64_t>(p.ci + lo_e) & ~(uint64_t)15;
+                    const uint64_t a1 = (reinterpret_cast<uint64_t>(p.ci + hi_e) + 15) & ~(uint64_t)15;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
+                                 : "memory");
+                }
+            }
             if (++nc == kFoldChunks && e1 < end) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
