@@ -58,7 +58,7 @@ typedef enum {
     IGP_ERR_NUMERICAL = 4,   /* reserved */
     IGP_ERR_CUDA = 5,        /* CUDA runtime/launch error (detail in igp_last_error_message) */
     IGP_ERR_OOM = 6,         /* device allocation failed */
-    IGP_ERR_UNSUPPORTED = 7  /* valid request outside this build's envelope (e.g. d not in {16,32,64,128}) */
+    IGP_ERR_UNSUPPORTED = 7  /* valid request outside this build's envelope (e.g. d not a multiple of 16) */
 } igp_status;
 
 /* ---------------------------------------------------------------------------
@@ -154,7 +154,7 @@ IGP_API igp_status igp_destroy_graph_async(igp_graph_t g, igp_stream_t stream);
 
 typedef struct {
     float tau;            /* degree correction tau (Eq. (1) for tau < 0; D + tau I otherwise); finite */
-    int32_t d;            /* embedding dimensionality, one of 16, 32, 64, 128 */
+    int32_t d;            /* embedding dimensionality: a multiple of 16 in [16, 1024] (the paper uses 16-64) */
     int32_t steps;        /* L >= 0 filter steps (layers) */
     uint64_t seed;        /* Philox key for Theta */
     uint64_t subsequence; /* Philox subsequence (e.g. streaming stage t, Alg. 2 l.3) */
@@ -180,7 +180,7 @@ IGP_API void igp_embed_opts_default(igp_embed_opts* opts);
  * allocated stream-ordered (cudaMallocAsync) and released before return, so the
  * handle is read-only and concurrent embeds on different streams are safe.
  * Errors (host-validated, nothing enqueued): NULL g/d_out or non-finite tau ->
- * IGP_ERR_INPUT; d not in {16,32,64,128} -> IGP_ERR_UNSUPPORTED; steps < 0 ->
+ * IGP_ERR_INPUT; d not a multiple of 16 in [16, 1024] -> IGP_ERR_UNSUPPORTED; steps < 0 ->
  * IGP_ERR_INPUT.  Deterministic: identical arguments give bitwise-identical output. */
 IGP_API igp_status igp_embed(igp_graph_t g, float tau, int32_t d, int32_t steps, uint64_t seed,
                      float* d_out, igp_stream_t stream);

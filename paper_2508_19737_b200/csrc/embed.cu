@@ -598,14 +598,15 @@ double gather_gbps(int row_bytes, double footprint_mb) {
 // slice width: minimise predicted gather time + the CSR re-read per slice (IGP_SLICE_WIDTH overrides)
 int choose_width(int d, int32_t n, int64_t nnz) {
     // measured (profiles/r01): W=32 slices are fastest once the W=64 slice exceeds ~64 MB
-    // of gathered footprint; the model below reproduces that ranking
+    // of gathered footprint; the model below reproduces that ranking.  W must divide d.
     if (const char* env = getenv("IGP_SLICE_WIDTH")) {
         const int w = atoi(env);
         if ((w == 16 || w == 32 || w == 64 || w == 128) && w <= d && d % w == 0) return w;
     }
-    int best = d;
+    int best = 16;
     double best_t = 1e300;
-    for (int w = d; w >= 16; w /= 2) {  // from the widest: fewer slices win ties
+    for (int w = 128; w >= 16; w /= 2) {  // from the widest: fewer slices win ties
+        if (w > d || d % w != 0) continue;
         const double slices = (double)d / w;
         const double gather = (double)nnz * 4.0 * w / (gather_gbps(4 * w, (double)n * 4.0 * w / 1048576.0) * 1e9);
         const double csr = (4.0 * (double)nnz + 8.0 * n) / 6.0e12;
@@ -615,7 +616,6 @@ int choose_width(int d, int32_t n, int64_t nnz) {
             best = w;
         }
     }
-    if (d / best > kMaxSlices) best = d / kMaxSlices;
     return best;
 }
 
@@ -768,8 +768,8 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
 igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s, HostCopy* hc) {
     DeviceInfo di;
     if (!device_info(&di)) return IGP_ERR_CUDA;
-    if (o.d != 16 && o.d != 32 && o.d != 64 && o.d != 128) {
-        set_error("igp_embed: d must be one of 16, 32, 64, 128");
+    if (o.d < 16 || o.d > kMaxD || o.d % 16 != 0) {
+        set_error("igp_embed: d must be a multiple of 16 in [16, 1024]");
         return IGP_ERR_UNSUPPORTED;
     }
     const char* occ_env = getenv("IGP_LAYER_OCC");  // development knob: 2 or 3 blocks per SM

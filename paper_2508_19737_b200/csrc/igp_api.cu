@@ -188,8 +188,8 @@ static igp_status check_opts(const igp_embed_opts* o) {
         set_error("unknown mode");
         return IGP_ERR_INPUT;
     }
-    if (o->d != 16 && o->d != 32 && o->d != 64 && o->d != 128) {
-        set_error("d must be one of 16, 32, 64, 128");
+    if (o->d < 16 || o->d > kMaxD || o->d % 16 != 0) {
+        set_error("d must be a multiple of 16 in [16, 1024]");
         return IGP_ERR_UNSUPPORTED;
     }
     return IGP_OK;
@@ -486,7 +486,7 @@ igp_status igp_embed_host(const int32_t* h_edges, int64_t num_edges, int32_t num
     HostCopy hc;
     hc.h_out = h_out;
     st = cuda_status(cudaStreamCreateWithFlags(&hc.cs, cudaStreamNonBlocking), "copy stream");
-    for (int k = 0; k < kMaxSlices && st == IGP_OK; ++k)
+    for (int k = 0; k < opts->d / 16 && st == IGP_OK; ++k)  // at most d/16 column slices
         st = cuda_status(cudaEventCreateWithFlags(&hc.ev[k], cudaEventDisableTiming), "event");
     if (st == IGP_OK) st = cuda_status(alloc_async((void**)&d_out, ob, s), "out alloc");
     if (st == IGP_OK) st = cuda_status(cudaStreamWaitEvent(s, g->ready, 0), "stream wait");

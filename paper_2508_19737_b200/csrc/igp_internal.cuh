@@ -99,7 +99,8 @@ igp_status launch_philox_normal(uint64_t seed, uint64_t sub, int64_t count, floa
 // ---------------------------------------------------------------------------
 // embed.cu
 // ---------------------------------------------------------------------------
-constexpr int kMaxSlices = 8;
+constexpr int kMaxD = 1024;                // embedding widths: multiples of 16 up to this
+constexpr int kMaxSlices = kMaxD / 16;     // column slices of width W in {16, 32, 64, 128} dividing d
 // process-wide filter-step timer (igp_layer_timer_*): a pair of events per timed slice
 struct TimerSlot {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;

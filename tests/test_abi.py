@@ -90,6 +90,9 @@ def test_more_host_validated_errors(igp):
     o.flags = 0
     o.eps = 0.0
     assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o), out, None) == 2               # eps must be > 0
+    for bad_d in (40, 8, 2048):                                                          # multiple of 16 in [16, 1024]
+        o2 = igp.make_opts(-1.0, bad_d, 3)
+        assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o2), out, None) == 7
     assert lib.igp_kernel_launch_count() == 0
 
 

@@ -138,7 +138,7 @@ def test_embed_medium_config(igp, tau, seed):
     assert err <= TOL
 
 
-@pytest.mark.parametrize("d", [16, 32, 64, 128])
+@pytest.mark.parametrize("d", [16, 32, 48, 64, 96, 128, 192, 256])
 @pytest.mark.parametrize("n", [1, 7, 777, 4099])
 def test_embed_dims_and_ragged_sizes(igp, d, n):
     rng = np.random.default_rng(n + d)
@@ -209,9 +209,10 @@ def test_embed_host_matches_device_path(igp):
 
 def test_embed_argument_errors(igp):
     g = gpu_graph(igp, np.array([[0, 1]], np.int32), 2)
-    with pytest.raises(igp.IGPError) as ei:
-        igp.embed(g, -1.0, 48, 3, 0)
-    assert ei.value.status == 7
+    for bad_d in (40, 8, 2048):  # d must be a multiple of 16 in [16, 1024]
+        with pytest.raises(igp.IGPError) as ei:
+            igp.embed(g, -1.0, bad_d, 3, 0)
+        assert ei.value.status == 7
     with pytest.raises(igp.IGPError):
         igp.embed(g, float("nan"), 64, 3, 0)
     with pytest.raises(igp.IGPError):
