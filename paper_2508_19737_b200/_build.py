@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-Xcompiler", "-fvisibility=hidden",
          "-I" + os.path.join(ROOT, "include")]
+if os.environ.get("IGP_DEBUG") == "1":  # device asserts on every dereferenced index (igp_internal.cuh)
+    FLAGS += ["-DIGP_DEBUG"]
 
 
 def _stale(target: str, deps) -> bool:

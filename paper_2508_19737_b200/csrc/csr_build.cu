@@ -70,7 +70,9 @@ __global__ void scatter_kernel(const int32_t* __restrict__ edges, int64_t E, int
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += stride) {
         const int32_t u = __ldg(edges + 2 * e), v = __ldg(edges + 2 * e + 1);
         if ((unsigned)u >= (unsigned)n || (unsigned)v >= (unsigned)n || u == v) continue;
-        tmp[off[u] + atomicAdd(fill + u, 1)] = v;
+        const int32_t pu = off[u] + atomicAdd(fill + u, 1);
+        IGP_DASSERT(pu >= off[u] && pu < off[u + 1]);
+        tmp[pu] = v;
         tmp[off[v] + atomicAdd(fill + v, 1)] = u;
     }
 }
@@ -399,7 +401,10 @@ __global__ void compact_kernel(const int32_t* __restrict__ off, const int32_t* _
     const int32_t nwarps = gridDim.x * (blockDim.x >> 5);
     for (int32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nwarps) {
         const int32_t src = off[r], dst = row_ptr[r], len = row_ptr[r + 1] - dst;
-        for (int32_t i = lane; i < len; i += 32) col_idx[dst + i] = tmp[src + i];
+        for (int32_t i = lane; i < len; i += 32) {
+            IGP_DASSERT(tmp[src + i] >= 0 && tmp[src + i] < n);
+            col_idx[dst + i] = tmp[src + i];
+        }
     }
 }
 
@@ -483,6 +488,7 @@ __global__ void __launch_bounds__(32) tile_digit_scatter_kernel(const int32_t* _
             __syncwarp(am);
             if (lane == leader) cnt[dg] = base + __popc(peers);
             const int64_t pos = (int64_t)Hs[(int64_t)dg * ntiles + blockIdx.x] + base + __popc(peers & lanemask_lt());
+            IGP_DASSERT(pos >= 0 && pos < n);
             okeys[pos] = key;
             ovals[pos] = val;
         }
@@ -541,7 +547,10 @@ __global__ void perm_scatter_kernel(const int32_t* __restrict__ order, const int
     for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
         const int32_t o = order[r];
         const int32_t src = rp[o], len = rp[o + 1] - src, dst = rpp[r];
-        for (int32_t k = lane; k < len; k += 32) cip[dst + k] = inv[ci[src + k]];
+        for (int32_t k = lane; k < len; k += 32) {
+            IGP_DASSERT(ci[src + k] >= 0 && ci[src + k] < n && inv[ci[src + k]] >= 0 && inv[ci[src + k]] < n);
+            cip[dst + k] = inv[ci[src + k]];
+        }
     }
 }
 
@@ -644,7 +653,10 @@ __global__ void __launch_bounds__(256) label_prop_kernel(const int32_t* __restri
         const int len = min(rp[r + 1] - beg, 31);
         const bool act = lane <= len;
         int32_t lab = INT_MAX;
-        if (lane < len) lab = lin[ci[beg + lane]];
+        if (lane < len) {
+            IGP_DASSERT(ci[beg + lane] >= 0 && ci[beg + lane] < n);
+            lab = lin[ci[beg + lane]];
+        }
         else if (lane == len) lab = lin[r];
         const unsigned am = __ballot_sync(0xffffffffu, act);
         int cnt = 0;

@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
                     for (int t = 0; t < kBatch; ++t) {
                         const int u = u0 + t;
                         const int j = __shfl_sync(kFull, jr[u % IPL], u / IPL, LPR);
+                        IGP_DASSERT(j >= 0 && j < p.n);
                         ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
                     }
 #pragma unroll
@@ -363,7 +364,10 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
                         const int u = u0 + t;
                         const int j = __shfl_sync(kFull, jr[u % IPL], u / IPL, LPR);
                         v[t][0] = v[t][1] = v[t][2] = v[t][3] = 0ull;
-                        if (u >= lo && u < hi) ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
+                        if (u >= lo && u < hi) {
+                            IGP_DASSERT(j >= 0 && j < p.n);
+                            ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
+                        }
                     }
 #pragma unroll
                     for (int t = 0; t < kBatch; ++t)
@@ -522,6 +526,7 @@ __global__ void output_kernel(const float4* __restrict__ y, const float4* __rest
                 a[k] = (mode == IGP_MODE_FULL) ? 1.0f / (1.0f + expf(-z)) : z;
             }
         }
+        IGP_DASSERT(order[i] >= 0 && order[i] < n);
         *(float4*)(out + (int64_t)order[i] * d + col0 + 4 * q) = make_float4(a[0], a[1], a[2], a[3]);
     }
 }

@@ -11,6 +11,16 @@
 
 #include "../../include/igp.h"
 
+// Debug builds (IGP_DEBUG=1 python paper_2508_19737_b200/_build.py --force) check every index a
+// kernel dereferences with device asserts (compute-sanitizer is unavailable on the GPU pool);
+// release builds compile the checks away.
+#ifdef IGP_DEBUG
+#include <cassert>
+#define IGP_DASSERT(cond) assert(cond)
+#else
+#define IGP_DASSERT(cond) ((void)0)
+#endif
+
 namespace igp {
 
 // error detail string, thread-local
