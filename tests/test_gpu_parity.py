@@ -704,3 +704,18 @@ def test_initial_state_hook(igp, cfg):
         record(f"{cfg}_z0_{order}", err)
         assert err <= TOL, order
         g.close()
+
+
+@pytest.mark.parametrize("tau,theta,alpha,L", [(-1.0, 0.1, 1.0, 200),   # many layers: no drift to NaN/inf
+                                               (1e6, 0.1, 1.0, 10),     # huge positive correction: s ~ 1e-3
+                                               (-1.0, 0.0, 0.0, 5),     # phi* = 0: constant columns -> 0.5
+                                               (-1.0, 1.0, -1.0, 8),    # alpha < 0 (Eq. (2) allows [-1, 1])
+                                               (-2.5, 0.0, 1.0, 8)])    # no self term
+def test_parameter_extremes(igp, tau, theta, alpha, L):
+    c = CONFIGS["tiny"]
+    edges, _ = generate(c)
+    z, ref = run_parity(igp, edges, c.num_nodes, 32, L, tau, seed=9, theta=theta, alpha=alpha)
+    assert np.all(np.isfinite(z))
+    err = row_rel_err(z, ref)
+    record(f"extreme_tau{tau}_theta{theta}_alpha{alpha}_L{L}", err)
+    assert err <= TOL
