@@ -719,3 +719,52 @@ def test_parameter_extremes(igp, tau, theta, alpha, L):
     err = row_rel_err(z, ref)
     record(f"extreme_tau{tau}_theta{theta}_alpha{alpha}_L{L}", err)
     assert err <= TOL
+
+
+@pytest.mark.parametrize("case", ["empty", "star", "two_cliques_bridge", "ragged"])
+def test_community_order_adversarial(igp, case):
+    """The label-propagation order on graphs where communities are degenerate (no edges, one hub,
+    two dense blocks, random): canonical CSR unchanged, embeddings match the oracle."""
+    rng = np.random.default_rng(4)
+    if case == "empty":
+        n, edges = 300, np.zeros((0, 2), np.int32)
+    elif case == "star":
+        n = 3000
+        edges = np.stack([np.zeros(n - 1, np.int32), np.arange(1, n, dtype=np.int32)], 1)
+    elif case == "two_cliques_bridge":
+        a = np.array([(i, j) for i in range(40) for j in range(i + 1, 40)], np.int32)
+        edges = np.concatenate([a, a + 40, [[0, 40]]]).astype(np.int32)
+        n = 80
+    else:
+        n = 2049
+        edges = rng.integers(0, n, (9000, 2)).astype(np.int32)
+    e = torch.from_numpy(np.ascontiguousarray(edges)).cuda()
+    g = igp.build_graph(e, n, order="community")
+    rp, ci = g.csr()
+    rp_o, ci_o, _ = oracle.build_csr(edges, n)
+    assert np.array_equal(rp.cpu().numpy(), rp_o) and np.array_equal(ci.cpu().numpy(), ci_o)
+    z = igp.embed(g, -1.0, 32, 8, 2).cpu().numpy()
+    ref = oracle.embed(rp_o, ci_o, n, 32, 8, -1.0, seed=2, nthreads=NTHREADS)
+    err = row_rel_err(z, ref)
+    record(f"community_{case}", err)
+    assert err <= TOL
+
+
+def test_streaming_merges_in_community_order(igp):
+    """igp_graph_add_edges keeps the graph's row order mode: merges of a community-ordered graph
+    stay canonical and embed like the oracle."""
+    from synth.dcsbm import stream_batches
+    c = CONFIGS["medium"]
+    edges, _ = generate(c)
+    batches = stream_batches(edges, 4)
+    g = igp.build_graph(torch.from_numpy(batches[0]).cuda(), c.num_nodes, order="community")
+    for b in batches[1:]:
+        g.add_edges(torch.from_numpy(b).cuda())
+    rp, ci = g.csr()
+    rp_o, ci_o, _ = oracle.build_csr(edges, c.num_nodes)
+    assert np.array_equal(rp.cpu().numpy(), rp_o) and np.array_equal(ci.cpu().numpy(), ci_o)
+    z = igp.embed(g, c.tau, c.d, 10, 0).cpu().numpy()
+    ref = oracle.embed(rp_o, ci_o, c.num_nodes, c.d, 10, c.tau, seed=0, nthreads=NTHREADS)
+    err = row_rel_err(z, ref)
+    record("streaming_community_merged", err)
+    assert err <= TOL
