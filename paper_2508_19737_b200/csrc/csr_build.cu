@@ -667,6 +667,17 @@ __global__ void __launch_bounds__(256) label_prop_kernel(const int32_t* __restri
     }
 }
 
+// label-propagation sweep 1 from lin[i] = i (all counts 1): the smallest id among the node and its
+// first <= 31 neighbours; neighbours are in ascending order, so that is min(i, first neighbour)
+__global__ void lp_first_sweep_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, int32_t n,
+                                      int32_t* __restrict__ lout) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int32_t beg = rp[i];
+        lout[i] = rp[i + 1] > beg ? min((int32_t)i, ci[beg]) : (int32_t)i;
+    }
+}
+
 void free_csr(const CsrDevice& c, cudaStream_t s) {
     free_async(c.row_ptr, s);
     free_async(c.col_idx, s);
@@ -829,9 +840,11 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         IGP_STEP(cuda_status(cudaEventRecord(ev_csr, s), "event record"));
         IGP_STEP(cuda_status(cudaStreamWaitEvent(ss, ev_csr, 0), "stream wait"));
         const int ng = grid_for(n, 256, di.num_sms, 8);
-        iota_kernel<<<ng, 256, 0, ss>>>(lab0, n);
-        igp_status lst = launch_status("iota_kernel");
-        for (int it = 0; it < kLabelPropIters && lst == IGP_OK; ++it) {
+        // sweep 1 from the identity labels in closed form: every label counts once, so the tie rule
+        // picks the smallest of {i} and the first <= 31 neighbours, i.e. min(i, first neighbour)
+        lp_first_sweep_kernel<<<ng, 256, 0, ss>>>(c.row_ptr, c.col_idx, n, lab0);
+        igp_status lst = launch_status("lp_first_sweep_kernel");
+        for (int it = 1; it < kLabelPropIters && lst == IGP_OK; ++it) {
             label_prop_kernel<<<grid_for((int64_t)n * 32, 256, di.num_sms, 8), 256, 0, ss>>>(c.row_ptr, c.col_idx, n,
                                                                                              lab0, lab1);
             lst = launch_status("label_prop_kernel");
