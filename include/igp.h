@@ -72,7 +72,7 @@ typedef enum {
  *              {u, v}, u != v, becomes A_uv = A_vu = 1 once.
  *   num_edges  >= 0 (0 is valid: M = 0, all degrees 0); 2*num_edges must be
  *              <= INT32_MAX - 64 (int32 CSR offsets; else IGP_ERR_UNSUPPORTED).
- *   num_nodes  N >= 1 (else IGP_ERR_INPUT).
+ *   num_nodes  N >= 1 (else IGP_ERR_INPUT) and <= INT32_MAX - 64 (else IGP_ERR_UNSUPPORTED).
  *   out        receives a new handle owning device row_ptr int32[N+1] and
  *              col_idx int32[2M] (rows ascending, columns strictly ascending); the
  *              column arrays are allocated for the 2*num_edges directed entries before

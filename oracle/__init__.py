@@ -64,6 +64,8 @@ def _load():
     lib.oracle_box_muller.restype = None
     lib.oracle_normal.argtypes = [u64, u64, i64, P]
     lib.oracle_normal.restype = None
+    lib.oracle_normal_at.argtypes = [u64, u64, P, i64, P]
+    lib.oracle_normal_at.restype = None
     lib.oracle_propagate.argtypes = [P, P, i32, i32, P, P, f64, f64, i32, P]
     lib.oracle_propagate.restype = None
     lib.oracle_zscore_columns.argtypes = [P, i32, i32]
@@ -139,6 +141,17 @@ def normal(seed: int, sub: int, count: int) -> np.ndarray:
     lib = _load()
     out = np.zeros(count, dtype=np.float64)
     lib.oracle_normal(seed, sub, count, _ptr(out))
+    return out
+
+
+def normal_at(seed: int, sub: int, index) -> np.ndarray:
+    """Elements ``index`` (flat, any order) of the ``normal(seed, sub, .)`` stream, fp64."""
+    lib = _load()
+    idx = np.ascontiguousarray(np.asarray(index, dtype=np.int64).ravel())
+    if idx.size and idx.min() < 0:
+        raise OracleError("negative stream index")
+    out = np.zeros(idx.size, dtype=np.float64)
+    lib.oracle_normal_at(seed, sub, _ptr(idx), idx.size, _ptr(out))
     return out
 
 

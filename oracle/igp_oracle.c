@@ -184,6 +184,23 @@ void oracle_normal(uint64_t seed, uint64_t sub, int64_t count, double* out) {
     free(r);
 }
 
+/* Element k of the same stream for arbitrary k (sampled checks at sizes where the
+ * whole stream is too large to draw): block b = k / 4 as in oracle_philox_bits, then
+ * the Box-Muller pair (r_{2p}, r_{2p+1}), p = (k % 4) / 2, element k % 2 of it. */
+void oracle_normal_at(uint64_t seed, uint64_t sub, const int64_t* idx, int64_t count, double* out) {
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int64_t m = 0; m < count; ++m) {
+        const int64_t k = idx[m], b = k / 4;
+        uint32_t ctr[4] = {(uint32_t)b, (uint32_t)((uint64_t)b >> 32), (uint32_t)sub, (uint32_t)(sub >> 32)};
+        uint32_t w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        const int p = (int)((k % 4) / 2);
+        double pair[2];
+        oracle_box_muller(w[2 * p], w[2 * p + 1], pair);
+        out[m] = pair[k % 2];
+    }
+}
+
 /* ------------------------------------------------------------------------ */
 /* Eq. (3), PAPER.md:155 (general Eq. (2) form with (alpha, theta)):          */
 /*   phi * Z = theta Z + alpha D_tau^{-1/2} A D_tau^{-1/2} Z                  */

@@ -261,8 +261,8 @@ __global__ void __launch_bounds__(256) sort_rows_warp_kernel(const int32_t* __re
     __shared__ int32_t sbuf[8][kWarpSortCap];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int32_t* buf = sbuf[warp];
-    const int32_t nwarps = gridDim.x * 8;
-    for (int32_t r = blockIdx.x * 8 + warp; r < n; r += nwarps) {
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < n; r += nwarps) {
         const int32_t o = off[r];
         const int len = off[r + 1] - o;
         if (len > kWarpSortCap) {
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(1024) sort_rows_block_kernel(const int32_t* __
     __shared__ int32_t wt[32];
     __shared__ int32_t tot;
     const int32_t cnt = *big_count;
-    for (int32_t b = blockIdx.x; b < cnt; b += gridDim.x) {
+    for (int64_t b = blockIdx.x; b < cnt; b += gridDim.x) {
         const int32_t r = big_list[b];
         const int32_t o = off[r];
         const int len = off[r + 1] - o;
@@ -362,11 +362,11 @@ __global__ void __launch_bounds__(1024) sort_rows_giant_kernel(const int32_t* __
                                                                uint32_t* __restrict__ bitmap, int32_t n) {
     __shared__ int32_t wt[32];
     __shared__ int32_t tot;
-    const int32_t words = (n + 31) >> 5;
+    const int32_t words = (int32_t)(((int64_t)n + 31) >> 5);
     uint32_t* bm = bitmap + (int64_t)blockIdx.x * words;
     const int32_t cnt = *giant_count;
     const int32_t per = (words + blockDim.x - 1) / blockDim.x;
-    for (int32_t b = blockIdx.x; b < cnt; b += gridDim.x) {
+    for (int64_t b = blockIdx.x; b < cnt; b += gridDim.x) {
         const int32_t r = giant_list[b];
         const int32_t o = off[r];
         const int32_t len = off[r + 1] - o;
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(1024) sort_rows_giant_kernel(const int32_t* __
 __global__ void compact_kernel(const int32_t* __restrict__ off, const int32_t* __restrict__ tmp,
                                const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx, int32_t n) {
     const int lane = threadIdx.x & 31;
-    const int32_t nwarps = gridDim.x * (blockDim.x >> 5);
-    for (int32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nwarps) {
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nwarps) {
         const int32_t src = off[r], dst = row_ptr[r], len = row_ptr[r + 1] - dst;
         for (int32_t i = lane; i < len; i += 32) {
             IGP_DASSERT(tmp[src + i] >= 0 && tmp[src + i] < n);
@@ -701,7 +701,7 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         set_error("edge count exceeds the int32 CSR index range");
         return IGP_ERR_UNSUPPORTED;
     }
-    const int32_t words = (n + 31) >> 5;
+    const int32_t words = (int32_t)(((int64_t)n + 31) >> 5);
     const int32_t lists = n > kDegBuckets ? n : kDegBuckets;
     // temporaries in one stream-ordered block
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };

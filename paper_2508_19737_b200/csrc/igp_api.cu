@@ -248,6 +248,10 @@ igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t
         set_error("2*num_edges exceeds the int32 CSR index range");
         return IGP_ERR_UNSUPPORTED;
     }
+    if (num_nodes > kMaxEntries) {  // row_ptr[N] and the row loops stay inside int32 with headroom
+        set_error("num_nodes exceeds INT32_MAX - 64");
+        return IGP_ERR_UNSUPPORTED;
+    }
     igp_graph_s* g = new (std::nothrow) igp_graph_s();
     if (!g) return IGP_ERR_OOM;
     cudaStream_t s = (cudaStream_t)stream;

@@ -60,6 +60,7 @@ def test_host_side_calls_without_device(igp):
     assert lib.igp_build_graph(None, 0, 0, None, ctypes.byref(h)) == 2
     assert lib.igp_build_graph(None, -1, 5, None, ctypes.byref(h)) == 2
     assert lib.igp_build_graph(ctypes.c_void_p(0x1000), 2**31, 5, None, ctypes.byref(h)) == 7  # not dereferenced
+    assert lib.igp_build_graph(None, 0, 2**31 - 1, None, ctypes.byref(h)) == 7                # N > INT32_MAX - 64
     o = igp.make_opts(-1.0, 48, 10)
     assert lib.igp_embed_ex(None, ctypes.byref(o), None, None) == 2
     assert lib.igp_destroy_graph(None) == 0

@@ -768,3 +768,59 @@ def test_streaming_merges_in_community_order(igp):
     err = row_rel_err(z, ref)
     record("streaming_community_merged", err)
     assert err <= TOL
+
+
+# ------------------------------------------------------------------ maximum CSR size
+def test_maximum_csr_size_circulant(igp):
+    """The largest graph the int32 CSR admits (include/igp.h: 2E <= INT32_MAX - 64): the circulant
+    C_n(1..32) with n = 2^25 - 2 has 2E = 64n = 2^31 - 128 directed entries (synth/circulant.py).
+    CSR: bit-exact on every row against its closed form.  One LINEAR filter step (Eq. 3):
+    sampled rows against oracle.propagate over each row's neighbourhood with the oracle's own
+    Philox inputs.  Two FULL layers: the ZNorm properties (column mean 0, population std 1) that
+    hold at any size."""
+    from synth.circulant import circulant_edges, circulant_row
+    k, n = 32, 2**25 - 2
+    assert 2 * n * k <= 2**31 - 1 - 64
+    e = circulant_edges(n, k, "cuda")
+    g = igp.build_graph(e, n)
+    del e
+    assert g.nnz == 2 * n * k and g.num_edges == n * k
+    rp, ci = g.csr()
+    assert torch.equal(rp, torch.arange(n + 1, device="cuda", dtype=torch.int32) * (2 * k))
+    ci2 = ci.view(n, 2 * k)
+    offs = torch.cat([torch.arange(-k, 0), torch.arange(1, k + 1)]).to(device="cuda", dtype=torch.int32)
+    step = 1 << 22
+    for r0 in range(k, n - k, step):
+        r1 = min(r0 + step, n - k)
+        rows = torch.arange(r0, r1, device="cuda", dtype=torch.int32)
+        assert torch.equal(ci2[r0:r1] - rows[:, None], offs.expand(r1 - r0, -1)), f"rows {r0}..{r1}"
+    wrap = list(range(k)) + list(range(n - k, n))
+    ci_w = ci2[wrap].cpu().numpy()
+    for t, i in enumerate(wrap):
+        assert np.array_equal(ci_w[t], circulant_row(n, k, i)), f"row {i}"
+    del rp, ci, ci2
+
+    d, tau, seed = 16, -1.0, 3
+    z = igp.embed(g, tau, d, 1, seed, mode="linear")
+    sample = np.concatenate([[0, 1, k, n // 2, n - k - 1, n - 1], np.random.default_rng(0).integers(0, n, 10)])
+    zs = z[torch.from_numpy(sample).cuda()].cpu().numpy().astype(np.float64)
+    del z
+    Dt = oracle.corrected_degree([2 * k], tau)[0]
+    rp_l = np.array([0] + [2 * k] * (2 * k + 1), np.int32)  # row 0 = the sampled node, others empty
+    ci_l = np.arange(1, 2 * k + 1, dtype=np.int32)
+    worst = 0.0
+    for t, i in enumerate(sample):
+        ids = np.concatenate([[i], circulant_row(n, k, int(i))]).astype(np.int64)
+        X = oracle.normal_at(seed, 0, (ids[:, None] * d + np.arange(d)[None, :]).ravel()).reshape(-1, d)
+        P = oracle.propagate(rp_l, ci_l, np.full(ids.size, Dt), X / np.sqrt(d))[0]
+        worst = max(worst, float(np.max(np.abs(zs[t] - P)) / np.linalg.norm(P)))
+    record("max_size_linear_sampled", worst)
+    assert worst <= 1e-5, worst
+
+    zp = igp.embed(g, tau, d, 2, seed, mode="pre_sigmoid").double()
+    mu, sd = zp.mean(0), zp.std(0, correction=0)
+    assert float(mu.abs().max()) < 1e-5 and float((sd - 1).abs().max()) < 1e-5, (mu, sd)
+    del zp
+    zf = igp.embed(g, tau, d, 2, seed)
+    assert float(zf.min()) > 0.0 and float(zf.max()) < 1.0
+    g.close()

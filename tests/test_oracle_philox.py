@@ -91,3 +91,19 @@ def test_theta_variance_is_one_over_d():
     """Alg. 1 l.2: Theta ~ N(0, 1/d) (reading A1); SPEC.md:179 (1/64 +- 10%)."""
     th = oracle.input_theta(0, 0, 10_000, 64)
     assert abs(th.var() - 1 / 64) < 0.1 / 64
+
+
+def test_normal_at_matches_the_stream_and_curand(curand_pin):
+    """normal_at (sampled elements, used at sizes where the stream is too large to draw) equals
+    the pinned stream element by element, and cuRAND's curand_normal4 at an offset past 2^32 blocks."""
+    x = oracle.normal(11, 2, 1 << 16)
+    idx = np.random.default_rng(5).integers(0, 1 << 16, size=3000)
+    assert np.array_equal(oracle.normal_at(11, 2, idx), x[idx])
+    assert np.array_equal(oracle.normal_at(11, 2, np.arange(64)), x[:64])
+    b = 2**32 + 12345  # block index beyond 32 bits: the counter's high word is used
+    ref = np.zeros(8, dtype=np.float32)
+    curand_pin.pin_curand_normal4(11, 2, 4 * b, 2, np_ptr(ref))
+    got = oracle.normal_at(11, 2, 4 * b + np.arange(8))
+    assert np.max(np.abs(got - ref.astype(np.float64))) < 2e-5
+    with pytest.raises(oracle.OracleError):
+        oracle.normal_at(11, 2, [-1])
