@@ -150,6 +150,20 @@ def test_embed_dims_and_ragged_sizes(igp, d, n):
         assert err <= TOL, (mode, d, n)
 
 
+@pytest.mark.parametrize("d", [1008, 1024])
+def test_embed_maximum_d(igp, d):
+    """The largest d (include/igp.h: a multiple of 16 up to 1024): 1024 = 8 slices of 128 columns,
+    1008 = 63 slices of 16 (the slice count limit is 64); ragged N, every slice checked."""
+    rng = np.random.default_rng(d)
+    n = 1531
+    edges = rng.integers(0, n, (8 * n, 2)).astype(np.int32)
+    for mode in ["full", "pre_sigmoid"]:
+        z, ref = run_parity(igp, edges, n, d, 4, -1.0, seed=5, mode=mode)
+        err = row_rel_err(z, ref)
+        record(f"max_d{d}_{mode}", err)
+        assert err <= TOL, (mode, d)
+
+
 def test_embed_linear_mode(igp):
     rng = np.random.default_rng(9)
     n = 500
