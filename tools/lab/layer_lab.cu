@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(256, MINB) lab_pre(const int* __restrict__ rp,
       end = __ldg(rp + row + 1);
     }
     uint64_t own[NV];
-    if (PRE >= 3 && valid) {
+    if (PRE == 3 && valid) {
       const uint64_t* op = Y + ((size_t)row * LPR + q) * NV;
       ldg256(op, own);
     }
@@ -530,9 +530,12 @@ __global__ void __launch_bounds__(256, MINB) lab_pre(const int* __restrict__ rp,
       for (int k = 0; k < IPL; ++k) jr[k] = jn[k];
     }
     if (PRE >= 2 && max_nch == 0) load_idx<IPL>(ci, nbeg & ~3, nend, q, jfirst);
-    if (valid) {
+    if (PRE == 4 && valid) {  // gather-only: the raw neighbour sums, for a separate epilogue pass
+#pragma unroll
+      for (int k = 0; k < NV; ++k) O[((size_t)row * LPR + q) * NV + k] = acc[k];
+    } else if (valid) {
       const float si = s[row];
-      if (PRE < 3) {
+      if (PRE != 3) {
         const uint64_t* op = Y + ((size_t)row * LPR + q) * NV;
 #pragma unroll
         for (int k = 0; k < NV; ++k) own[k] = op[k];
@@ -777,6 +780,9 @@ int main(int argc, char** argv) {
   RUN("pre3 B4 occ4", (lab_pre<4, 3, 4>), 0);
   RUN("pre2 B4 occ3", (lab_pre<4, 2, 3>), 0);
   RUN("pre2 B8 occ3", (lab_pre<8, 2, 3>), 0);
+  RUN("gather-only B8 occ2 (sums stored)", (lab_pre<8, 4, 2>), 0);
+  RUN("gather-only B8 occ3 (sums stored)", (lab_pre<8, 4, 3>), 0);
+  RUN("gather-only B4 occ4 (sums stored)", (lab_pre<4, 4, 4>), 0);
   // correctness: pieces vs base (same math, summation order differs)
   {
     int regs;
