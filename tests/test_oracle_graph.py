@@ -97,3 +97,18 @@ def test_corrected_degree_bounds():
     assert np.array_equal(oracle.corrected_degree(deg, 0.0), deg.astype(float))
     for tau in [0.5, 1.0, 5.0, 10.0]:
         assert np.all(oracle.corrected_degree(deg, tau) >= deg)
+
+
+@pytest.mark.parametrize("n,k", [(5, 2), (9, 1), (40, 7), (1000, 32)])
+def test_circulant_generator_matches_its_closed_form(n, k):
+    """synth/circulant.py (the maximum-size GPU test's input) against the oracle's CSR: every row
+    is {i +- 1..k mod n}, every degree 2k."""
+    from synth.circulant import circulant_edges, circulant_row
+    e = circulant_edges(n, k).numpy()
+    assert e.shape == (n * k, 2)
+    rp, ci, m = oracle.build_csr(e, n)
+    assert m == n * k and np.array_equal(np.diff(rp), np.full(n, 2 * k))
+    for i in range(n):
+        assert np.array_equal(ci[rp[i]:rp[i + 1]], circulant_row(n, k, i))
+    with pytest.raises(ValueError):
+        circulant_edges(4, 2)  # 2k >= n would repeat pairs
