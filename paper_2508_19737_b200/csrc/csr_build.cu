@@ -750,13 +750,14 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     // the column arrays are sized by the entries before deduplication, so nothing on the
     // host waits for nnz; vector index loads may read up to kColPad entries past a row
     const size_t cbytes = sizeof(int32_t) * (size_t)(raw + kColPad);
-    igp_status st = cuda_status(alloc_async((void**)&c.row_ptr, sizeof(int32_t) * ((size_t)n + 1), s), "alloc");
+    igp_status st =
+        cuda_status(alloc_async((void**)&c.row_ptr, sizeof(int32_t) * ((size_t)n + 1 + kRpPad), s), "alloc");
     if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.order, sizeof(int32_t) * (size_t)n, s), "alloc");
     if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.meta, 4 * sizeof(int32_t), s), "alloc");
     if (st == IGP_OK) st = cuda_status(alloc_async((void**)&c.col_idx, cbytes, s), "col_idx alloc");
-    // rp_perm padded by 4 entries: 16-byte bulk copies of a row-pointer slice may overrun the end
+    // row-pointer arrays padded by kRpPad entries: 16-byte bulk copies of a slice may overrun the end
     if (st == IGP_OK && reorder)
-        st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 5), s), "alloc");
+        st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 1 + kRpPad), s), "alloc");
     if (st == IGP_OK && reorder) st = cuda_status(alloc_async((void**)&c.col_perm, cbytes, s), "col_perm alloc");
     if (!reorder) c.perm_alias = true;
     cudaEvent_t ev_csr = nullptr, ev_lp = nullptr;  // community order: side-stream fork / join
@@ -796,6 +797,7 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         IGP_STEP(launch_status("count_kernel"));
     }
     IGP_STEP(scan_exclusive(cnt, off, n, s));
+    IGP_STEP(cuda_status(cudaMemsetAsync(c.row_ptr + n + 1, 0, kRpPad * sizeof(int32_t), s), "pad memset"));
     const int rg = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
     if (base) {
         base_copy_kernel<<<rg, 256, 0, s>>>(base->row_ptr, base->col_idx, n, off, tmp);
@@ -885,7 +887,7 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     inverse_perm_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n, inv, c.row_ptr, degp);
     IGP_STEP(launch_status("inverse_perm_kernel"));
     IGP_STEP(scan_exclusive(degp, c.rp_perm, n, s));
-    IGP_STEP(cuda_status(cudaMemsetAsync(c.rp_perm + n + 1, 0, 4 * sizeof(int32_t), s), "pad memset"));
+    IGP_STEP(cuda_status(cudaMemsetAsync(c.rp_perm + n + 1, 0, kRpPad * sizeof(int32_t), s), "pad memset"));
     if (raw > 0) {
         // each relabelled row keeps its canonical neighbour order (ascending original id), so a
         // row's summation order is the same under any permutation (up to where the 128-neighbour

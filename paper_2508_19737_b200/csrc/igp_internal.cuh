@@ -85,6 +85,9 @@ struct CsrDevice {
 // release every array of c in stream order on s
 void free_csr(const CsrDevice& c, cudaStream_t s);
 constexpr int kColPad = 16;
+// row-pointer arrays carry kRpPad entries past [N]: the filter step's bulk copies of a row-pointer
+// slice are rounded up to 16 bytes and may start below / end past the batch's rows
+constexpr int kRpPad = 64;
 // largest CSR entry count (before dedup): int32 offsets with headroom for the kernels' chunk
 // arithmetic (a chunk start + 2 chunks of 16 must not overflow)
 constexpr int64_t kMaxEntries = (int64_t)INT32_MAX - 64;

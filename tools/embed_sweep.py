@@ -13,7 +13,8 @@ cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "headline"]
 widths = [int(w) for w in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["16", "32", "64"])]
 occs = [int(o) for o in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["2"])]
 envs = [kv for kv in (sys.argv[4].split(";") if len(sys.argv) > 4 else [""])]
-edges, _ = generate(cfg)
+from ncu_embed import cached_edges  # noqa: E402
+edges = cached_edges(cfg)
 e = torch.from_numpy(edges).cuda()
 g = igp.build_graph(e, cfg.num_nodes)
 out = torch.empty((cfg.num_nodes, cfg.d), device="cuda")
