@@ -20,6 +20,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "igp_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "birch_oracle.c")]
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 MODE_FULL = 0
@@ -35,11 +36,13 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so (gcc, -O2, OpenMP, no fast-math)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB_PATH) or any(os.path.getmtime(_LIB_PATH) < os.path.getmtime(s)
+                                                      for s in _SRCS):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        # -ffp-contract=off: no implicit fma; birch_oracle.c uses explicit fma() where it means one
         subprocess.check_call(
-            ["gcc", "-O2", "-fPIC", "-shared", "-fopenmp", "-fno-fast-math", "-std=c11",
-             "-Wall", "-o", tmp, _SRC, "-lm"])
+            ["gcc", "-O2", "-fPIC", "-shared", "-fopenmp", "-fno-fast-math", "-ffp-contract=off", "-std=c11",
+             "-Wall", "-o", tmp, *_SRCS, "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -74,6 +77,22 @@ def _load():
     lib.oracle_row_l2.restype = None
     lib.oracle_embed.argtypes = [P, P, i32, i32, i32, f64, f64, f64, f64, P, u64, u64, i32, i32, P]
     lib.oracle_embed.restype = ctypes.c_int
+    lib.oracle_embed_f32.argtypes = [P, P, i32, i32, i32, f64, f64, f64, f64, P, u64, u64, i32, i32, P]
+    lib.oracle_embed_f32.restype = ctypes.c_int
+    lib.oracle_birch_new.argtypes = [i32, f64, i32]
+    lib.oracle_birch_new.restype = P
+    lib.oracle_birch_free.argtypes = [P]
+    lib.oracle_birch_free.restype = None
+    lib.oracle_birch_partial_fit.argtypes = [P, P, i64]
+    lib.oracle_birch_partial_fit.restype = ctypes.c_int
+    lib.oracle_birch_num_clusters.argtypes = [P]
+    lib.oracle_birch_num_clusters.restype = i64
+    lib.oracle_birch_clusters.argtypes = [P, P, P, P, P, P]
+    lib.oracle_birch_clusters.restype = None
+    lib.oracle_birch_shape.argtypes = [P, P, P, P]
+    lib.oracle_birch_shape.restype = None
+    lib.oracle_birch_predict.argtypes = [P, P, i64, i32, P, i64, P]
+    lib.oracle_birch_predict.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -191,8 +210,11 @@ def row_l2(Z) -> np.ndarray:
 
 def embed(row_ptr, col_idx, num_nodes: int, d: int, steps: int, tau: float, seed: int = 0,
           sub: int = 0, theta=THETA, alpha=ALPHA, eps=EPS, Z0=None, mode=MODE_FULL,
-          nthreads: int = 1) -> np.ndarray:
-    """Alg. 1 lines 1-6 in fp64; returns Z~ (or Z^(L) / linear output per ``mode``)."""
+          nthreads: int = 1, fp32_twin: bool = False) -> np.ndarray:
+    """Alg. 1 lines 1-6 in fp64; returns Z~ (or Z^(L) / linear output per ``mode``).
+
+    ``fp32_twin=True`` runs ``oracle_embed_f32`` instead: the same steps with float storage
+    and arithmetic (fp64 column statistics), used only to report the fp32 drift floor."""
     lib = _load()
     rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
     ci = np.ascontiguousarray(col_idx, dtype=np.int32)
@@ -201,8 +223,9 @@ def embed(row_ptr, col_idx, num_nodes: int, d: int, steps: int, tau: float, seed
     if Z0 is not None:
         Z0 = np.ascontiguousarray(Z0, dtype=np.float64).reshape(num_nodes, d)
         z0p = _ptr(Z0)
-    rc = lib.oracle_embed(_ptr(rp), _ptr(ci), num_nodes, d, steps, tau, theta, alpha, eps, z0p,
-                          seed, sub, mode, nthreads, _ptr(out))
+    fn = lib.oracle_embed_f32 if fp32_twin else lib.oracle_embed
+    rc = fn(_ptr(rp), _ptr(ci), num_nodes, d, steps, tau, theta, alpha, eps, z0p, seed, sub, mode, nthreads,
+            _ptr(out))
     if rc != 0:
         raise OracleError(f"oracle_embed rejected its arguments (rc={rc})")
     return out
@@ -211,3 +234,64 @@ def embed(row_ptr, col_idx, num_nodes: int, d: int, steps: int, tau: float, seed
 def input_theta(seed: int, sub: int, num_nodes: int, d: int) -> np.ndarray:
     """Theta = X / sqrt(d), X the Philox/Box-Muller stream (Alg. 1 l.2, reading A1)."""
     return normal(seed, sub, num_nodes * d).reshape(num_nodes, d) / np.sqrt(d)
+
+
+# ---------------------------------------------------------------- BIRCH (Alg. 1 l.7, Alg. 2 l.9-11)
+class Birch:
+    """The oracle's CF tree (oracle/birch_oracle.c): ``partial_fit`` inserts rows in order,
+    ``clusters()`` returns the leaf entries (the K-agnostic clusters) in leaf-chain order,
+    ``predict`` labels rows by their nearest cluster centroid.  fp64 throughout."""
+
+    def __init__(self, d: int, threshold: float = 0.5, branching: int = 50):
+        self._lib = _load()
+        self.d = d
+        self._h = self._lib.oracle_birch_new(d, float(threshold), int(branching))
+        if not self._h:
+            raise OracleError("oracle_birch_new rejected its arguments")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.oracle_birch_free(h)
+            self._h = None
+
+    def partial_fit(self, X):
+        X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, self.d)
+        rc = self._lib.oracle_birch_partial_fit(self._h, _ptr(X), X.shape[0])
+        if rc != 0:
+            raise OracleError(f"oracle_birch_partial_fit failed (rc={rc})")
+        return self
+
+    fit = partial_fit  # a fresh tree: fit == partial_fit on all rows in order
+
+    def clusters(self):
+        """(centroids [K,d], sqn [K], n [K], LS [K,d], SS [K])"""
+        K = int(self._lib.oracle_birch_num_clusters(self._h))
+        cen = np.zeros((K, self.d))
+        ls = np.zeros((K, self.d))
+        sqn, n, ss = np.zeros(K), np.zeros(K), np.zeros(K)
+        self._lib.oracle_birch_clusters(self._h, _ptr(cen), _ptr(sqn), _ptr(n), _ptr(ls), _ptr(ss))
+        return cen, sqn, n, ls, ss
+
+    def shape(self):
+        dep, nodes, pts = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int64(0)
+        self._lib.oracle_birch_shape(self._h, ctypes.byref(dep), ctypes.byref(nodes), ctypes.byref(pts))
+        return dep.value, nodes.value, pts.value
+
+    def predict(self, X):
+        cen, sqn, _, _, _ = self.clusters()
+        return birch_predict(cen, sqn, X)
+
+
+def birch_predict(cen, sqn, X) -> np.ndarray:
+    """label_i = argmin_j sqn_j - 2 c_j . x_i (first minimum), fp64."""
+    lib = _load()
+    cen = np.ascontiguousarray(cen, dtype=np.float64)
+    sqn = np.ascontiguousarray(sqn, dtype=np.float64)
+    K, d = cen.shape
+    X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, d)
+    out = np.zeros(X.shape[0], dtype=np.int32)
+    rc = lib.oracle_birch_predict(_ptr(cen), _ptr(sqn), K, d, _ptr(X), X.shape[0], _ptr(out))
+    if rc != 0:
+        raise OracleError(f"oracle_birch_predict rejected its arguments (rc={rc})")
+    return out

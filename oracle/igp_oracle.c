@@ -339,3 +339,113 @@ int oracle_embed(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int3
     free(P);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* fp32 TWIN of oracle_embed (SURVEY.md §8(c) "fp32 twin").   */
+/* The same Alg. 1 lines 1-6 in the same order, with every stored value and */
+/* every propagate / tanh / sigmoid operation in float (the paper's PyTorch   */
+/* default precision, PAPER.md:426-427 names no other), and the column       */
+/* statistics of ZNorm in double over the float values.  It never validates */
+/* the GPU: it measures the irreducible drift of fp32 storage against the    */
+/* fp64 oracle on each config (the "fp32 floor" reported beside every GPU    */
+/* error), so a GPU miss can be attributed to fp32 itself or to the kernel.  */
+/* ------------------------------------------------------------------------ */
+static void twin_propagate(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int32_t d, const float* s,
+                           const float* Z, float theta, float alpha, int32_t nthreads, float* P) {
+    (void)nthreads;
+#ifdef _OPENMP
+    int nt = nthreads > 0 ? nthreads : 1;
+#pragma omp parallel num_threads(nt)
+#endif
+    {
+        float* nb = (float*)malloc((size_t)d * sizeof(float));
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 256)
+#endif
+        for (int32_t i = 0; i < N; ++i) {
+            float* Pi = P + (int64_t)i * d;
+            const float* Zi = Z + (int64_t)i * d;
+            int32_t beg = row_ptr[i], end = row_ptr[i + 1];
+            for (int32_t c = 0; c < d; ++c) nb[c] = 0.0f;
+            for (int32_t e = beg; e < end; ++e) {
+                int32_t j = col_idx[e];
+                const float* Zj = Z + (int64_t)j * d;
+                for (int32_t c = 0; c < d; ++c) nb[c] += s[j] * Zj[c];
+            }
+            for (int32_t c = 0; c < d; ++c) {
+                float term = (end > beg) ? alpha * s[i] * nb[c] : 0.0f;
+                Pi[c] = theta * Zi[c] + term;
+            }
+        }
+        free(nb);
+    }
+}
+
+/* ZNorm of float columns: mean / population std in double, result rounded to float */
+static void twin_zscore_columns(float* T, int32_t N, int32_t d) {
+    for (int32_t c = 0; c < d; ++c) {
+        double sum = 0.0;
+        for (int32_t i = 0; i < N; ++i) sum += (double)T[(int64_t)i * d + c];
+        double mu = sum / (double)N;
+        double ss = 0.0;
+        for (int32_t i = 0; i < N; ++i) {
+            double x = (double)T[(int64_t)i * d + c] - mu;
+            ss += x * x;
+        }
+        double s = sqrt(ss / (double)N);
+        for (int32_t i = 0; i < N; ++i) {
+            float* x = &T[(int64_t)i * d + c];
+            *x = (s < 1e-8) ? 0.0f : (float)(((double)*x - mu) / s);
+        }
+    }
+}
+
+/* Same arguments as oracle_embed (Z0 in double, rounded to float on entry); out in double
+ * holds the float results. */
+int oracle_embed_f32(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int32_t d, int32_t L,
+                     double tau, double theta, double alpha, double eps, const double* Z0,
+                     uint64_t seed, uint64_t sub, int32_t mode, int32_t nthreads, double* out) {
+    if (N <= 0 || d <= 0 || L < 0 || (Z0 == NULL && d % 4 != 0)) return ORACLE_ERR_INPUT;
+    int64_t nd = (int64_t)N * d;
+    float* s = (float*)malloc((size_t)N * sizeof(float));
+    float* Z = (float*)malloc((size_t)nd * sizeof(float));
+    float* P = (float*)malloc((size_t)nd * sizeof(float));
+    double* X = Z0 ? NULL : (double*)malloc((size_t)nd * sizeof(double));
+    if (!s || !Z || !P || (!Z0 && !X)) {
+        free(s);
+        free(Z);
+        free(P);
+        free(X);
+        return ORACLE_ERR_INPUT;
+    }
+    /* line 1: D_tau by Eq. (1) (the same double formula), s = D^-1/2 rounded to float */
+    for (int32_t i = 0; i < N; ++i)
+        s[i] = (float)(1.0 / sqrt(oracle_corrected_degree(row_ptr[i + 1] - row_ptr[i], tau, eps)));
+    /* lines 2-3: the same Philox / Box-Muller draws, Theta = X / sqrt(d) rounded to float */
+    if (Z0) {
+        for (int64_t k = 0; k < nd; ++k) Z[k] = (float)Z0[k];
+    } else {
+        oracle_normal(seed, sub, nd, X);
+        double sq = sqrt((double)d);
+        for (int64_t k = 0; k < nd; ++k) Z[k] = (float)(X[k] / sq);
+        free(X);
+    }
+    /* lines 4-5 */
+    for (int32_t l = 1; l <= L; ++l) {
+        twin_propagate(row_ptr, col_idx, N, d, s, Z, (float)theta, (float)alpha, nthreads, P);
+        if (mode == ORACLE_MODE_LINEAR) {
+            memcpy(Z, P, (size_t)nd * sizeof(float));
+            continue;
+        }
+        for (int64_t k = 0; k < nd; ++k) P[k] = tanhf(P[k]);
+        twin_zscore_columns(P, N, d);
+        memcpy(Z, P, (size_t)nd * sizeof(float));
+    }
+    /* line 6 */
+    for (int64_t k = 0; k < nd; ++k)
+        out[k] = (mode == ORACLE_MODE_FULL) ? (double)(1.0f / (1.0f + expf(-Z[k]))) : (double)Z[k];
+    free(s);
+    free(Z);
+    free(P);
+    return 0;
+}

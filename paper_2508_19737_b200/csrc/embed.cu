@@ -37,7 +37,6 @@
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
-#include <cstring>
 
 #include "igp_internal.cuh"
 #include "philox.cuh"
@@ -502,398 +501,6 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
     }
 }
 
-// ---------------------------------------------------------------------------------------------
-// layer_ws_kernel: the filter step with TMA-staged warp batches (the default since round 2).
-//
-// Same arithmetic as layer_kernel (Eq. (3) with the deferred z-score, tanh, exact statistics),
-// different data movement.  Each warp owns a sequence of row batches (G = 32 / LPR consecutive
-// rows of the relabelled CSR; batch b = warp, warp + all warps, ...).  While it gathers batch b,
-// one lane has already queued batch b+1's inputs on the copy engine with one mbarrier:
-//   - the row-pointer slice, the batch's neighbour indices (one contiguous CSR range),
-//   - the batch's own y rows and node parameters {s, r} (+ {c_hi, c_lo} from step 2 on),
-// as 1-D bulk copies (cp.async.bulk, no registers, no L1 pollution).  The gather lanes then read
-// indices from shared memory (no index shuffles, no index registers held across batches, no
-// 16-aligned chunk masking: a row costs ceil(deg / 8) batches of 8 gathers), and the epilogue reads
-// its own row from shared memory (no L2 round trip between the last gather and the store).  What
-// stays in registers during the gather phase is the 8-deep 256-bit landing buffer, the packed
-// accumulators and a few scalars, so more warps per SM keep 8 gathers each in flight.
-// A batch whose index range exceeds the per-warp buffer (hub rows) reads its indices from global.
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WS_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WS_WAIT;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// 1-D bulk copy global -> shared, completion counted on `bar` (bytes and addresses 16-B multiples)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                              uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ int lds_s32(uint32_t addr) {
-    int v;
-    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-
-// Per-warp shared-memory layout of layer_ws_kernel<W>.
-//  - ring: the neighbour indices of the batches in flight, as a ring of RC ints; each batch's CSR
-//    range (one contiguous copy, split in two where it wraps) is placed right behind the previous
-//    one, so a batch may use up to RC minus its predecessor's share (hub batches beyond that read
-//    their indices from global memory);
-//  - two batch buffers (row-pointer slice, {s, r}, {c_hi, c_lo}, own y rows, ring offset);
-//  - one scratch area: the fp64 partial sums of rows longer than 128 neighbours during the gather
-//    phase, then the t tile for the column statistics (disjoint in time).
-template <int W>
-struct WsShape {
-    static constexpr int LPR = W / 8;        // lanes per row (8 columns each)
-    static constexpr int G = 32 / LPR;       // rows per warp batch
-    static constexpr int RC = 256 * G < 2048 ? 256 * G : 2048;  // index ring (ints, power of 2)
-    static constexpr int RPC = ((G + 8) + 3) & ~3;              // row-pointer slice capacity (ints)
-    static constexpr int TS = W + 4;         // t tile row stride (floats): conflict-free staging
-};
-
-template <int W>
-struct __align__(16) WsBuf {
-    using S = WsShape<W>;
-    int32_t rps[S::RPC];      // row pointers [r0 & ~3, ...]
-    float2 sr[S::G];          // {s, r} of the batch's rows
-    float2 cc[S::G];          // {c_hi, c_lo}
-    float ys[S::G * W];       // own rows of y_in
-    int32_t meta[4];          // [0] ring offset of index rp[r0] & ~3, or -1: indices in global memory
-};
-
-template <int W>
-struct __align__(16) WsWarp {
-    using S = WsShape<W>;
-    int32_t ring[S::RC];
-    WsBuf<W> buf[2];
-    union {
-        double fold[S::G * W];
-        float tile[S::G * S::TS];
-    } scratch;
-};
-
-template <int W>
-constexpr size_t ws_warp_smem() {
-    return sizeof(WsWarp<W>);
-}
-
-// lane 0: queue batch b's inputs into buffer D (signalled on bar); elo/ehi = rp[r0], rp[r0 + Gv].
-// rh / used: the ring head and the ring share of the batch currently being gathered.
-template <int W>
-__device__ __forceinline__ void ws_issue(const LayerArgs& p, int64_t b, WsWarp<W>& M, WsBuf<W>& D, uint64_t* bar,
-                                         int32_t elo, int32_t ehi, int32_t& rh, int32_t& used, uint64_t pol_idx) {
-    using S = WsShape<W>;
-    const int64_t r0 = b * S::G;
-    const int Gv = (int)((int64_t)p.n - r0 < S::G ? (int64_t)p.n - r0 : S::G);
-    const int64_t rs = r0 & ~(int64_t)3;
-    const uint32_t rcnt = (uint32_t)((r0 + Gv + 1 - rs + 3) & ~(int64_t)3);
-    const uint32_t nb = (uint32_t)((Gv * 8 + 15) & ~15);
-    const int32_t ea = elo & ~3;
-    const int32_t icnt = (ehi - ea + 3) & ~3;
-    const bool use_ring = icnt > 0 && icnt + used <= S::RC;
-    uint32_t bytes = rcnt * 4 + nb + (uint32_t)Gv * W * 4;
-    if (p.sums_in) bytes += nb;
-    if (use_ring) bytes += (uint32_t)icnt * 4;
-    D.meta[0] = icnt == 0 ? 0 : (use_ring ? rh : -1);  // published by the arrive below (release)
-    // the buffers are only READ through the generic proxy, and every lane's reads completed
-    // before the __syncwarp that precedes this call: no proxy fence is needed
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s(D.rps, p.rp + rs, rcnt * 4, bar);
-    bulk_g2s(D.sr, p.sr + r0, nb, bar);
-    if (p.sums_in) bulk_g2s(D.cc, p.cc + r0, nb, bar);
-    bulk_g2s(D.ys, reinterpret_cast<const float*>(p.yin) + r0 * W, (uint32_t)Gv * W * 4, bar);
-    if (use_ring) {
-        const int32_t first = S::RC - rh < icnt ? S::RC - rh : icnt;
-        bulk_g2s_hint(M.ring + rh, p.ci + ea, (uint32_t)first * 4, bar, pol_idx);
-        if (first < icnt) bulk_g2s_hint(M.ring, p.ci + ea + first, (uint32_t)(icnt - first) * 4, bar, pol_idx);
-        rh = (rh + icnt) & (S::RC - 1);
-        used = icnt;
-    } else {
-        used = 0;
-    }
-}
-
-// gather phase of one warp batch: each lane group sums its row's neighbour rows (8 columns per lane)
-// in batches of 8 256-bit gathers; fp32 partials span at most 128 neighbours, then fold into fp64
-// (af, as layer_kernel).  Indices from the ring: index of edge beg + i at ring[(pos0 + i) & mask].
-template <int W>
-__device__ __forceinline__ void ws_gather_smem(uint32_t ring, int32_t pos0, int32_t beg, int32_t end, int maxb,
-                                               const uint64_t* __restrict__ yin, int q, uint64_t (&acc)[4],
-                                               double* af, bool& folded) {
-    constexpr int LPR = W / 8;
-    constexpr int32_t mask = WsShape<W>::RC - 1;
-    int nc = 0;
-    for (int c = 0; c < maxb; ++c) {
-        const int32_t e = beg + 8 * c;
-        uint64_t v[8][4];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            v[t][0] = v[t][1] = v[t][2] = v[t][3] = 0ull;
-            if (e + t < end) {
-                const int j = lds_s32(ring + 4u * (uint32_t)((pos0 + 8 * c + t) & mask));
-                ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-#pragma unroll
-            for (int h = 0; h < 4; ++h) acc[h] = fadd2(acc[h], v[t][h]);
-        if (++nc == 2 * kFoldChunks && e + 8 < end) {
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const float2 f = unpack2(acc[h]);
-                af[2 * h] += (double)f.x;
-                af[2 * h + 1] += (double)f.y;
-                acc[h] = 0ull;
-            }
-            nc = 0;
-            folded = true;
-        }
-    }
-}
-// hub batches (index range larger than the ring's free share): indices straight from global memory,
-// the whole sum folded into the fp64 partials af (out of line, so the hot loop keeps its registers)
-template <int W>
-__device__ __noinline__ void ws_gather_global(const int32_t* __restrict__ ci, int32_t beg, int32_t end, int maxb,
-                                              const uint64_t* __restrict__ yin, int q, double* af) {
-    constexpr int LPR = W / 8;
-    const uint64_t pol = evict_first_policy(1.0f);
-    uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-    int nc = 0;
-    for (int c = 0; c < maxb; ++c) {
-        const int32_t e = beg + 8 * c;
-        uint64_t v[8][4];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            v[t][0] = v[t][1] = v[t][2] = v[t][3] = 0ull;
-            if (e + t < end) ldg256(yin + ((size_t)ld_idx1(ci + e + t, pol) * LPR + q) * 4, v[t]);
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-#pragma unroll
-            for (int h = 0; h < 4; ++h) acc[h] = fadd2(acc[h], v[t][h]);
-        if (++nc == 2 * kFoldChunks || c + 1 == maxb) {
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const float2 f = unpack2(acc[h]);
-                af[2 * h] += (double)f.x;
-                af[2 * h + 1] += (double)f.y;
-                acc[h] = 0ull;
-            }
-            nc = 0;
-        }
-    }
-}
-
-template <int W, int NW, int MB>
-__global__ void __launch_bounds__(NW * 32, MB) layer_ws_kernel(const LayerArgs p) {
-    using S = WsShape<W>;
-    constexpr int LPR = S::LPR, G = S::G, TS = S::TS;
-    constexpr int OC = W >= 32 ? W / 32 : 1;  // statistics columns owned per lane
-    constexpr int OR = W >= 32 ? G : G / 2;   // ... each over OR rows of the warp tile
-    constexpr int kThreads = NW * 32;
-    __shared__ double2 st[W + W / 8];  // (mu, 1/sigma) of the previous step, column c at c + c/8
-    __shared__ uint64_t bars[NW][2];
-    extern __shared__ __align__(128) unsigned char ws_smem[];
-    WsWarp<W>* warps = reinterpret_cast<WsWarp<W>*>(ws_smem);
-
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int q = lane % LPR, g = lane / LPR;
-    WsWarp<W>& M = warps[warp];
-    double* af = M.scratch.fold + g * W + 8 * q;
-    float* tile = M.scratch.tile;
-    if (lane == 0) {
-        mbar_init(&bars[warp][0], 1);
-        mbar_init(&bars[warp][1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    const uint64_t* yin = reinterpret_cast<const uint64_t*>(p.yin);  // row j, lane q: yin + (j*LPR + q)*4
-    uint64_t* yout = reinterpret_cast<uint64_t*>(p.yout);
-    const uint64_t pol_idx = evict_first_policy(p.idx_ef);
-    const int oc0 = W >= 32 ? lane * OC : lane / 2;  // owned statistics columns / rows
-    const int or0 = W >= 32 ? 0 : (lane & 1) * OR;
-    double s1[OC], s2[OC];
-#pragma unroll
-    for (int k = 0; k < OC; ++k) s1[k] = s2[k] = 0.0;
-
-    const int64_t nbatch = ((int64_t)p.n + G - 1) / G;
-    const int64_t TW = (int64_t)gridDim.x * NW;
-    const int64_t gw = (int64_t)blockIdx.x * NW + warp;
-    // lane 0 keeps (rp[r0], rp[r0 + Gv]) of the next batch to queue (static CSR: read before the wait)
-    // and the index ring's head / the ring share of the batch being gathered
-    int32_t nlo = 0, nhi = 0, rh = 0, used = 0;
-    auto load_bounds = [&](int64_t b) {
-        if (b < nbatch) {
-            const int64_t r0 = b * G;
-            const int64_t r1 = r0 + G < (int64_t)p.n ? r0 + G : (int64_t)p.n;
-            nlo = __ldg(p.rp + r0);
-            nhi = __ldg(p.rp + r1);
-        }
-    };
-    if (lane == 0) load_bounds(gw);
-    // the previous step's output (yin) and column sums (sums_in) are read only after this point
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    for (int c = threadIdx.x; c < W; c += kThreads) {
-        double m = 0.0, is = 1.0;
-        if (p.sums_in) column_stats(p.sums_in, c, W, p.n, m, is);
-        st[c + c / 8] = make_double2(m, is);
-    }
-    __syncthreads();  // st and the barrier initialisation
-    if (lane == 0 && gw < nbatch) {
-        ws_issue<W>(p, gw, M, M.buf[0], &bars[warp][0], nlo, nhi, rh, used, pol_idx);
-        load_bounds(gw + TW);
-    }
-    const uint32_t ring = smem_u32(M.ring);
-    int k = 0;
-    for (int64_t b = gw; b < nbatch; b += TW, ++k) {
-        WsBuf<W>& B = M.buf[k & 1];
-        if (lane == 0 && b + TW < nbatch) {  // queue the next batch, then fetch the bounds of the one after
-            ws_issue<W>(p, b + TW, M, M.buf[(k + 1) & 1], &bars[warp][(k + 1) & 1], nlo, nhi, rh, used, pol_idx);
-            load_bounds(b + 2 * TW);
-        }
-        mbar_wait(&bars[warp][k & 1], (uint32_t)((k >> 1) & 1));
-        const int64_t r0 = b * G;
-        const int Gv = (int)((int64_t)p.n - r0 < G ? (int64_t)p.n - r0 : G);
-        const int ro = (int)(r0 & 3);
-        const bool valid = g < Gv;
-        const int64_t row = r0 + g;
-        const int32_t beg = valid ? B.rps[ro + g] : 0;
-        const int32_t end = valid ? B.rps[ro + g + 1] : 0;
-        const int32_t ea = B.rps[ro] & ~3;
-        const int32_t off = B.meta[0];
-        const int nb = end > beg ? (end - beg + 7) >> 3 : 0;
-        const int maxb = __reduce_max_sync(kFull, nb);
-        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-        bool folded = false;
-#pragma unroll
-        for (int h = 0; h < 8; ++h) af[h] = 0.0;
-        if (off >= 0) {
-            ws_gather_smem<W>(ring, off + (beg - ea), beg, end, maxb, yin, q, acc, af, folded);
-        } else {  // hub batches: indices straight from global memory (out of line)
-            ws_gather_global<W>(p.ci, beg, end, maxb, yin, q, af);
-            folded = true;
-        }
-        float t8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        const float* yrow = B.ys + g * W + 8 * q;
-        if (valid) {
-            double ad[8];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const float2 f = unpack2(acc[h]);
-                ad[2 * h] = (double)f.x;
-                ad[2 * h + 1] = (double)f.y;
-            }
-            if (folded) {
-#pragma unroll
-                for (int h = 0; h < 8; ++h) ad[h] += af[h];
-            }
-            const float2 sr2 = B.sr[g];
-            const double si = (double)sr2.x;
-            const double cc = p.sums_in ? (double)B.cc[g].x + (double)B.cc[g].y : 0.0;
-            const float4 y0 = *reinterpret_cast<const float4*>(yrow);
-            const float4 y1 = *reinterpret_cast<const float4*>(yrow + 4);
-            const float yv[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
-            uint64_t o[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                float yy[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const double2 m = st[9 * q + 2 * h + u];
-                    const float tself = yv[2 * h + u] * sr2.y;  // t_i = y_i / s_i
-                    const double P =
-                        ((double)p.theta * (double)tself + (double)p.alpha * si * ad[2 * h + u] - m.x * cc) * m.y;
-                    const float t = p.linear ? (float)P : tanhf((float)P);
-                    t8[2 * h + u] = t;
-                    yy[u] = sr2.x * t;
-                }
-                o[h] = pack2(yy[0], yy[1]);
-            }
-            stg256(yout + ((size_t)row * LPR + q) * 4, o, evict_first_policy(p.st_ef));
-        }
-        __syncwarp();  // the fold partials are dead: the scratch becomes the t tile
-        if (!p.linear) {
-            // stage the warp's G x W tile of t (invalid rows 0); each lane then folds its owned
-            // columns (exact grid-rounded fp64 sums).  Lanes with (q & 4) store their upper half
-            // first, so each 8-lane store phase covers all 32 banks once (rows TS = W + 4 apart).
-            const float4 lo4 = make_float4(t8[0], t8[1], t8[2], t8[3]), hi4 = make_float4(t8[4], t8[5], t8[6], t8[7]);
-            const bool swap = (q & 4) != 0;
-            *reinterpret_cast<float4*>(tile + g * TS + 8 * q + (swap ? 4 : 0)) = swap ? hi4 : lo4;
-            *reinterpret_cast<float4*>(tile + g * TS + 8 * q + (swap ? 0 : 4)) = swap ? lo4 : hi4;
-            __syncwarp();
-#pragma unroll
-            for (int r = 0; r < OR; ++r) {
-                float x[OC];
-                const float* src = tile + (or0 + r) * TS + oc0;
-                if constexpr (OC == 4) {
-                    const float4 vv = *reinterpret_cast<const float4*>(src);
-                    x[0] = vv.x, x[1] = vv.y, x[2] = vv.z, x[3] = vv.w;
-                } else if constexpr (OC == 2) {
-                    const float2 vv = *reinterpret_cast<const float2*>(src);
-                    x[0] = vv.x, x[1] = vv.y;
-                } else {
-                    x[0] = *src;
-                }
-#pragma unroll
-                for (int kk = 0; kk < OC; ++kk) {
-                    const double xd = (double)x[kk];
-                    s1[kk] += grid_round(xd, p.grid_c);
-                    s2[kk] += grid_round(xd * xd, p.grid_c);
-                }
-            }
-        }
-        __syncwarp();  // every lane is done with this buffer and the scratch before they are reused
-    }
-    if (p.linear) return;
-    if (W < 32) {
-#pragma unroll
-        for (int kk = 0; kk < OC; ++kk) {
-            s1[kk] += __shfl_xor_sync(kFull, s1[kk], 1);
-            s2[kk] += __shfl_xor_sync(kFull, s2[kk], 1);
-        }
-    }
-    __syncthreads();  // the warps' scratch areas hold the per-warp reduction [2W] doubles
-    double* red = warps[warp].scratch.fold;
-    if (W >= 32 || (lane & 1) == 0) {
-#pragma unroll
-        for (int kk = 0; kk < OC; ++kk) {
-            red[oc0 + kk] = s1[kk];
-            red[W + oc0 + kk] = s2[kk];
-        }
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < 2 * W; t += kThreads) {
-        double v = 0.0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) v += warps[w].scratch.fold[t];
-        atomicAdd(p.sums_out + t, v);
-    }
-}
-
 // Z~ = sigmoid((t - mu)/sigma) of a slice into columns [col0, col0 + W) of out [N][d]
 // (relabelled row i is written to the row of its original id order[i])
 template <int W>
@@ -1019,80 +626,14 @@ int choose_width(int d, int32_t n, int64_t nnz) {
     return best;
 }
 
-// launch shape of layer_ws_kernel<W>: warps per block x blocks per SM, persistent grid of
-// (SMs x resident blocks) capped by the number of row batches.  IGP_WS_SHAPE=<warps>x<blocks>
-// (development knob) picks one of the instantiated shapes.
-struct WsLaunch {
-    void (*fn)(LayerArgs) = nullptr;
-    int threads = 0, grid = 0;
-    size_t smem = 0;
-};
-template <int W, int NW, int MB>
-WsLaunch ws_shape(int32_t n, const DeviceInfo& di) {
-    WsLaunch w;
-    w.fn = layer_ws_kernel<W, NW, MB>;
-    w.threads = NW * 32;
-    w.smem = NW * ws_warp_smem<W>();
-    // per device: the smem attribute is set (idempotently) before the occupancy is published
-    static std::atomic<int> occ_cache[64];
-    int occ = occ_cache[di.device & 63].load(std::memory_order_acquire);
-    if (occ == 0) {
-        int o = 0;
-        if (cudaFuncSetAttribute(w.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w.smem) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, w.fn, w.threads, w.smem) != cudaSuccess)
-            o = 0;
-        occ = o > 0 ? o : -1;
-        occ_cache[di.device & 63].store(occ, std::memory_order_release);
-    }
-    if (occ < 0) {
-        w.fn = nullptr;
-        return w;
-    }
-    const int64_t batches = ((int64_t)n + WsShape<W>::G - 1) / WsShape<W>::G;
-    const int64_t want = (batches + NW - 1) / NW;
-    const int64_t cap = (int64_t)di.num_sms * occ;
-    w.grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
-    return w;
-}
-template <int W>
-WsLaunch ws_launch(int32_t n, const DeviceInfo& di) {
-    const char* e = getenv("IGP_WS_SHAPE");
-    const int nw = e ? atoi(e) : 0;
-    const char* x = e ? strchr(e, 'x') : nullptr;
-    const int mb = x ? atoi(x + 1) : 0;
-    // small graphs: 2-warp blocks, so the batches spread over every SM
-    const int64_t batches = ((int64_t)n + WsShape<W>::G - 1) / WsShape<W>::G;
-    if (nw == 0 && batches < (int64_t)di.num_sms * 20) return ws_shape<W, 2, 8>(n, di);
-    if (nw == 16 && mb == 1) return ws_shape<W, 16, 1>(n, di);
-    if (nw == 4 && mb == 4) return ws_shape<W, 4, 4>(n, di);
-    if (nw == 6 && mb == 2) return ws_shape<W, 6, 2>(n, di);
-    if (nw == 2 && mb == 8) return ws_shape<W, 2, 8>(n, di);
-    return ws_shape<W, 8, 2>(n, di);
-}
-
 template <int W, int MB>
 igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s,
                        const DeviceInfo& di, HostCopy* hc) {
     const int32_t n = g.n;
     const int L = o.steps, d = o.d, nslices = d / W;
-    // filter-step kernel: the TMA-staged warp-batch kernel (default) or the round-1 register kernel
-    // (IGP_LAYER_KERNEL=classic, kept for A/B measurements; results agree within fp32 summation order)
-    const char* kenv = getenv("IGP_LAYER_KERNEL");
-    const bool classic = !(kenv && kenv[0] == 'w');  // measured: the staged kernel is slower
-    // classic: graphs too small to give every SM a block of 8 warps run 2-warp blocks (4x the blocks)
+    // graphs too small to give every SM a block of 8 warps run 2-warp blocks (4x the blocks)
     const bool small = (n + 8 * (256 / W) - 1) / (8 * (256 / W)) < di.num_sms;
-    WsLaunch wl{};
-    int grid = 0;
-    if (classic) {
-        grid = small ? layer_grid<W, MB, 2>(n, di) : layer_grid<W, MB, 8>(n, di);
-    } else {
-        wl = ws_launch<W>(n, di);
-        if (!wl.fn) {
-            set_error("layer_ws_kernel: no launchable shape");
-            return IGP_ERR_CUDA;
-        }
-        grid = wl.grid;
-    }
+    const int grid = small ? layer_grid<W, MB, 2>(n, di) : layer_grid<W, MB, 8>(n, di);
     const size_t nw = (size_t)n * W;
     // workspace: sr | cc (N + 2 float2 each) | y0 | y1 (N x W each) | sums [slices][L+1][2W]
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -1184,22 +725,16 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 a.st_ef = st_ef;
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(grid);
-                if (classic) {
-                    cfg.blockDim = dim3(small ? 64 : 256);
-                    cfg.dynamicSmemBytes = small ? layer_smem<W, 2>() : layer_smem<W, 8>();
-                } else {
-                    cfg.blockDim = dim3(wl.threads);
-                    cfg.dynamicSmemBytes = wl.smem;
-                }
+                cfg.blockDim = dim3(small ? 64 : 256);
+                cfg.dynamicSmemBytes = small ? layer_smem<W, 2>() : layer_smem<W, 8>();
                 cfg.stream = s;
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
                 attr[0].val.programmaticStreamSerializationAllowed = 1;
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
-                const cudaError_t le = !classic ? cudaLaunchKernelEx(&cfg, wl.fn, a)
-                                       : small  ? cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 2>, a)
-                                                : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 8>, a);
+                const cudaError_t le = small ? cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 2>, a)
+                                             : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 8>, a);
                 if ((rc = cuda_status(le, "layer_kernel launch")) != IGP_OK) break;
                 if ((rc = launch_status("layer_kernel")) != IGP_OK) break;
             }

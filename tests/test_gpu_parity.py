@@ -108,19 +108,26 @@ def test_philox_normal_within_one_ulp(igp):
 
 
 # ------------------------------------------------------------------ embeddings
-def run_parity(igp, edges, n, d, L, tau, seed=0, mode="full", sub=0, **kw):
+def run_parity(igp, edges, n, d, L, tau, seed=0, mode="full", sub=0, floor=None, **kw):
+    """GPU embed vs the fp64 oracle on the same seeded input.  With floor=<name>, the oracle's
+    fp32 twin (same steps in float) is run too and its drift from the fp64
+    oracle is recorded as <name>_fp32_floor beside the GPU error (the irreducible fp32 part)."""
     g = gpu_graph(igp, edges, n)
     z = igp.embed(g, tau, d, L, seed, mode=mode, subsequence=sub, **kw).cpu().numpy()
     rp, ci, _ = oracle.build_csr(edges, n)
     omode = {"full": oracle.MODE_FULL, "pre_sigmoid": oracle.MODE_PRE_SIGMOID, "linear": oracle.MODE_LINEAR}[mode]
     ref = oracle.embed(rp, ci, n, d, L, tau, seed=seed, sub=sub, mode=omode, nthreads=NTHREADS, **kw)
+    if floor is not None:
+        twin = oracle.embed(rp, ci, n, d, L, tau, seed=seed, sub=sub, mode=omode, nthreads=NTHREADS,
+                            fp32_twin=True, **kw)
+        record(f"{floor}_fp32_floor", row_rel_err(twin, ref))
     return z, ref
 
 
 def test_embed_tiny_config(igp):
     c = CONFIGS["tiny"]
     edges, _ = generate(c)
-    z, ref = run_parity(igp, edges, c.num_nodes, c.d, c.steps, c.tau)
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, c.steps, c.tau, floor="tiny")
     err = row_rel_err(z, ref)
     record("tiny", err)
     assert err <= TOL
@@ -132,7 +139,7 @@ def test_embed_tiny_config(igp):
 def test_embed_medium_config(igp, tau, seed):
     c = CONFIGS["medium"]
     edges, _ = generate(c, seed=seed)
-    z, ref = run_parity(igp, edges, c.num_nodes, c.d, c.steps, tau, seed=seed)
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, c.steps, tau, seed=seed, floor=f"medium_tau{tau}_seed{seed}")
     err = row_rel_err(z, ref)
     record(f"medium_tau{tau}_seed{seed}", err)
     assert err <= TOL
@@ -254,7 +261,7 @@ def test_headline_parity_full_steps(igp, headline):
     bench.py, element by element against the fp64 oracle (IGP_QUICK=1: L = 3)."""
     c, edges = headline
     L = 3 if QUICK else c.steps
-    z, ref = run_parity(igp, edges, c.num_nodes, c.d, L, c.tau)
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, L, c.tau, floor=f"headline_L{L}")
     err = row_rel_err(z, ref)
     record(f"headline_L{L}", err)
     assert err <= TOL
@@ -517,7 +524,7 @@ def test_paper_settings_full_parity(igp, cfg):
     from synth.dcsbm import PAPER_CONFIGS
     c = PAPER_CONFIGS[cfg]
     edges, _ = generate(c)
-    z, ref = run_parity(igp, edges, c.num_nodes, c.d, c.steps, c.tau)
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, c.steps, c.tau, floor=cfg)
     err = row_rel_err(z, ref)
     record(cfg, err)
     assert err <= TOL
@@ -552,8 +559,11 @@ def test_paper_settings_chaotic_tau_layerwise(igp, cfg):
             zl = igp.embed(g, c.tau, c.d, 1, 0, mode=mode, z0=torch.from_numpy(zs).cuda()).cpu().numpy()
             ref = oracle.embed(rp, ci, c.num_nodes, c.d, 1, c.tau, Z0=zs.astype(np.float64), mode=om,
                                nthreads=NTHREADS)
+            twin = oracle.embed(rp, ci, c.num_nodes, c.d, 1, c.tau, Z0=zs.astype(np.float64), mode=om,
+                                nthreads=NTHREADS, fp32_twin=True)
             err = row_rel_err(zl, ref)
             record(f"{cfg}_one_layer_from_{kind}_state_{mode}", err)
+            record(f"{cfg}_one_layer_from_{kind}_state_{mode}_fp32_floor", row_rel_err(twin, ref))
             assert err <= LAYER_TOL_CHAOTIC, (kind, mode)
     za = igp.embed(g, c.tau, c.d, c.steps, 0)
     zb = igp.embed(g, c.tau, c.d, c.steps, 0)

@@ -136,3 +136,53 @@ def test_row_l2_unit_norm_and_direction():
     assert np.allclose(out * np.linalg.norm(Z, axis=1, keepdims=True), Z, rtol=1e-14, atol=0)
     # idempotent
     assert np.allclose(oracle.row_l2(out), out, atol=1e-15)
+
+
+# ---------------------------------------------------------------- fp32 twin
+def _matching(n):
+    """Perfect matching (2k, 2k+1): every degree 1, so D_tau = 1 and s = 1 exactly at tau = 0."""
+    edges = np.array([[2 * k, 2 * k + 1] for k in range(n // 2)], dtype=np.int32)
+    rp, ci, _ = oracle.build_csr(edges, n)
+    return rp, ci
+
+
+def test_fp32_twin_exact_on_dyadic_linear_case():
+    """Closed form: on a perfect matching at tau = 0 (s = 1), theta = 0.5, alpha = 1 and integer
+    Z0, every LINEAR-mode value P_i = Z_i / 2 + Z_partner is exactly representable in float, so
+    the twin equals the fp64 oracle bit for bit and equals the closed form."""
+    n, d, L = 40, 8, 3
+    rp, ci = _matching(n)
+    rng = np.random.default_rng(2)
+    Z0 = rng.integers(-8, 9, size=(n, d)).astype(np.float64)
+    kw = dict(theta=0.5, alpha=1.0, Z0=Z0, mode=oracle.MODE_LINEAR)
+    a = oracle.embed(rp, ci, n, d, L, 0.0, **kw)
+    b = oracle.embed(rp, ci, n, d, L, 0.0, fp32_twin=True, **kw)
+    Z = Z0.copy()
+    partner = np.arange(n) ^ 1
+    for _ in range(L):
+        Z = 0.5 * Z + Z[partner]
+    assert np.array_equal(a, Z) and np.array_equal(b, Z)
+
+
+def test_fp32_twin_is_float_and_within_fp32_bound():
+    """The twin really rounds to float (it differs from fp64 on a generic graph) and stays within
+    the fp32 drift bound the SURVEY probe measured for such graphs (<= 1e-5 row-relative)."""
+    n, d, L = 300, 16, 8
+    _, rp, ci = _graph(7, n, 0.04)
+    a = oracle.embed(rp, ci, n, d, L, -1.0, seed=3)
+    b = oracle.embed(rp, ci, n, d, L, -1.0, seed=3, fp32_twin=True)
+    err = np.max(np.abs(a - b) / np.linalg.norm(a, axis=1, keepdims=True))
+    assert 1e-9 < err < 1e-5
+    assert np.all(b.astype(np.float32).astype(np.float64) == b)  # float values
+
+
+def test_fp32_twin_znorm_golden():
+    """M = 0, L = 1 from Z0 = tanh^-1 of [1,2,3]/4 scaled back by theta: one ZNorm of the column
+    [t1, t2, t3] = [0.25, 0.5, 0.75] gives [-1.2247, 0, 1.2247] (SPEC.md:197), in float."""
+    n, d = 3, 4
+    rp = np.zeros(n + 1, dtype=np.int32)
+    ci = np.zeros(0, dtype=np.int32)
+    t = np.array([0.25, 0.5, 0.75])
+    Z0 = np.repeat((np.arctanh(t) / 0.1)[:, None], d, axis=1)
+    out = oracle.embed(rp, ci, n, d, 1, -1.0, Z0=Z0, mode=oracle.MODE_PRE_SIGMOID, fp32_twin=True)
+    np.testing.assert_allclose(out[:, 0], [-np.sqrt(1.5), 0.0, np.sqrt(1.5)], atol=2e-6)
