@@ -20,13 +20,22 @@ cpu_baseline = the fp64 oracle (oracle/, test infrastructure) on a bounded sampl
 --impl reference times the oracle itself as the reference arm (rank 0 only).
 Multi-GPU: replicas only: each rank embeds its own graph (seed =
 rank), no data-path collective; NCCL is used only for the barrier and the
-max-over-ranks timing reduction.
+max-over-ranks timing reduction.  `--gpus N` without a torchrun environment
+re-launches itself under torch.distributed.run with N processes.
+
+--config streaming: one step = the 10 cumulative stages of BASELINE.json config 4
+(stage 0 build, stages 1-9 igp_graph_add_edges merges, each followed by a re-embed
+with Philox subsequence t, Alg. 2 l.1-7); per-stage merge / embed ms are reported.
+After the timed region the downstream BIRCH (Alg. 1 l.7) is timed once on the step's
+embedding and reported beside the FFP ("birch"), with the oracle's BIRCH time.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -37,7 +46,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synth.dcsbm import ALL_CONFIGS as CONFIGS, generate  # noqa: E402
+from synth.dcsbm import ALL_CONFIGS as CONFIGS, generate, stream_batches  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 
@@ -132,27 +141,53 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+TRAFFIC_JSON = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+KERNEL_SRC = os.path.join(ROOT, "paper_2508_19737_b200", "csrc", "embed.cu")
+
+
+def kernel_source_sha():
+    """sha256 of the filter-step kernel's source (the ncu traffic numbers are tied to it)."""
+    with open(KERNEL_SRC, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
+def load_traffic_entry(config_name):
+    try:
+        with open(TRAFFIC_JSON) as f:
+            return json.load(f).get(config_name) or {}
+    except Exception:
+        return {}
+
+
 def load_gather_ceiling(config_name):
     """Measured random-gather ceiling (GB/s) of this workload's index stream, if profiled."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            v = json.load(f).get(config_name) or {}
-        return v.get("gather_ceiling_GBps")
-    except Exception:
-        return None
+    return load_traffic_entry(config_name).get("gather_ceiling_GBps")
 
 
 def load_traffic(config_name):
-    """DRAM bytes (read + write) of one filter-step launch, from the committed ncu --set full
-    capture of the bench command (profiles/ncu_traffic.json)."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    try:
-        with open(p) as f:
-            t = json.load(f)
-        v = t.get(config_name)
-        return None if v is None else float(v["dram_bytes_per_launch"])
-    except Exception:
-        return None
+    """DRAM bytes (read + write) of one filter-step launch from the committed ncu --set full
+    capture (profiles/ncu_traffic.json), ONLY if it was captured from the current kernel source
+    (its kernel_source_sha matches embed.cu); otherwise (None, reason)."""
+    v = load_traffic_entry(config_name)
+    if "dram_bytes_per_launch" not in v:
+        return None, "no ncu capture for this config"
+    if v.get("kernel_source_sha") != kernel_source_sha():
+        return None, "ncu capture predates the current embed.cu (sha mismatch): not reported"
+    return float(v["dram_bytes_per_launch"]), v.get("source")
+
+
+def l2_policy(cfg, nnz, l2_bytes):
+    """How the timing rule on L2 is met for this config (stated in config.l2): inputs larger than
+    L2, or an explicit L2 flush between timed steps."""
+    edges_b = 8 * (cfg.num_edges if cfg.name != "streaming" else cfg.num_edges)
+    z_b = 4 * cfg.num_nodes * cfg.d
+    csr_b = 4 * nnz + 4 * (cfg.num_nodes + 1)
+    foot = edges_b + z_b + csr_b
+    big = foot > 2 * l2_bytes
+    desc = (f"footprint {foot / 1e6:.0f} MB (edges {edges_b / 1e6:.0f} MB, CSR {csr_b / 1e6:.0f} MB, "
+            f"Z {z_b / 1e6:.0f} MB) vs L2 {l2_bytes / 1e6:.0f} MB: ")
+    desc += "inputs > 2 x L2, no flush" if big else "L2 flushed (256 MB write) before every timed step, untimed"
+    return (not big), desc
 
 
 # ---------------------------------------------------------------- CPU oracle leg
@@ -164,6 +199,26 @@ def oracle_sample(cfg, edges, layers, nthreads):
     t0 = time.perf_counter()
     oracle.embed(rp, ci, cfg.num_nodes, cfg.d, layers, cfg.tau, seed=cfg.seed, nthreads=nthreads)
     return time.perf_counter() - t0, int(ci.size)
+
+
+def oracle_single_thread(cfg, edges, layers=1):
+    """The oracle on ONE thread, `layers` filter steps (+ input, output) of the same graph."""
+    secs, onnz = oracle_sample(cfg, edges, layers, 1)
+    return {"value": onnz * cfg.d * layers / secs / 1e9, "unit": "GEdge·feat/s", "cores": 1, "kind": "oracle",
+            "sample": f"{cfg.name} graph, {layers} of L={cfg.steps} filter steps (+ Philox input, sigmoid), fp64, "
+                      f"1 thread, {secs:.1f} s"}
+
+
+def birch_oracle_time(Z, threshold, branching, max_rows=None):
+    """The oracle's BIRCH (fit + predict) on the same fp32 rows, single thread (the reference
+    for the downstream clustering step)."""
+    import oracle
+    X = Z if max_rows is None else Z[:max_rows]
+    X = X.astype("float64")
+    t0 = time.perf_counter()
+    b = oracle.Birch(X.shape[1], threshold, branching).fit(X)
+    b.predict(X)
+    return time.perf_counter() - t0, X.shape[0]
 
 
 def cpu_model():
@@ -214,12 +269,88 @@ def run_reference(args, cfg):
             "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic DC-SBM (synth/dcsbm.py)",
             "config": {"workload": cfg.name, "num_nodes": cfg.num_nodes, "nnz": nnz, "d": cfg.d, "tau": cfg.tau,
-                       "L": cfg.steps, "L_sampled": layers},
+                       "L": cfg.steps, "L_sampled": layers,
+                       "note": "a per-edge-feature RATE: each step runs the oracle on the full graph for "
+                               f"{layers} of the L = {cfg.steps} filter steps (+ input, output); GEdge·feat/s "
+                               "does not depend on L, so the ratio to the GPU arm is a per-layer rate ratio"},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "GEdge·feat/s", "cores": cores, "kind": "oracle",
                              "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": "GEdge·feat/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def dist_init(backend, device=None):
+    import torch.distributed as dist
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=device)
+    else:
+        dist.init_process_group(backend)
+
+
+def gather_rank_values(vals, device=None):
+    """all_gather of a small float64 vector per rank -> list of lists (rank order)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    allt = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(allt, t)
+    return [[float(v) for v in x] for x in allt]
+
+
+def relaunch_under_torchrun(n):
+    """`--gpus N` outside torchrun: run this script again as N ranks (one process per GPU)."""
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def base_line(args, cfg, world, value, ms_per_step, dtype, nnz, extra_cfg):
+    line = {"metric": "FFP embed throughput (GEdge·feat/s)", "value": value, "unit": "GEdge·feat/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+            "data": "synthetic DC-SBM (synth/dcsbm.py), seed = rank",
+            "config": {"workload": cfg.name, "num_nodes": cfg.num_nodes, "nnz": nnz, "d": cfg.d, "tau": cfg.tau,
+                       "L": cfg.steps, "parallelism": f"replicas x{world}"}}
+    line["config"].update(extra_cfg)
+    return line
+
+
+# ---------------------------------------------------------------- CPU self-test of the multi-rank path
+def run_selftest_cpu(args, cfg):
+    """The multi-rank skeleton of the GPU arm on CPU (gloo): the same init, barrier, per-rank
+    timing exchange and aggregation, with a CPU stand-in for the step.  Used by
+    tests/test_multirank.py to check `--gpus N` end to end without a GPU."""
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist_init("gloo")
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    acc = 0
+    for i in range(20000 * (rank + 1)):  # rank r does (r + 1) units of work
+        acc += i * i
+    ms = (time.perf_counter() - t0) * 1e3
+    units = float(rank + 1) * 1e6
+    if world > 1:
+        vals = gather_rank_values([ms, units])
+        per_ms, per_units = [v[0] for v in vals], [v[1] for v in vals]
+    else:
+        per_ms, per_units = [ms], [units]
+    value, tmax = aggregate(per_ms, per_units)
+    if rank == 0:
+        line = base_line(args, cfg, world, value / 1e9, tmax / args.steps, "cpu-selftest", 0, {"selftest": True})
+        line["per_rank_ms"] = per_ms
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
     return 0
 
 
@@ -230,8 +361,7 @@ def run_gpu(args, cfg):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        dist_init("nccl", dev)
     import paper_2508_19737_b200 as igp
 
     seed = cfg.seed + rank  # replicas: independent graphs
@@ -242,12 +372,28 @@ def run_gpu(args, cfg):
     stream = torch.cuda.current_stream(dev)
     N, d, L, tau = cfg.num_nodes, cfg.d, cfg.steps, cfg.tau
     out = torch.empty((N, d), dtype=torch.float32, device=dev)
+    streaming = cfg.name == "streaming"
+    batches = [torch.from_numpy(b).to(dev) for b in stream_batches(edges_np, 10)] if streaming else None
+    stage_ev = None
 
-    def step(timed):
-        # the whole step is enqueued without a host sync: asynchronous build (range errors
-        # are checked on the warm-up graphs), embed, stream-ordered release of the graph
-        g = igp.build_graph(edges, N, stream=stream, async_build=True)
-        igp.embed(g, tau, d, L, seed, out=out, stream=stream, time_layers=timed)
+    def step(timed, record_stages=False):
+        # the whole step is enqueued without a host sync: asynchronous build (range errors are
+        # checked on the warm-up graphs), embed, stream-ordered release of the graph
+        if not streaming:
+            g = igp.build_graph(edges, N, stream=stream, async_build=True)
+            igp.embed(g, tau, d, L, seed, out=out, stream=stream, time_layers=timed)
+            g.close(stream=stream)
+            return
+        # Alg. 2 l.1-7 over the 10 cumulative stages: stage 0 build, then merge + re-embed
+        g = igp.build_graph(batches[0], N, stream=stream, async_build=True)
+        for t in range(10):
+            if t > 0:
+                g.add_edges(batches[t], stream=stream)
+            if record_stages:
+                stage_ev[t][0].record(stream)
+            igp.embed(g, tau, d, L, seed, out=out, stream=stream, time_layers=timed, subsequence=t)
+            if record_stages:
+                stage_ev[t][1].record(stream)
         g.close(stream=stream)
 
     def barrier():
@@ -256,9 +402,25 @@ def run_gpu(args, cfg):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    g = igp.build_graph(edges, N, stream=stream)  # synchronous build: validates the input, gives nnz
-    nnz = g.nnz
-    g.close()
+    # units of one step: nnz x d x L (streaming: summed over the 10 stages' graphs)
+    if streaming:
+        g = igp.build_graph(batches[0], N, stream=stream)
+        stage_nnz = [g.nnz]
+        for t in range(1, 10):
+            g.add_edges(batches[t], stream=stream)
+            stage_nnz.append(g.nnz)
+        g.close()
+        nnz = stage_nnz[-1]
+        units_step = sum(stage_nnz) * d * L
+    else:
+        g = igp.build_graph(edges, N, stream=stream)  # synchronous build: validates the input, gives nnz
+        nnz = g.nnz
+        g.close()
+        units_step = nnz * d * L
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush, l2_desc = l2_policy(cfg, nnz, l2_bytes)
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if flush else None
+
     for _ in range(args.warmup):
         step(True)  # same calls as the timed steps (the timer's events are created here)
     torch.cuda.synchronize(dev)
@@ -269,42 +431,50 @@ def run_gpu(args, cfg):
     step(True)  # the GPU idled while the sampler started: one more untimed step brings it back up
     igp.layer_timer_reset()
     launches0 = igp.kernel_launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev0.record(stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if streaming:
+        stage_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
     for k in range(args.steps):
-        step(True)
-        step_ev[k].record(stream)
-    ev1.record(stream)
+        if flush:
+            flush_buf.fill_(float(k))  # untimed: outside the step's events
+        ev[k][0].record(stream)
+        step(True, record_stages=streaming and k == args.steps - 1)
+        ev[k][1].record(stream)
     barrier()
-    log(f"[rank {rank}] per-step ms: " + " ".join(
-        f"{(ev0 if k == 0 else step_ev[k - 1]).elapsed_time(step_ev[k]):.2f}" for k in range(args.steps)))
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    log(f"[rank {rank}] per-step ms: " + " ".join(f"{x:.2f}" for x in per_step))
     launches = igp.kernel_launch_count() - launches0
     clock_rec = clocks.stop()
-    ms_total = ev0.elapsed_time(ev1)
+    ms_total = sum(per_step)
     tot_layer_ms, tot_launches = igp.layer_timer_read()
+    stages = None
+    if streaming:
+        st_embed = [a.elapsed_time(b) for a, b in stage_ev]
+        # stage t's build / merge = from the previous stage's embed end (or the step start) to this embed
+        starts = [ev[-1][0]] + [stage_ev[t - 1][1] for t in range(1, 10)]
+        st_merge = [starts[t].elapsed_time(stage_ev[t][0]) for t in range(10)]
+        stages = [{"stage": t, "nnz": stage_nnz[t], "build_or_merge_ms": st_merge[t], "embed_ms": st_embed[t]}
+                  for t in range(10)]
 
-    # embed-only timing (no build), same stream, for the breakdown
-    g = igp.build_graph(edges, N, stream=stream)
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        igp.embed(g, tau, d, L, seed, out=out, stream=stream)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    embed_ms = e0.elapsed_time(e1) / args.steps
-    g.close()
+    # embed-only timing (no build), same stream, for the breakdown (static configs)
+    embed_ms = None
+    if not streaming:
+        g = igp.build_graph(edges, N, stream=stream)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            igp.embed(g, tau, d, L, seed, out=out, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        embed_ms = e0.elapsed_time(e1) / args.steps
+        g.close()
 
-    units = nnz * d * L * args.steps
+    units = units_step * args.steps
     if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms_total, float(units)], dtype=torch.float64, device=dev)
-        all_t = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(all_t, t)
-        per_ms = [float(x[0]) for x in all_t]
-        per_units = [float(x[1]) for x in all_t]
+        vals = gather_rank_values([ms_total, float(units)], dev)
+        per_ms, per_units = [v[0] for v in vals], [v[1] for v in vals]
     else:
         per_ms, per_units = [ms_total], [float(units)]
     value, t_max = aggregate(per_ms, per_units)
@@ -314,43 +484,48 @@ def run_gpu(args, cfg):
     # columns is d/W launches of layer_kernel<W> (column slices); the
     # algorithmic bytes are those of the whole step (SURVEY.md §8(d) B_step), so
     # achieved = B_step / (time of the d/W launches that make up one step).
-    slices = max(1, tot_launches // max(1, L * args.steps))
+    n_embeds = 10 if streaming else 1
+    slices = max(1, tot_launches // max(1, L * args.steps * n_embeds))
     width = d // slices
     avg_launch_s = tot_layer_ms / 1e3 / max(tot_launches, 1)
     step_s = avg_launch_s * slices
     b_step = step_bytes(N, nnz, d)
     peak, peak_src = hbm_peak()
     achieved = b_step / step_s / 1e9
-    traffic = load_traffic(cfg.name)
+    traffic, traffic_src = load_traffic(cfg.name)
     # per launch (the contract's unit): one filter step is `slices` column-slice launches, so a
     # launch's algorithmic bytes are B_step / slices and achieved = that / the average launch
     # time (identical to B_step / step time); traffic is the ncu DRAM bytes of one launch
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": f"layer_kernel<{width}> ({slices} column-slice launches per filter step)",
+            "traffic": traffic, "traffic_source": traffic_src, "kernel_source_sha": kernel_source_sha()[:16],
+            "kernel": f"layer_kernel<{width}> ({slices} column-slice launches per filter step)",
             "per": "launch", "algorithmic_bytes": b_step / slices, "algorithmic_bytes_per_step": b_step,
             "traffic_per_step": None if traffic is None else traffic * slices,
             "step_us": step_s * 1e6, "avg_launch_us": avg_launch_s * 1e6, "peak_source": peak_src,
             "gather_bytes_per_step": 4 * nnz * d, "gather_GBps": 4 * nnz * d / step_s / 1e9,
             "gather_ceiling_GBps": load_gather_ceiling(cfg.name),
-            "share_of_step": tot_layer_ms / ms_total,
-            # whole-embed compulsory bytes over the embed time (SURVEY.md §8(d) "B_embed/(t HBM)")
-            "embed_algorithmic_bytes": embed_bytes(N, nnz, d, L),
-            "embed_frac": embed_bytes(N, nnz, d, L) / (embed_ms / 1e3) / 1e9 / peak,
-            "embed_frac_8TBs": embed_bytes(N, nnz, d, L) / (embed_ms / 1e3) / 8e12}
+            "share_of_step": tot_layer_ms / ms_total}
+    if streaming:
+        roof["note"] = "streaming: the final stage's nnz (the largest graph) is the byte basis of B_step"
+    if embed_ms is not None:
+        # whole-embed compulsory bytes over the embed time (SURVEY.md §8(d) "B_embed/(t HBM)")
+        roof.update({"embed_algorithmic_bytes": embed_bytes(N, nnz, d, L),
+                     "embed_frac": embed_bytes(N, nnz, d, L) / (embed_ms / 1e3) / 1e9 / peak,
+                     "embed_frac_8TBs": embed_bytes(N, nnz, d, L) / (embed_ms / 1e3) / 8e12})
 
-    line = {"metric": "FFP embed throughput (GEdge·feat/s)", "value": value, "unit": "GEdge·feat/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic DC-SBM (synth/dcsbm.py), seed = rank",
-            "config": {"workload": cfg.name, "num_nodes": N, "nnz": nnz, "d": d, "tau": tau, "L": L,
-                       "step": "igp_build_graph + igp_embed", "embed_ms": embed_ms,
-                       "build_ms": t_max / args.steps - embed_ms,
-                       "l2": "inputs > L2: edge list 160 MB, Z 256 MB per buffer, no flush needed",
-                       "parallelism": f"replicas x{world}"},
-            "roofline": roof, "gpu_launches": launches, "clocks": clock_rec}
+    step_desc = ("10 stages: igp_build_graph (stage 0) / igp_graph_add_edges (stages 1-9) + igp_embed "
+                 "(subsequence t)" if streaming else "igp_build_graph + igp_embed")
+    extra = {"step": step_desc, "l2": l2_desc}
+    if embed_ms is not None:
+        extra.update({"embed_ms": embed_ms, "build_ms": t_max / args.steps - embed_ms})
+    if stages is not None:
+        extra["stages"] = stages
+        extra["units_per_step"] = "sum over the 10 stages of nnz_t x d x L"
+    line = base_line(args, cfg, world, value, t_max / args.steps, "f32", nnz, extra)
+    line.update({"roofline": roof, "gpu_launches": launches, "clocks": clock_rec})
 
-    # e2e through the public host-buffer API (pinned host memory in and out)
-    if not args.no_e2e:
+    # e2e through the public host-buffer API (pinned host memory in and out); static configs
+    if not args.no_e2e and not streaming:
         h_edges = torch.from_numpy(edges_np).pin_memory()
         h_out = torch.empty((N, d), dtype=torch.float32, pin_memory=True)
         igp.embed_host(h_edges, N, tau, d, L, seed, out=h_out, stream=stream)  # warm
@@ -364,21 +539,44 @@ def run_gpu(args, cfg):
         barrier()
         e2e_ms = x0.elapsed_time(x1) / ke
         if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t)
+            e2e_ms = max(v[0] for v in gather_rank_values([e2e_ms], dev))
         line["e2e"] = {"value": nnz * d * L * world / (e2e_ms / 1e3) / 1e9, "unit": "GEdge·feat/s",
                        "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(h_edges.numel() * 4),
                        "d2h_bytes_per_step": int(h_out.numel() * 4)}
 
+    # the downstream BIRCH (Alg. 1 l.7) on this step's embedding: reported beside the FFP, not
+    # part of the step; the oracle's BIRCH on the same rows (one thread) is its reference
+    if not args.no_birch:
+        torch.cuda.synchronize(dev)
+        b0 = time.perf_counter()
+        bt = igp.Birch(d, args.birch_threshold, args.birch_branching, device=dev).partial_fit(out, stream=stream)
+        fit_s = time.perf_counter() - b0
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        bt.predict(out, stream=stream)
+        p1.record(stream)
+        torch.cuda.synchronize(dev)
+        K, depth, nodes, pts = bt.info()
+        bt.close()
+        line["birch"] = {"fit_s": fit_s, "predict_ms": p0.elapsed_time(p1), "clusters": K, "depth": depth,
+                         "threshold": args.birch_threshold, "branching": args.birch_branching, "rows": pts,
+                         "what": "igp_birch_partial_fit (CF-tree build, one persistent CTA, fp64) + igp_birch_predict "
+                                 "on the step's embedding; not part of the timed step"}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            rows = min(N, args.birch_oracle_rows)
+            secs, n_rows = birch_oracle_time(out.cpu().numpy(), args.birch_threshold, args.birch_branching, rows)
+            line["birch"]["oracle"] = {"s": secs, "rows": n_rows, "cores": 1,
+                                       "rows_per_s": n_rows / secs, "gpu_rows_per_s": pts / (fit_s + p0.elapsed_time(p1) / 1e3)}
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = cpu_cores()
-        secs, onnz = oracle_sample(cfg, edges_np, args.cpu_layers, cores)
+        secs, onnz = oracle_sample(cfg, edges_np if not streaming else np.concatenate(stream_batches(edges_np, 10)),
+                                   args.cpu_layers, cores)
         line["cpu_baseline"] = {"value": onnz * d * args.cpu_layers / secs / 1e9, "unit": "GEdge·feat/s",
                                 "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                                 "sample": f"{cfg.name} graph, {args.cpu_layers} of L={L} filter steps "
-                                          f"(+ Philox input, sigmoid), fp64, {secs:.1f} s"}
+                                          f"(+ Philox input, sigmoid), fp64, {secs:.1f} s",
+                                "single_thread": oracle_single_thread(cfg, edges_np, 1)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -398,10 +596,19 @@ def main():
     ap.add_argument("--ref-layers", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-birch", action="store_true")
+    ap.add_argument("--birch-threshold", type=float, default=1.0)  # reading B1
+    ap.add_argument("--birch-branching", type=int, default=50)
+    ap.add_argument("--birch-oracle-rows", type=int, default=200_000)
+    ap.add_argument("--selftest-cpu", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args.gpus)
     cfg = CONFIGS[args.config]
+    if args.selftest_cpu:
+        return run_selftest_cpu(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_gpu(args, cfg)

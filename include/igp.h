@@ -72,7 +72,8 @@ typedef enum {
  *              {u, v}, u != v, becomes A_uv = A_vu = 1 once.
  *   num_edges  >= 0 (0 is valid: M = 0, all degrees 0); 2*num_edges must be
  *              <= INT32_MAX - 64 (int32 CSR offsets; else IGP_ERR_UNSUPPORTED).
- *   num_nodes  N >= 1 (else IGP_ERR_INPUT) and <= INT32_MAX - 64 (else IGP_ERR_UNSUPPORTED).
+ *   num_nodes  N >= 1 (else IGP_ERR_INPUT) and <= 2^30 - 4096 (else IGP_ERR_UNSUPPORTED: the
+ *              builder's int32 scans and digit histograms cover ~2N entries).
  *   out        receives a new handle owning device row_ptr int32[N+1] and
  *              col_idx int32[2M] (rows ascending, columns strictly ascending); the
  *              column arrays are allocated for the 2*num_edges directed entries before
@@ -127,10 +128,15 @@ IGP_API igp_status igp_graph_info(igp_graph_t g, int32_t* num_nodes, int64_t* nn
 IGP_API igp_status igp_graph_status(igp_graph_t g);
 
 /* Copy the canonical CSR (original node ids) into caller-owned device buffers
- * d_row_ptr int32[N+1] and d_col_idx int32[nnz]; asynchronous on `stream`. */
-IGP_API igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t* d_col_idx, igp_stream_t stream);
+ * d_row_ptr int32[N+1], d_col_idx int32[nnz] and d_deg int32[N] (deg_i = row_ptr[i+1] -
+ * row_ptr[i], the degree diagonal D of PAPER.md:82); d_deg may be NULL.  Asynchronous on
+ * `stream`. */
+IGP_API igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t* d_col_idx, int32_t* d_deg,
+                                      igp_stream_t stream);
 
-/* Release a graph (synchronises the device before freeing).  NULL is a no-op. */
+/* Release a graph.  Waits only for the work this library enqueued on the graph (its build /
+ * merges and every embed's use of it, tracked by events), never for unrelated streams; the
+ * memory is released in stream order behind those uses.  NULL is a no-op. */
 IGP_API igp_status igp_destroy_graph(igp_graph_t g);
 
 /* Release a graph in stream order on `stream` without any host synchronisation: all
@@ -164,9 +170,12 @@ typedef struct {
     int32_t mode;         /* IGP_MODE_* */
     uint32_t flags;       /* IGP_FLAG_* */
     const float* d_z0;    /* NULL (default): Z^(0) = Theta from Philox (Alg. 1 l.2).  Otherwise a
-                             caller-owned device fp32 [N][d] row-major Z^(0) (row i = node id i) used
-                             instead of Theta: an inspection / verification hook (e.g. layer-by-layer
-                             checks from a given state, Alg. 1 l.3 "Z^(0) <- Theta" replaced) */
+                             caller-owned device fp32 [N][d] row-major Z^(0) (row i = node id i), 16-byte
+                             aligned, used instead of Theta: an inspection / verification hook (e.g.
+                             layer-by-layer checks from a given state, Alg. 1 l.3 "Z^(0) <- Theta" replaced) */
+    int32_t ddof;         /* ZNorm's standard deviation divides by N - ddof: 0 (default) = population std
+                             (reading A2; PAPER.md:166 does not say), 1 = sample std.  0 <= ddof <= 1;
+                             a column with N <= ddof is treated as constant (reading A3) */
 } igp_embed_opts;
 
 /* Fill opts with the paper's defaults: theta 0.1, alpha 1, eps 1e-3, subsequence 0,
@@ -179,9 +188,11 @@ IGP_API void igp_embed_opts_default(igp_embed_opts* opts);
  * (readings A1, A11).  Fully asynchronous on `stream`; workspace is
  * allocated stream-ordered (cudaMallocAsync) and released before return, so the
  * handle is read-only and concurrent embeds on different streams are safe.
- * Errors (host-validated, nothing enqueued): NULL g/d_out or non-finite tau ->
- * IGP_ERR_INPUT; d not a multiple of 16 in [16, 1024] -> IGP_ERR_UNSUPPORTED; steps < 0 ->
- * IGP_ERR_INPUT.  Deterministic: identical arguments give bitwise-identical output. */
+ * Errors (host-validated, nothing enqueued): NULL g/d_out, d_out (or opts.d_z0) not 16-byte
+ * aligned, or non-finite tau -> IGP_ERR_INPUT; d not a multiple of 16 in [16, 1024] ->
+ * IGP_ERR_UNSUPPORTED; steps < 0 -> IGP_ERR_INPUT.  Deterministic: identical arguments give
+ * bitwise-identical output.  (There is no separate "stop after layer k" mode: steps = k is
+ * that run; DESIGN.md §8(b) deviations.) */
 IGP_API igp_status igp_embed(igp_graph_t g, float tau, int32_t d, int32_t steps, uint64_t seed,
                      float* d_out, igp_stream_t stream);
 
@@ -220,6 +231,51 @@ IGP_API igp_status igp_philox_normal(uint64_t seed, uint64_t subsequence, int64_
                              igp_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * BIRCH clustering of the embeddings  (Alg. 1 l.7; streaming Alg. 2
+ * l.9-11; BIRCH as the paper invokes it)
+ *
+ * A CF tree (clustering features n, LS, SS per entry; at most `branching` entries per
+ * node; leaf entries of radius <= threshold) built by single-pass insertion of rows in
+ * row order; its leaf entries, in leaf-chain order, are the K-agnostic clusters, and a
+ * row's label is the index of its nearest leaf centroid.  fp64 on the device, with the
+ * exact operation order of oracle/birch_oracle.c (readings B1-B6), so trees,
+ * clusters and labels are bitwise reproducible.
+ * ------------------------------------------------------------------------- */
+typedef struct igp_birch_s* igp_birch_t;
+
+/* New empty tree on the current device for rows of width d (1 <= d <= 1024), radius
+ * threshold T > 0 (finite) and branching factor 2 <= B <= 63 (scikit-learn's defaults,
+ * T = 0.5 and B = 50).  Invalid arguments -> IGP_ERR_INPUT. */
+IGP_API igp_status igp_birch_create(int32_t d, double threshold, int32_t branching, igp_birch_t* out);
+
+/* Insert rows d_X (device fp32 [m][d] row-major, e.g. igp_embed's output, widened to
+ * fp64 exactly) in row order: fit on a new tree (Alg. 1 l.7), partial fit on an existing
+ * one (Alg. 2 l.9).  Synchronous: returns after the tree is updated (the insertion is a
+ * sequential process; the device pools grow as needed).  m = 0 is a no-op.  A non-finite
+ * value -> IGP_ERR_INPUT (tree unchanged). */
+IGP_API igp_status igp_birch_partial_fit(igp_birch_t b, const float* d_X, int64_t m, igp_stream_t stream);
+
+/* Tree statistics: number of clusters K (leaf entries), depth (levels), nodes, points
+ * inserted.  Any output may be NULL.  Synchronous. */
+IGP_API igp_status igp_birch_info(igp_birch_t b, int64_t* num_clusters, int32_t* depth, int64_t* nodes,
+                                  int64_t* points);
+
+/* The K clusters in label order: device fp64 centroids [K][d], |centroid|^2 [K], point
+ * counts n [K], linear sums LS [K][d], square sums SS [K] (caller-owned; any may be NULL).
+ * Asynchronous on `stream` (after a synchronous count). */
+IGP_API igp_status igp_birch_clusters(igp_birch_t b, double* d_centroids, double* d_sqn, double* d_n, double* d_ls,
+                                      double* d_ss, igp_stream_t stream);
+
+/* Labels (Alg. 2 l.11): d_labels[i] = argmin_j |c_j|^2 - 2 c_j . x_i over the K clusters
+ * (first minimum; |x_i|^2 is common to all j, reading B5), device int32 [m].  Does not
+ * modify the tree.  Empty tree -> IGP_ERR_INPUT.  Asynchronous on `stream`. */
+IGP_API igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m, int32_t* d_labels,
+                                     igp_stream_t stream);
+
+/* Release the tree (waits for the legacy default stream).  NULL is a no-op. */
+IGP_API igp_status igp_birch_destroy(igp_birch_t b);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics
  * ------------------------------------------------------------------------- */
 IGP_API const char* igp_status_string(igp_status s);
@@ -228,6 +284,10 @@ IGP_API const char* igp_last_error_message(void);
 IGP_API uint64_t igp_kernel_launch_count(void);
 /* Library version string. */
 IGP_API const char* igp_version(void);
+/* Return the library's cached device memory to the driver.  Every workspace (builds, embeds)
+ * comes from a memory pool private to this library (never the device's default pool), which
+ * keeps freed blocks for reuse by later calls; this trims it on the current device. */
+IGP_API igp_status igp_trim_memory(void);
 
 #ifdef __cplusplus
 }

@@ -77,6 +77,10 @@ def _load():
     lib.oracle_row_l2.restype = None
     lib.oracle_embed.argtypes = [P, P, i32, i32, i32, f64, f64, f64, f64, P, u64, u64, i32, i32, P]
     lib.oracle_embed.restype = ctypes.c_int
+    lib.oracle_embed_ddof.argtypes = [P, P, i32, i32, i32, f64, f64, f64, f64, P, u64, u64, i32, i32, i32, P]
+    lib.oracle_embed_ddof.restype = ctypes.c_int
+    lib.oracle_zscore_columns_ddof.argtypes = [P, i32, i32, i32]
+    lib.oracle_zscore_columns_ddof.restype = None
     lib.oracle_embed_f32.argtypes = [P, P, i32, i32, i32, f64, f64, f64, f64, P, u64, u64, i32, i32, P]
     lib.oracle_embed_f32.restype = ctypes.c_int
     lib.oracle_birch_new.argtypes = [i32, f64, i32]
@@ -189,12 +193,13 @@ def propagate(row_ptr, col_idx, Dtau, Z, theta=THETA, alpha=ALPHA, nthreads=1) -
     return P
 
 
-def zscore_columns(T) -> np.ndarray:
+def zscore_columns(T, ddof: int = 0) -> np.ndarray:
+    """Column z-score (ZNorm), std over N - ddof (reading A2: ddof = 0)."""
     lib = _load()
     T = np.array(T, dtype=np.float64, order="C", copy=True)
     if T.ndim == 1:
         T = T[:, None]
-    lib.oracle_zscore_columns(_ptr(T), T.shape[0], T.shape[1])
+    lib.oracle_zscore_columns_ddof(_ptr(T), T.shape[0], T.shape[1], int(ddof))
     return T
 
 
@@ -210,7 +215,7 @@ def row_l2(Z) -> np.ndarray:
 
 def embed(row_ptr, col_idx, num_nodes: int, d: int, steps: int, tau: float, seed: int = 0,
           sub: int = 0, theta=THETA, alpha=ALPHA, eps=EPS, Z0=None, mode=MODE_FULL,
-          nthreads: int = 1, fp32_twin: bool = False) -> np.ndarray:
+          nthreads: int = 1, fp32_twin: bool = False, ddof: int = 0) -> np.ndarray:
     """Alg. 1 lines 1-6 in fp64; returns Z~ (or Z^(L) / linear output per ``mode``).
 
     ``fp32_twin=True`` runs ``oracle_embed_f32`` instead: the same steps with float storage
@@ -223,9 +228,14 @@ def embed(row_ptr, col_idx, num_nodes: int, d: int, steps: int, tau: float, seed
     if Z0 is not None:
         Z0 = np.ascontiguousarray(Z0, dtype=np.float64).reshape(num_nodes, d)
         z0p = _ptr(Z0)
-    fn = lib.oracle_embed_f32 if fp32_twin else lib.oracle_embed
-    rc = fn(_ptr(rp), _ptr(ci), num_nodes, d, steps, tau, theta, alpha, eps, z0p, seed, sub, mode, nthreads,
-            _ptr(out))
+    if fp32_twin:
+        if ddof:
+            raise OracleError("the fp32 twin uses the population std (ddof = 0)")
+        rc = lib.oracle_embed_f32(_ptr(rp), _ptr(ci), num_nodes, d, steps, tau, theta, alpha, eps, z0p, seed, sub,
+                                  mode, nthreads, _ptr(out))
+    else:
+        rc = lib.oracle_embed_ddof(_ptr(rp), _ptr(ci), num_nodes, d, steps, tau, theta, alpha, eps, z0p, seed, sub,
+                                   mode, nthreads, int(ddof), _ptr(out))
     if rc != 0:
         raise OracleError(f"oracle_embed rejected its arguments (rc={rc})")
     return out

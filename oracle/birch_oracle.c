@@ -32,7 +32,7 @@
  *   clusters:   the leaf entries in leaf-chain order; label(x) = argmin_j sqn_j - 2 c_j . x.
  *
  * Arithmetic (fixed so that an independent implementation can reproduce every bit):
- * dot(a, b) = fma-accumulated sum over k = 0..d-1 in ascending k; CF addition updates
+ * dot(a, b) = eight fma partial sums over k mod 8, combined pairwise (dotk); CF addition updates
  * n, LS (elementwise), SS, then c = LS / n (division), sqn = dot(c, c); the merge test
  * uses c' = (1 / n') * LS' (reciprocal, then products).
  */
@@ -66,10 +66,13 @@ typedef struct {
     int64_t npoints;
 } birch_tree;
 
+/* dot(a, b): eight fma-accumulated partial sums p_r over k = r (mod 8), k ascending, combined
+ * as ((p0 + p1) + (p2 + p3)) + ((p4 + p5) + (p6 + p7))  (reading B6: a dot product's summation
+ * order is not part of BIRCH; this one is fixed so another implementation can match it) */
 static double dotk(const double* a, const double* b, int32_t d) {
-    double acc = 0.0;
-    for (int32_t k = 0; k < d; ++k) acc = fma(a[k], b[k], acc);
-    return acc;
+    double p[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int32_t k = 0; k < d; ++k) p[k % 8] = fma(a[k], b[k], p[k % 8]);
+    return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
 }
 
 static int grow_subs(birch_tree* t) {

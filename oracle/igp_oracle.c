@@ -245,10 +245,11 @@ void oracle_propagate(const int32_t* row_ptr, const int32_t* col_idx, int32_t N,
     free(s);
 }
 
-/* ZNorm(x) := (x - mu(x)) / s(x), column-wise, population
- * standard deviation (reading A2); a column with s < 1e-8 becomes 0 (A3).
+/* ZNorm(x) := (x - mu(x)) / s(x), column-wise; s is the standard deviation
+ * with N - ddof in the denominator: ddof = 0 (population, reading A2, the default) or 1
+ * (sample); a column with s < 1e-8, or N <= ddof, becomes 0 (A3).
  * In place on T (N x d, row-major).  Two passes, serial, ascending rows. */
-void oracle_zscore_columns(double* T, int32_t N, int32_t d) {
+void oracle_zscore_columns_ddof(double* T, int32_t N, int32_t d, int32_t ddof) {
     for (int32_t c = 0; c < d; ++c) {
         double sum = 0.0;
         for (int32_t i = 0; i < N; ++i) sum += T[(int64_t)i * d + c];
@@ -258,13 +259,15 @@ void oracle_zscore_columns(double* T, int32_t N, int32_t d) {
             double x = T[(int64_t)i * d + c] - mu;
             ss += x * x;
         }
-        double s = sqrt(ss / (double)N);
+        double s = N > ddof ? sqrt(ss / (double)(N - ddof)) : 0.0;
         for (int32_t i = 0; i < N; ++i) {
             double* x = &T[(int64_t)i * d + c];
             *x = (s < 1e-8) ? 0.0 : (*x - mu) / s;
         }
     }
 }
+
+void oracle_zscore_columns(double* T, int32_t N, int32_t d) { oracle_zscore_columns_ddof(T, N, d, 0); }
 
 /* Optional row L2 normalisation of an output (NOT part of the paper's method: Eq. (4),
  * PAPER.md:164-166, ends with the sigmoid; the north star's wording "the rows are normalised
@@ -295,10 +298,10 @@ void oracle_row_l2(double* Z, int32_t N, int32_t d) {
  *   4-5: Z^(l) <- ZNorm(tanh(phi * Z^(l-1)))   for l = 1..L
  *   6: Z~ <- sigmoid(Z^(L))
  * Returns 0, or ORACLE_ERR_INPUT on invalid arguments. */
-int oracle_embed(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int32_t d, int32_t L,
-                 double tau, double theta, double alpha, double eps, const double* Z0,
-                 uint64_t seed, uint64_t sub, int32_t mode, int32_t nthreads, double* out) {
-    if (N <= 0 || d <= 0 || L < 0 || (Z0 == NULL && d % 4 != 0)) return ORACLE_ERR_INPUT;
+int oracle_embed_ddof(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int32_t d, int32_t L,
+                      double tau, double theta, double alpha, double eps, const double* Z0,
+                      uint64_t seed, uint64_t sub, int32_t mode, int32_t nthreads, int32_t ddof, double* out) {
+    if (N <= 0 || d <= 0 || L < 0 || (Z0 == NULL && d % 4 != 0) || ddof < 0) return ORACLE_ERR_INPUT;
     int64_t nd = (int64_t)N * d;
     double* Dtau = (double*)malloc((size_t)N * sizeof(double));
     double* Z = (double*)malloc((size_t)nd * sizeof(double));
@@ -328,7 +331,7 @@ int oracle_embed(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int3
             continue;
         }
         for (int64_t k = 0; k < nd; ++k) P[k] = tanh(P[k]);
-        oracle_zscore_columns(P, N, d);
+        oracle_zscore_columns_ddof(P, N, d, ddof);
         memcpy(Z, P, (size_t)nd * sizeof(double));
     }
     /* line 6 */
@@ -338,6 +341,12 @@ int oracle_embed(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int3
     free(Z);
     free(P);
     return 0;
+}
+
+int oracle_embed(const int32_t* row_ptr, const int32_t* col_idx, int32_t N, int32_t d, int32_t L,
+                 double tau, double theta, double alpha, double eps, const double* Z0,
+                 uint64_t seed, uint64_t sub, int32_t mode, int32_t nthreads, double* out) {
+    return oracle_embed_ddof(row_ptr, col_idx, N, d, L, tau, theta, alpha, eps, Z0, seed, sub, mode, nthreads, 0, out);
 }
 
 /* ------------------------------------------------------------------------ */

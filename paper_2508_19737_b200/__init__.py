@@ -43,7 +43,7 @@ class EmbedOpts(ctypes.Structure):
     _fields_ = [("tau", ctypes.c_float), ("d", ctypes.c_int32), ("steps", ctypes.c_int32),
                 ("seed", ctypes.c_uint64), ("subsequence", ctypes.c_uint64), ("theta", ctypes.c_float),
                 ("alpha", ctypes.c_float), ("eps", ctypes.c_float), ("mode", ctypes.c_int32),
-                ("flags", ctypes.c_uint32), ("d_z0", ctypes.c_void_p)]
+                ("flags", ctypes.c_uint32), ("d_z0", ctypes.c_void_p), ("ddof", ctypes.c_int32)]
 
 
 # name -> (restype, argtypes); mirrors include/igp.h
@@ -54,7 +54,7 @@ SIGNATURES = {
     "igp_graph_add_edges": (ctypes.c_int, [_P, _P, _i64, _P]),
     "igp_graph_info": (ctypes.c_int, [_P, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "igp_graph_status": (ctypes.c_int, [_P]),
-    "igp_graph_copy_csr": (ctypes.c_int, [_P, _P, _P, _P]),
+    "igp_graph_copy_csr": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "igp_destroy_graph": (ctypes.c_int, [_P]),
     "igp_destroy_graph_async": (ctypes.c_int, [_P, _P]),
     "igp_embed_opts_default": (None, [ctypes.POINTER(EmbedOpts)]),
@@ -65,10 +65,18 @@ SIGNATURES = {
     "igp_layer_timer_read": (ctypes.c_int, [ctypes.POINTER(_f32), ctypes.POINTER(_i64)]),
     "igp_philox_bits": (ctypes.c_int, [_u64, _u64, _i64, _P, _P]),
     "igp_philox_normal": (ctypes.c_int, [_u64, _u64, _i64, _P, _P]),
+    "igp_birch_create": (ctypes.c_int, [_i32, ctypes.c_double, _i32, ctypes.POINTER(_P)]),
+    "igp_birch_partial_fit": (ctypes.c_int, [_P, _P, _i64, _P]),
+    "igp_birch_info": (ctypes.c_int, [_P, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i64),
+                                      ctypes.POINTER(_i64)]),
+    "igp_birch_clusters": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "igp_birch_predict": (ctypes.c_int, [_P, _P, _i64, _P, _P]),
+    "igp_birch_destroy": (ctypes.c_int, [_P]),
     "igp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "igp_last_error_message": (ctypes.c_char_p, []),
     "igp_kernel_launch_count": (_u64, []),
     "igp_version": (ctypes.c_char_p, []),
+    "igp_trim_memory": (ctypes.c_int, []),
 }
 
 if not os.path.exists(LIB_PATH):
@@ -140,13 +148,15 @@ class Graph:
         """igp_graph_status: wait for the build / last merge; raises IGPError on a range error."""
         _check(_lib.igp_graph_status(self.handle))
 
-    def csr(self, stream=None):
-        """(row_ptr int32[N+1], col_idx int32[nnz]) copies on the graph's device."""
+    def csr(self, stream=None, degrees: bool = False):
+        """(row_ptr int32[N+1], col_idx int32[nnz]) copies on the graph's device; with
+        ``degrees=True`` also deg int32[N] (igp_graph_copy_csr's d_deg)."""
         rp = torch.empty(self.num_nodes + 1, dtype=torch.int32, device=self.device)
         ci = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=self.device)
+        deg = torch.empty(self.num_nodes, dtype=torch.int32, device=self.device) if degrees else None
         _check(_lib.igp_graph_copy_csr(self.handle, ctypes.c_void_p(rp.data_ptr()), ctypes.c_void_p(ci.data_ptr()),
-                                       _stream_ptr(stream)))
-        return rp, ci[: self.nnz]
+                                       ctypes.c_void_p(deg.data_ptr() if degrees else 0), _stream_ptr(stream)))
+        return (rp, ci[: self.nnz], deg) if degrees else (rp, ci[: self.nnz])
 
     def add_edges(self, edges: torch.Tensor, stream=None):
         """igp_graph_add_edges: merge new edges (CUDA int32 [E, 2]) into this graph in place."""
@@ -227,11 +237,11 @@ def layer_timer_read():
 
 def make_opts(tau: float, d: int, steps: int, seed: int = 0, *, subsequence: int = 0, theta: float = 0.1,
               alpha: float = 1.0, eps: float = 1e-3, mode: str = "full", time_layers: bool = False,
-              row_l2: bool = False, z0: torch.Tensor | None = None) -> EmbedOpts:
+              row_l2: bool = False, z0: torch.Tensor | None = None, ddof: int = 0) -> EmbedOpts:
     o = EmbedOpts()
     _lib.igp_embed_opts_default(ctypes.byref(o))
     o.tau, o.d, o.steps, o.seed, o.subsequence = float(tau), int(d), int(steps), int(seed), int(subsequence)
-    o.theta, o.alpha, o.eps, o.mode = float(theta), float(alpha), float(eps), MODES[mode]
+    o.theta, o.alpha, o.eps, o.mode, o.ddof = float(theta), float(alpha), float(eps), MODES[mode], int(ddof)
     o.flags = (FLAG_TIME_LAYERS if time_layers else 0) | (FLAG_ROW_L2 if row_l2 else 0)
     if z0 is not None:  # caller-provided Z^(0) (CUDA float32 [N, d]) instead of Theta
         _require_cuda(z0, torch.float32, "z0")
@@ -284,6 +294,79 @@ def philox_normal(seed: int, subsequence: int, count: int, device="cuda", stream
     out = torch.empty(max(count, 4), dtype=torch.float32, device=device)
     _check(_lib.igp_philox_normal(seed, subsequence, count, ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
     return out[:count]
+
+
+class Birch:
+    """BIRCH CF tree on the device (igp_birch_t; Alg. 1 l.7, Alg. 2 l.9-11): ``partial_fit``
+    inserts rows (CUDA float32 [m, d]) in order, ``predict`` labels rows by their nearest
+    cluster, ``clusters`` returns the leaf entries (K-agnostic clusters) in label order."""
+
+    def __init__(self, d: int, threshold: float = 0.5, branching: int = 50, device=None):
+        self.d = int(d)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        h = _P()
+        with torch.cuda.device(self.device):
+            _check(_lib.igp_birch_create(self.d, float(threshold), int(branching), ctypes.byref(h)))
+        self._h = h
+
+    def _rows(self, X):
+        _require_cuda(X, torch.float32, "X")
+        if X.dim() != 2 or X.shape[1] != self.d:
+            raise ValueError(f"X must have shape [m, {self.d}]")
+        return X
+
+    def partial_fit(self, X: torch.Tensor, stream=None):
+        X = self._rows(X)
+        with torch.cuda.device(self.device):
+            _check(_lib.igp_birch_partial_fit(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[0], _stream_ptr(stream)))
+        return self
+
+    fit = partial_fit
+
+    def info(self):
+        """(K clusters, depth, nodes, points)"""
+        k, dep, nodes, pts = _i64(), _i32(), _i64(), _i64()
+        with torch.cuda.device(self.device):
+            _check(_lib.igp_birch_info(self._h, ctypes.byref(k), ctypes.byref(dep), ctypes.byref(nodes),
+                                       ctypes.byref(pts)))
+        return k.value, dep.value, nodes.value, pts.value
+
+    def clusters(self, stream=None):
+        """(centroids [K, d], sqn [K], n [K], LS [K, d], SS [K]) as CUDA float64 tensors."""
+        K = self.info()[0]
+        f = dict(dtype=torch.float64, device=self.device)
+        cen, ls = torch.empty((K, self.d), **f), torch.empty((K, self.d), **f)
+        sqn, n, ss = torch.empty(K, **f), torch.empty(K, **f), torch.empty(K, **f)
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        with torch.cuda.device(self.device):
+            _check(_lib.igp_birch_clusters(self._h, ptr(cen), ptr(sqn), ptr(n), ptr(ls), ptr(ss), _stream_ptr(stream)))
+        return cen, sqn, n, ls, ss
+
+    def predict(self, X: torch.Tensor, stream=None, out: torch.Tensor | None = None) -> torch.Tensor:
+        X = self._rows(X)
+        if out is None:
+            out = torch.empty(X.shape[0], dtype=torch.int32, device=self.device)
+        _require_cuda(out, torch.int32, "out")
+        with torch.cuda.device(self.device):
+            _check(_lib.igp_birch_predict(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[0],
+                                          ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.igp_birch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def trim_memory():
+    """igp_trim_memory: return the library's cached pool memory on the current device to the driver."""
+    _check(_lib.igp_trim_memory())
 
 
 def kernel_launch_count() -> int:

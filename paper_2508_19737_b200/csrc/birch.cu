@@ -1,0 +1,874 @@
+// birch.cu — BIRCH on the GPU: the downstream clustering of InfraredGP's embeddings
+// (Alg. 1 l.7; streaming Alg. 2 l.9-11).
+//
+// The paper feeds Z~ to BIRCH (Zhang et al. 1996; scikit-learn's implementation with no
+// cluster count): a single pass of CF-tree insertions in row order, the
+// leaf entries being the K-agnostic clusters, then every row labelled by its nearest leaf
+// centroid.  Insertion is inherently sequential (each point's path depends on every earlier
+// point), so the fit runs as ONE persistent CTA that inserts the points one after another
+// with all of its 512 threads on each insertion:
+//   - the distances from x to a node's <= B + 1 entry centroids: one 8-lane group per entry,
+//     lane r accumulating k = r (mod 8) with fma, the 8 partials combined by a fixed shuffle
+//     tree -- the oracle's dot order (reading B6), so every distance is bit-identical;
+//   - first-minimum argmin over the entries (warp shuffles + one shared-memory round);
+//   - the leaf's merge test (radius^2 <= T^2) and the CF updates of the path, parallel over
+//     the d coordinates;
+//   - node splits: all pairwise entry distances (upper triangle, 8 lanes per pair), the first
+//     farthest pair, the two halves' CF sums in entry order.
+// Everything is fp64 and follows oracle/birch_oracle.c step for step (same formulas, same
+// operation order), so the tree -- and hence the clusters and labels -- are bit-identical to
+// the oracle's.  The entry and node pools live in global memory (L1/L2-resident for the top
+// levels); the fit stops cleanly before a point whose worst-case growth would overflow a pool,
+// the host doubles the pools and relaunches from that point.
+//
+// Predict (Alg. 2 l.11) is data-parallel: label_i = argmin_j sqn_j - 2 c_j . x_i over the K
+// leaf centroids (first minimum), one thread per point, cluster tiles staged in shared memory.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "igp_internal.cuh"
+
+namespace igp {
+namespace {
+
+constexpr int kFitThreads = 512;  // 64 groups of 8 lanes: one node's <= B + 1 <= 64 entries at once
+constexpr int kMaxDepth = 64;
+constexpr unsigned kFullMask = 0xffffffffu;
+constexpr int kMaxBirchD = 1024;
+constexpr int kMaxBirchBranching = 63;
+
+// tree header (device int64 words)
+enum { H_NS = 0, H_NN, H_ROOT, H_FIRST_LEAF, H_NPOINTS, H_STOP, H_DEPTH, H_WORDS };
+
+struct TreeDev {
+    int d, B;
+    double T2;
+    // entries
+    double* n;
+    double* ls;   // [cap_s][d]
+    double* ss;
+    double* cen;  // [cap_s][d]
+    double* sqn;
+    int32_t* child;
+    int64_t cap_s;
+    // nodes
+    int32_t* is_leaf;
+    int32_t* nsub;
+    int32_t* sub;  // [cap_n][B + 1]
+    int32_t* prev;
+    int32_t* next;
+    int64_t cap_n;
+    long long* hdr;
+};
+
+// full 8-way dot of a and b on the 8 lanes of the calling group (lane r = threadIdx.x & 7):
+// p_r = fma-sum over k = r (mod 8), combined ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7))
+// `mask`: the lanes of the warp that call (whole groups of 8)
+__device__ __forceinline__ double dot8(const double* a, const double* b, int d, int r, unsigned mask = kFullMask) {
+    double acc = 0.0;
+    for (int k = r; k < d; k += 8) acc = __fma_rn(a[k], b[k], acc);
+    acc = __dadd_rn(acc, __shfl_xor_sync(mask, acc, 1));
+    acc = __dadd_rn(acc, __shfl_xor_sync(mask, acc, 2));
+    acc = __dadd_rn(acc, __shfl_xor_sync(mask, acc, 4));
+    return acc;
+}
+
+struct FitShared {
+    double best_d[kFitThreads / 32];
+    int best_j[kFitThreads / 32];
+    int path_node[kMaxDepth];
+    int path_j[kMaxDepth];
+    int depth;
+    int cur;      // broadcast slot
+    int flag;
+    double scal[4];
+};
+
+// argmin over groups g < cnt of dist (held by lane r == 0 of each group); first minimum
+__device__ int block_argmin(double dist, int g, int cnt, FitShared& sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double bd = (g < cnt && (threadIdx.x & 7) == 0) ? dist : INFINITY;
+    int bj = (g < cnt && (threadIdx.x & 7) == 0) ? g : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double od = __shfl_xor_sync(kFullMask, bd, o);
+        const int oj = __shfl_xor_sync(kFullMask, bj, o);
+        if (od < bd || (od == bd && oj < bj)) {
+            bd = od;
+            bj = oj;
+        }
+    }
+    if (lane == 0) {
+        sh.best_d[warp] = bd;
+        sh.best_j[warp] = bj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = sh.best_d[0];
+        int j = sh.best_j[0];
+        for (int w = 1; w < kFitThreads / 32; ++w)
+            if (sh.best_d[w] < b || (sh.best_d[w] == b && sh.best_j[w] < j)) {
+                b = sh.best_d[w];
+                j = sh.best_j[w];
+            }
+        sh.cur = j;
+    }
+    __syncthreads();
+    const int res = sh.cur;
+    __syncthreads();
+    return res;
+}
+
+// CF_s += point x (n = 1, LS = x, SS = xx); c = LS / n, sqn = dot(c, c).  All threads.
+__device__ void cf_add_point(const TreeDev& t, int s, const double* xs, double xx) {
+    const int d = t.d;
+    const double nn = t.n[s] + 1.0;
+    for (int k = threadIdx.x; k < d; k += kFitThreads) {
+        const double l = t.ls[(int64_t)s * d + k] + xs[k];
+        t.ls[(int64_t)s * d + k] = l;
+        t.cen[(int64_t)s * d + k] = l / nn;
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        const double q = dot8(t.cen + (int64_t)s * d, t.cen + (int64_t)s * d, d, threadIdx.x, 0xffu);
+        if (threadIdx.x == 0) {
+            t.n[s] = nn;
+            t.ss[s] = t.ss[s] + xx;
+            t.sqn[s] = q;
+        }
+    }
+    __syncthreads();
+}
+
+// a new zero entry (thread 0 only; returns its index)
+__device__ int new_entry(const TreeDev& t) {
+    const int s = (int)t.hdr[H_NS]++;
+    t.n[s] = 0.0;
+    t.ss[s] = 0.0;
+    t.sqn[s] = 0.0;
+    t.child[s] = -1;
+    return s;
+}
+__device__ int new_node(const TreeDev& t, int leaf) {
+    const int v = (int)t.hdr[H_NN]++;
+    t.is_leaf[v] = leaf;
+    t.nsub[v] = 0;
+    t.prev[v] = t.next[v] = -1;
+    return v;
+}
+
+// split node v (all threads).  Returns the two halves' entries in sh.scal-free ints via out.
+__device__ void split_node(const TreeDev& t, int v, double* D, FitShared& sh, int* h_out) {
+    const int d = t.d, B1 = t.B + 1;
+    const int m = t.nsub[v];
+    const int32_t* ent = t.sub + (int64_t)v * B1;
+    const int g = threadIdx.x >> 3, r = threadIdx.x & 7;
+    // pairwise d2 for a < b (one 8-lane group per pair), mirrored; diagonal 0
+    const int P = m * (m - 1) / 2;
+    for (int p0 = 0; p0 < P; p0 += kFitThreads / 8) {
+        const int p = p0 + g;
+        int a = 0, b = 0;
+        if (p < P) {  // pair index p -> (a, b) in row-major order of the upper triangle
+            int rem = p;
+            a = 0;
+            while (rem >= m - 1 - a) {
+                rem -= m - 1 - a;
+                ++a;
+            }
+            b = a + 1 + rem;
+        }
+        const int sa = ent[a], sb = ent[b];  // (a, b) = (0, 0) past the last pair: computed, discarded
+        const double x = dot8(t.cen + (int64_t)sa * d, t.cen + (int64_t)sb * d, d, r);
+        if (p < P && r == 0) {
+            double v2 = __dadd_rn(__dadd_rn(-2.0 * x, t.sqn[sa]), t.sqn[sb]);
+            v2 = v2 > 0.0 ? v2 : 0.0;
+            D[a * m + b] = v2;
+            D[b * m + a] = v2;
+        }
+    }
+    for (int a = threadIdx.x; a < m; a += kFitThreads) D[a * m + a] = 0.0;
+    __syncthreads();
+    // first maximum in row-major order (over the upper triangle: a < b comes first)
+    {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        double bv = -1.0;
+        int bi = 0x7fffffff;
+        for (int idx = threadIdx.x; idx < m * m; idx += kFitThreads)
+            if (D[idx] > bv) {  // ascending idx per thread: keeps the first of equal maxima
+                bv = D[idx];
+                bi = idx;
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(kFullMask, bv, o);
+            const int oi = __shfl_xor_sync(kFullMask, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            sh.best_d[warp] = bv;
+            sh.best_j[warp] = bi;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double b = sh.best_d[0];
+            int j = sh.best_j[0];
+            for (int w = 1; w < kFitThreads / 32; ++w)
+                if (sh.best_d[w] > b || (sh.best_d[w] == b && sh.best_j[w] < j)) {
+                    b = sh.best_d[w];
+                    j = sh.best_j[w];
+                }
+            // the new nodes and halves (thread 0)
+            const int ia = j / m, ib = j % m;
+            const int leaf = t.is_leaf[v];
+            const int n1 = new_node(t, leaf), n2 = new_node(t, leaf);
+            const int s1 = new_entry(t), s2 = new_entry(t);
+            t.child[s1] = n1;
+            t.child[s2] = n2;
+            if (leaf) {  // n1 takes v's place in the leaf chain, n2 follows it
+                const int pv = t.prev[v], qv = t.next[v];
+                t.prev[n1] = pv;
+                t.next[n1] = n2;
+                t.prev[n2] = n1;
+                t.next[n2] = qv;
+                if (pv >= 0) t.next[pv] = n1; else t.hdr[H_FIRST_LEAF] = n1;
+                if (qv >= 0) t.prev[qv] = n2;
+            }
+            double c1 = 0.0, c2 = 0.0, q1 = 0.0, q2 = 0.0;
+            for (int i = 0; i < m; ++i) {
+                const bool to1 = (i == ia) || (D[ia * m + i] < D[ib * m + i]);
+                const int nd = to1 ? n1 : n2;
+                t.sub[(int64_t)nd * B1 + t.nsub[nd]++] = ent[i];
+                if (to1) {
+                    c1 = c1 + t.n[ent[i]];
+                    q1 = q1 + t.ss[ent[i]];
+                } else {
+                    c2 = c2 + t.n[ent[i]];
+                    q2 = q2 + t.ss[ent[i]];
+                }
+            }
+            t.n[s1] = c1;
+            t.n[s2] = c2;
+            t.ss[s1] = q1;
+            t.ss[s2] = q2;
+            sh.best_j[0] = s1;
+            sh.best_j[1] = s2;
+            sh.best_j[2] = n1;
+            sh.best_j[3] = ia;
+            sh.best_j[4] = ib;
+        }
+        __syncthreads();
+    }
+    const int s1 = sh.best_j[0], s2 = sh.best_j[1], ia = sh.best_j[3], ib = sh.best_j[4];
+    // the halves' LS in entry order, then c = LS / n
+    for (int k = threadIdx.x; k < d; k += kFitThreads) {
+        double l1 = 0.0, l2 = 0.0;
+        for (int i = 0; i < m; ++i) {
+            const bool to1 = (i == ia) || (D[ia * m + i] < D[ib * m + i]);
+            const double v2 = t.ls[(int64_t)ent[i] * d + k];
+            if (to1) l1 = l1 + v2; else l2 = l2 + v2;
+        }
+        t.ls[(int64_t)s1 * d + k] = l1;
+        t.ls[(int64_t)s2 * d + k] = l2;
+        t.cen[(int64_t)s1 * d + k] = l1 / t.n[s1];
+        t.cen[(int64_t)s2 * d + k] = l2 / t.n[s2];
+    }
+    __syncthreads();
+    if (threadIdx.x < 16) {
+        const int s = threadIdx.x < 8 ? s1 : s2;
+        const double q = dot8(t.cen + (int64_t)s * d, t.cen + (int64_t)s * d, d, threadIdx.x & 7, 0xffffu);
+        if ((threadIdx.x & 7) == 0) t.sqn[s] = q;
+    }
+    __syncthreads();
+    h_out[0] = s1;
+    h_out[1] = s2;
+    __syncthreads();
+}
+
+// Insert rows [start, m) of X in order.  One CTA.  Stops (hdr[H_STOP] = i) before a point whose
+// worst-case growth (one leaf entry, two entries and two nodes per split level, a new root)
+// could overflow a pool.
+// copy the live part of a tree (entries [0, ns), nodes [0, nn), header) between two layouts
+__device__ void copy_tree(const TreeDev& dst, const TreeDev& src, long long ns, long long nn) {
+    const int d = src.d, B1 = src.B + 1;
+    for (long long e = threadIdx.x; e < ns; e += kFitThreads) {
+        dst.n[e] = src.n[e];
+        dst.ss[e] = src.ss[e];
+        dst.sqn[e] = src.sqn[e];
+        dst.child[e] = src.child[e];
+    }
+    for (long long e = threadIdx.x; e < ns * d; e += kFitThreads) {
+        dst.ls[e] = src.ls[e];
+        dst.cen[e] = src.cen[e];
+    }
+    for (long long v = threadIdx.x; v < nn; v += kFitThreads) {
+        dst.is_leaf[v] = src.is_leaf[v];
+        dst.nsub[v] = src.nsub[v];
+        dst.prev[v] = src.prev[v];
+        dst.next[v] = src.next[v];
+    }
+    for (long long e = threadIdx.x; e < nn * B1; e += kFitThreads) dst.sub[e] = src.sub[e];
+    for (int w = threadIdx.x; w < H_WORDS; w += kFitThreads) dst.hdr[w] = src.hdr[w];
+}
+
+// Insert rows [start, m) of X in order.  One CTA.  When the whole tree (plus the growth one
+// launch may need) fits in the cap_s_sm / cap_n_sm pool carved from shared memory, the tree is
+// moved there for the launch and written back at its end (every dependent lookup of the descent
+// then costs a shared-memory access instead of an L2 round trip); otherwise it is used in place.
+__global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, const float* __restrict__ X, int64_t m,
+                                                                    int64_t start, int64_t cap_s_sm, int64_t cap_n_sm) {
+    extern __shared__ double fit_smem[];
+    __shared__ FitShared sh;
+    __shared__ int use_sm;
+    const int d = t.d, B1 = t.B + 1;
+    double* xs = fit_smem;              // [d] the point
+    double* tmp = fit_smem + d;         // [2d] merge candidate LS', c'
+    double* D = fit_smem + 3 * d;       // [(B+1)^2] split distances
+    const int g = threadIdx.x >> 3, r = threadIdx.x & 7;
+    // shared-memory pool (if it holds the tree with room for at least a few hundred inserts)
+    TreeDev T = t;
+    if (threadIdx.x == 0) {
+        const long long ns0 = t.hdr[H_NS], nn0 = t.hdr[H_NN], dep0 = t.hdr[H_DEPTH];
+        use_sm = cap_s_sm > 0 && ns0 + 64 + 2 * (dep0 + 2) <= cap_s_sm && nn0 + 2 * (dep0 + 2) + 8 <= cap_n_sm;
+    }
+    __syncthreads();
+    if (use_sm) {
+        char* p = reinterpret_cast<char*>(D + (size_t)B1 * B1);
+        T.n = reinterpret_cast<double*>(p);
+        T.ss = T.n + cap_s_sm;
+        T.sqn = T.ss + cap_s_sm;
+        T.ls = T.sqn + cap_s_sm;
+        T.cen = T.ls + cap_s_sm * d;
+        T.hdr = reinterpret_cast<long long*>(T.cen + cap_s_sm * d);
+        T.child = reinterpret_cast<int32_t*>(T.hdr + H_WORDS);
+        T.is_leaf = T.child + cap_s_sm;
+        T.nsub = T.is_leaf + cap_n_sm;
+        T.prev = T.nsub + cap_n_sm;
+        T.next = T.prev + cap_n_sm;
+        T.sub = T.next + cap_n_sm;
+        T.cap_s = cap_s_sm;
+        T.cap_n = cap_n_sm;
+        copy_tree(T, t, t.hdr[H_NS], t.hdr[H_NN]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) T.hdr[H_STOP] = m;
+    for (int64_t i = start; i < m; ++i) {
+        // capacity (all threads read the same header values)
+        __syncthreads();
+        const long long ns = T.hdr[H_NS], nn = T.hdr[H_NN], dep = T.hdr[H_DEPTH];
+        if (ns + 1 + 2 * (dep + 1) > T.cap_s || nn + 2 * (dep + 1) + 1 > T.cap_n || dep + 1 >= kMaxDepth) {
+            if (threadIdx.x == 0) T.hdr[H_STOP] = i;
+            break;
+        }
+        for (int k = threadIdx.x; k < d; k += kFitThreads) xs[k] = (double)X[i * d + k];
+        __syncthreads();
+        double xx = 0.0;
+        if (threadIdx.x < 8) xx = dot8(xs, xs, d, threadIdx.x, 0xffu);
+        if (threadIdx.x == 0) sh.scal[0] = xx;
+        __syncthreads();
+        xx = sh.scal[0];
+        const int root = (int)T.hdr[H_ROOT];
+        if (T.nsub[root] == 0) {  // the empty root leaf takes the first point
+            if (threadIdx.x == 0) sh.cur = new_entry(t);
+            __syncthreads();
+            const int s = sh.cur;
+            for (int k = threadIdx.x; k < d; k += kFitThreads) T.ls[(int64_t)s * d + k] = 0.0;
+            __syncthreads();
+            cf_add_point(T, s, xs, xx);
+            if (threadIdx.x == 0) {
+                T.sub[(int64_t)root * B1 + T.nsub[root]++] = s;
+                T.hdr[H_NPOINTS]++;
+            }
+            continue;
+        }
+        // descend: closest entry at every level
+        int depth = 0, v = root;
+        while (true) {
+            const int cnt = T.nsub[v];
+            // every group computes (groups past the node's entries on entry 0, discarded)
+            const int s = T.sub[(int64_t)v * B1 + (g < cnt ? g : 0)];
+            const double dt = dot8(T.cen + (int64_t)s * d, xs, d, r);
+            const double dist = __dadd_rn(T.sqn[s], -2.0 * dt);
+            const int j = block_argmin(dist, g, cnt, sh);
+            if (threadIdx.x == 0) {
+                sh.path_node[depth] = v;
+                sh.path_j[depth] = j;
+            }
+            ++depth;
+            if (T.is_leaf[v]) break;
+            v = T.child[T.sub[(int64_t)v * B1 + j]];
+        }
+        __syncthreads();
+        // leaf: merge into the closest entry if the merged radius^2 <= T^2, else append
+        const int leaf = v;
+        const int sj = T.sub[(int64_t)leaf * B1 + sh.path_j[depth - 1]];
+        const double nn1 = T.n[sj] + 1.0;
+        const double inv = 1.0 / nn1;
+        for (int k = threadIdx.x; k < d; k += kFitThreads) {
+            const double l = T.ls[(int64_t)sj * d + k] + xs[k];
+            tmp[k] = l;
+            tmp[d + k] = inv * l;
+        }
+        __syncthreads();
+        if (threadIdx.x < 8) {
+            const double nsq = dot8(tmp + d, tmp + d, d, threadIdx.x, 0xffu);
+            if (threadIdx.x == 0) {
+                const double nss = T.ss[sj] + xx;
+                const double r2 = nss / nn1 - nsq;
+                sh.flag = r2 <= T.T2;
+                sh.scal[1] = nsq;
+                sh.scal[2] = nss;
+            }
+        }
+        __syncthreads();
+        int split = 0;
+        if (sh.flag) {
+            for (int k = threadIdx.x; k < d; k += kFitThreads) {
+                T.ls[(int64_t)sj * d + k] = tmp[k];
+                T.cen[(int64_t)sj * d + k] = tmp[d + k];
+            }
+            if (threadIdx.x == 0) {
+                T.n[sj] = nn1;
+                T.ss[sj] = sh.scal[2];
+                T.sqn[sj] = sh.scal[1];
+            }
+            __syncthreads();
+        } else {
+            if (threadIdx.x == 0) sh.cur = new_entry(t);
+            __syncthreads();
+            const int s = sh.cur;
+            for (int k = threadIdx.x; k < d; k += kFitThreads) T.ls[(int64_t)s * d + k] = 0.0;
+            __syncthreads();
+            cf_add_point(T, s, xs, xx);
+            if (threadIdx.x == 0) T.sub[(int64_t)leaf * B1 + T.nsub[leaf]++] = s;
+            __syncthreads();
+            split = T.nsub[leaf] > T.B;
+        }
+        // back up the path: plain CF updates above the highest split, splits below it
+        for (int l = depth - 2; l >= 0; --l) {
+            const int pv = sh.path_node[l], pj = sh.path_j[l];
+            const int se = T.sub[(int64_t)pv * B1 + pj];
+            if (!split) {
+                cf_add_point(T, se, xs, xx);
+                continue;
+            }
+            int h[2];
+            split_node(T, T.child[se], D, sh, h);
+            if (threadIdx.x == 0) {
+                T.sub[(int64_t)pv * B1 + pj] = h[0];
+                T.sub[(int64_t)pv * B1 + T.nsub[pv]++] = h[1];
+            }
+            __syncthreads();
+            split = T.nsub[pv] > T.B;
+        }
+        if (split) {  // the root itself split: a new internal root holds the two halves
+            int h[2];
+            split_node(T, root, D, sh, h);
+            if (threadIdx.x == 0) {
+                const int nr = new_node(T, 0);
+                T.sub[(int64_t)nr * B1 + T.nsub[nr]++] = h[0];
+                T.sub[(int64_t)nr * B1 + T.nsub[nr]++] = h[1];
+                T.hdr[H_ROOT] = nr;
+                T.hdr[H_DEPTH] = T.hdr[H_DEPTH] + 1;
+            }
+        }
+        if (threadIdx.x == 0) T.hdr[H_NPOINTS]++;
+    }
+    if (use_sm) {
+        __syncthreads();
+        copy_tree(t, T, T.hdr[H_NS], T.hdr[H_NN]);
+    }
+}
+
+// leaf entries in leaf-chain order -> idx[K] (one thread; K = hdr-derived count)
+__global__ void birch_list_kernel(TreeDev t, int32_t* idx, long long* count) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int B1 = t.B + 1;
+    long long k = 0;
+    for (int v = (int)t.hdr[H_FIRST_LEAF]; v >= 0; v = t.next[v])
+        for (int j = 0; j < t.nsub[v]; ++j) {
+            if (idx) idx[k] = t.sub[(int64_t)v * B1 + j];
+            ++k;
+        }
+    *count = k;
+}
+
+// gather the listed entries: centroids, sqn, n, LS, SS (any output may be null)
+__global__ void birch_gather_kernel(TreeDev t, const int32_t* __restrict__ idx, int64_t K, double* cen, double* sqn,
+                                    double* n, double* ls, double* ss) {
+    const int d = t.d;
+    const int64_t total = K * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / d, k = e % d;
+        const int s = idx[j];
+        if (cen) cen[e] = t.cen[(int64_t)s * d + k];
+        if (ls) ls[e] = t.ls[(int64_t)s * d + k];
+        if (k == 0) {
+            if (sqn) sqn[j] = t.sqn[s];
+            if (n) n[j] = t.n[s];
+            if (ss) ss[j] = t.ss[s];
+        }
+    }
+}
+
+// label_i = argmin_j sqn_j - 2 dot8(c_j, x_i) (first minimum).  128 points per block (one per
+// thread), cluster tiles of kPT centroids staged in shared memory; the point's row lives in
+// shared memory too (stride d + 1).
+constexpr int kPredThreads = 128;
+constexpr int kPT = 16;
+__global__ void __launch_bounds__(kPredThreads) birch_predict_kernel(const double* __restrict__ cen,
+                                                                    const double* __restrict__ sqn, int64_t K, int d,
+                                                                    const float* __restrict__ X, int64_t m,
+                                                                    int32_t* __restrict__ labels) {
+    extern __shared__ double pred_smem[];
+    double* xs = pred_smem;                              // [128][d + 1]
+    double* cs = pred_smem + (size_t)kPredThreads * (d + 1);  // [kPT][d]
+    const int64_t i0 = (int64_t)blockIdx.x * kPredThreads;
+    for (int e = threadIdx.x; e < kPredThreads * d; e += kPredThreads) {
+        const int p = e / d, k = e % d;
+        xs[p * (d + 1) + k] = (i0 + p < m) ? (double)X[(i0 + p) * d + k] : 0.0;
+    }
+    const double* x = xs + threadIdx.x * (d + 1);
+    double best = INFINITY;
+    int64_t bj = 0;
+    for (int64_t j0 = 0; j0 < K; j0 += kPT) {
+        const int nt = (int)(K - j0 < kPT ? K - j0 : kPT);
+        __syncthreads();
+        for (int e = threadIdx.x; e < nt * d; e += kPredThreads) cs[e] = cen[j0 * d + e];
+        __syncthreads();
+        for (int jj = 0; jj < nt; ++jj) {
+            const double* c = cs + jj * d;
+            double p[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            int k = 0;
+            for (; k + 8 <= d; k += 8) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) p[q] = __fma_rn(c[k + q], x[k + q], p[q]);
+            }
+            for (; k < d; ++k) p[k & 7] = __fma_rn(c[k], x[k], p[k & 7]);
+            const double dt = __dadd_rn(__dadd_rn(__dadd_rn(p[0], p[1]), __dadd_rn(p[2], p[3])),
+                                        __dadd_rn(__dadd_rn(p[4], p[5]), __dadd_rn(p[6], p[7])));
+            const double dist = __dadd_rn(sqn[j0 + jj], -2.0 * dt);
+            if (dist < best) {  // strict: keeps the first minimum
+                best = dist;
+                bj = j0 + jj;
+            }
+        }
+    }
+    if (i0 + threadIdx.x < m) labels[i0 + threadIdx.x] = (int32_t)bj;
+}
+
+__global__ void nonfinite_kernel(const float* __restrict__ X, int64_t count, int32_t* bad) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(X[e])) *bad = 1;
+}
+
+igp_status launch_nonfinite_check(const float* X, int64_t count, int32_t* bad, cudaStream_t s) {
+    IGP_CUDA(cudaMemsetAsync(bad, 0, sizeof(int32_t), s), "memset");
+    const int grid = (int)std::min<int64_t>((count + 255) / 256, 8192);
+    nonfinite_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(X, count, bad);
+    return launch_status("nonfinite_kernel");
+}
+
+}  // namespace
+}  // namespace igp
+
+using namespace igp;
+
+// ------------------------------------------------------------------------------ host handle
+struct igp_birch_s {
+    TreeDev t{};
+    int device = 0;
+    void* pool = nullptr;
+    int64_t points = 0;
+};
+
+namespace {
+
+size_t smem_fit(int d, int B) { return sizeof(double) * ((size_t)3 * d + (size_t)(B + 1) * (B + 1)); }
+// shared-memory pool capacities (entries, nodes) that fit beside the fit kernel's scratch
+void smem_pool_caps(int d, int B, int max_optin, int64_t* cs, int64_t* cn, size_t* bytes) {
+    const size_t base = smem_fit(d, B) + 2048;  // + static shared memory
+    const size_t per_e = sizeof(double) * (2 * (size_t)d + 3) + sizeof(int32_t);
+    const size_t per_n = sizeof(int32_t) * ((size_t)B + 1 + 4);
+    *cs = *cn = 0;
+    *bytes = 0;
+    if ((size_t)max_optin <= base) return;
+    const size_t avail = (size_t)max_optin - base - sizeof(long long) * H_WORDS - 64;
+    int64_t c = (int64_t)(avail / (per_e + per_n / 4 + 1));
+    while (c > 0 && (size_t)c * per_e + (size_t)(c / 4 + 8) * per_n > avail) --c;
+    if (c < 128) return;  // too small to be worth a launch-long residency
+    *cs = c;
+    *cn = c / 4 + 8;
+    *bytes = (size_t)c * per_e + (size_t)(*cn) * per_n + sizeof(long long) * H_WORDS;
+}
+
+// (re)allocate the pools with capacities (cs entries, cn nodes), copying the first (ns, nn) rows
+igp_status grow(igp_birch_s* b, int64_t cs, int64_t cn, cudaStream_t s) {
+    const int d = b->t.d, B1 = b->t.B + 1;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    size_t off = 0;
+    const size_t o_n = off; off = al(off + 8 * (size_t)cs);
+    const size_t o_ls = off; off = al(off + 8 * (size_t)cs * d);
+    const size_t o_ss = off; off = al(off + 8 * (size_t)cs);
+    const size_t o_cen = off; off = al(off + 8 * (size_t)cs * d);
+    const size_t o_sqn = off; off = al(off + 8 * (size_t)cs);
+    const size_t o_child = off; off = al(off + 4 * (size_t)cs);
+    const size_t o_leaf = off; off = al(off + 4 * (size_t)cn);
+    const size_t o_nsub = off; off = al(off + 4 * (size_t)cn);
+    const size_t o_sub = off; off = al(off + 4 * (size_t)cn * B1);
+    const size_t o_prev = off; off = al(off + 4 * (size_t)cn);
+    const size_t o_next = off; off = al(off + 4 * (size_t)cn);
+    const size_t o_hdr = off; off = al(off + 8 * (size_t)H_WORDS);
+    char* p = nullptr;
+    IGP_CUDA(cudaMallocAsync((void**)&p, off, s), "birch pool alloc");
+    TreeDev n = b->t;
+    n.n = (double*)(p + o_n);
+    n.ls = (double*)(p + o_ls);
+    n.ss = (double*)(p + o_ss);
+    n.cen = (double*)(p + o_cen);
+    n.sqn = (double*)(p + o_sqn);
+    n.child = (int32_t*)(p + o_child);
+    n.is_leaf = (int32_t*)(p + o_leaf);
+    n.nsub = (int32_t*)(p + o_nsub);
+    n.sub = (int32_t*)(p + o_sub);
+    n.prev = (int32_t*)(p + o_prev);
+    n.next = (int32_t*)(p + o_next);
+    n.hdr = (long long*)(p + o_hdr);
+    n.cap_s = cs;
+    n.cap_n = cn;
+    if (b->pool) {
+        long long h[H_WORDS];
+        IGP_CUDA(cudaMemcpyAsync(h, b->t.hdr, sizeof(h), cudaMemcpyDeviceToHost, s), "birch header");
+        IGP_CUDA(cudaStreamSynchronize(s), "birch sync");
+        const int64_t ns = h[H_NS], nn = h[H_NN];
+        const TreeDev& o = b->t;
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s) : cudaSuccess;
+        };
+        cudaError_t e = cudaSuccess;
+        if (e == cudaSuccess) e = cp(n.n, o.n, 8 * ns);
+        if (e == cudaSuccess) e = cp(n.ls, o.ls, 8 * ns * d);
+        if (e == cudaSuccess) e = cp(n.ss, o.ss, 8 * ns);
+        if (e == cudaSuccess) e = cp(n.cen, o.cen, 8 * ns * d);
+        if (e == cudaSuccess) e = cp(n.sqn, o.sqn, 8 * ns);
+        if (e == cudaSuccess) e = cp(n.child, o.child, 4 * ns);
+        if (e == cudaSuccess) e = cp(n.is_leaf, o.is_leaf, 4 * nn);
+        if (e == cudaSuccess) e = cp(n.nsub, o.nsub, 4 * nn);
+        if (e == cudaSuccess) e = cp(n.sub, o.sub, 4 * nn * B1);
+        if (e == cudaSuccess) e = cp(n.prev, o.prev, 4 * nn);
+        if (e == cudaSuccess) e = cp(n.next, o.next, 4 * nn);
+        if (e == cudaSuccess) e = cp(n.hdr, o.hdr, sizeof(h));
+        if (e != cudaSuccess) {
+            cudaFreeAsync(p, s);
+            return cuda_status(e, "birch pool copy");
+        }
+        cudaFreeAsync(b->pool, s);
+    }
+    b->pool = p;
+    b->t = n;
+    return IGP_OK;
+}
+
+igp_status read_hdr(igp_birch_s* b, long long* h, cudaStream_t s) {
+    IGP_CUDA(cudaMemcpyAsync(h, b->t.hdr, sizeof(long long) * H_WORDS, cudaMemcpyDeviceToHost, s), "birch header");
+    IGP_CUDA(cudaStreamSynchronize(s), "birch sync");
+    return IGP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+igp_status igp_birch_create(int32_t d, double threshold, int32_t branching, igp_birch_t* out) {
+    set_error("");
+    if (!out) {
+        set_error("out handle pointer is NULL");
+        return IGP_ERR_INPUT;
+    }
+    *out = nullptr;
+    if (d < 1 || d > kMaxBirchD || !(threshold > 0.0) || !std::isfinite(threshold) || branching < 2 ||
+        branching > kMaxBirchBranching) {
+        set_error("birch: need 1 <= d <= 1024, finite threshold > 0, 2 <= branching <= 63");
+        return IGP_ERR_INPUT;
+    }
+    DeviceInfo di;
+    if (!device_info(&di)) return IGP_ERR_CUDA;
+    igp_birch_s* b = new (std::nothrow) igp_birch_s();
+    if (!b) return IGP_ERR_OOM;
+    b->device = di.device;
+    b->t.d = d;
+    b->t.B = branching;
+    b->t.T2 = threshold * threshold;
+    cudaStream_t s = 0;
+    igp_status st = grow(b, 1024, 256, s);
+    if (st == IGP_OK) {
+        // header: ns 0, nn 1 (the empty root leaf 0), root 0, first leaf 0, depth 1
+        long long h[H_WORDS] = {0, 1, 0, 0, 0, 0, 1};
+        int32_t root[3] = {1, 0, -1};  // is_leaf, nsub, prev/next
+        st = cuda_status(cudaMemcpyAsync(b->t.hdr, h, sizeof(h), cudaMemcpyHostToDevice, s), "birch init");
+        if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(b->t.is_leaf, &root[0], 4, cudaMemcpyHostToDevice, s), "init");
+        if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(b->t.nsub, &root[1], 4, cudaMemcpyHostToDevice, s), "init");
+        if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(b->t.prev, &root[2], 4, cudaMemcpyHostToDevice, s), "init");
+        if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(b->t.next, &root[2], 4, cudaMemcpyHostToDevice, s), "init");
+        if (st == IGP_OK) st = cuda_status(cudaStreamSynchronize(s), "birch sync");
+    }
+    if (st != IGP_OK) {
+        if (b->pool) cudaFree(b->pool);
+        delete b;
+        return st;
+    }
+    *out = b;
+    return IGP_OK;
+}
+
+igp_status igp_birch_partial_fit(igp_birch_t b, const float* d_X, int64_t m, igp_stream_t stream) {
+    set_error("");
+    if (!b || m < 0 || (m > 0 && !d_X)) {
+        set_error("birch handle or rows invalid");
+        return IGP_ERR_INPUT;
+    }
+    if (m == 0) return IGP_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int d = b->t.d;
+    // non-finite rows are an input error: checked on the device before any insert
+    int32_t* bad = nullptr;
+    IGP_CUDA(cudaMallocAsync((void**)&bad, sizeof(int32_t), s), "alloc");
+    igp_status st = launch_nonfinite_check(d_X, m * (int64_t)d, bad, s);
+    int32_t hbad = 0;
+    if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s), "readback");
+    if (st == IGP_OK) st = cuda_status(cudaStreamSynchronize(s), "sync");
+    cudaFreeAsync(bad, s);
+    if (st != IGP_OK) return st;
+    if (hbad) {
+        set_error("birch: non-finite value in the rows");
+        return IGP_ERR_INPUT;
+    }
+    DeviceInfo di;
+    if (!device_info(&di)) return IGP_ERR_CUDA;
+    int64_t cs_sm = 0, cn_sm = 0;
+    size_t pool_bytes = 0;
+    smem_pool_caps(d, b->t.B, di.max_smem_optin, &cs_sm, &cn_sm, &pool_bytes);
+    // never more than the global pools hold (the tree is written back into them)
+    if (cs_sm > b->t.cap_s || cn_sm > b->t.cap_n) cs_sm = cn_sm = 0;
+    const size_t smem = smem_fit(d, b->t.B) + (cs_sm ? pool_bytes : 0);
+    IGP_CUDA(cudaFuncSetAttribute(birch_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+             "birch smem attribute");
+    int64_t start = 0;
+    while (start < m) {
+        birch_fit_kernel<<<1, kFitThreads, smem, s>>>(b->t, d_X, m, start, cs_sm, cn_sm);
+        IGP_TRY(launch_status("birch_fit_kernel"));
+        long long h[H_WORDS];
+        IGP_TRY(read_hdr(b, h, s));
+        start = h[H_STOP];
+        if (start < m) {  // a pool would overflow: double both and continue from row `start`
+            IGP_TRY(grow(b, 2 * b->t.cap_s + (int64_t)2 * (h[H_DEPTH] + 2), 2 * b->t.cap_n + 2 * (h[H_DEPTH] + 2), s));
+        }
+    }
+    b->points += m;
+    return IGP_OK;
+}
+
+igp_status igp_birch_info(igp_birch_t b, int64_t* num_clusters, int32_t* depth, int64_t* nodes, int64_t* points) {
+    set_error("");
+    if (!b) {
+        set_error("birch handle is NULL");
+        return IGP_ERR_INPUT;
+    }
+    cudaStream_t s = 0;
+    long long* cnt = nullptr;
+    IGP_CUDA(cudaMallocAsync((void**)&cnt, sizeof(long long), s), "alloc");
+    birch_list_kernel<<<1, 32, 0, s>>>(b->t, nullptr, cnt);
+    igp_status st = launch_status("birch_list_kernel");
+    long long k = 0, h[H_WORDS] = {0};
+    if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(&k, cnt, sizeof(k), cudaMemcpyDeviceToHost, s), "readback");
+    if (st == IGP_OK) st = read_hdr(b, h, s);
+    cudaFreeAsync(cnt, s);
+    if (st != IGP_OK) return st;
+    if (num_clusters) *num_clusters = k;
+    if (depth) *depth = (int32_t)h[H_DEPTH];
+    if (nodes) *nodes = h[H_NN];
+    if (points) *points = h[H_NPOINTS];
+    return IGP_OK;
+}
+
+igp_status igp_birch_clusters(igp_birch_t b, double* d_centroids, double* d_sqn, double* d_n, double* d_ls,
+                              double* d_ss, igp_stream_t stream) {
+    set_error("");
+    if (!b) {
+        set_error("birch handle is NULL");
+        return IGP_ERR_INPUT;
+    }
+    int64_t K = 0;
+    IGP_TRY(igp_birch_info(b, &K, nullptr, nullptr, nullptr));
+    if (K == 0) return IGP_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int32_t* idx = nullptr;
+    long long* cnt = nullptr;
+    IGP_CUDA(cudaMallocAsync((void**)&idx, 4 * (size_t)K, s), "alloc");
+    IGP_CUDA(cudaMallocAsync((void**)&cnt, sizeof(long long), s), "alloc");
+    birch_list_kernel<<<1, 32, 0, s>>>(b->t, idx, cnt);
+    igp_status st = launch_status("birch_list_kernel");
+    if (st == IGP_OK) {
+        const int grid = (int)std::min<int64_t>((K * b->t.d + 255) / 256, 4096);
+        birch_gather_kernel<<<grid, 256, 0, s>>>(b->t, idx, K, d_centroids, d_sqn, d_n, d_ls, d_ss);
+        st = launch_status("birch_gather_kernel");
+    }
+    cudaFreeAsync(idx, s);
+    cudaFreeAsync(cnt, s);
+    return st;
+}
+
+igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m, int32_t* d_labels, igp_stream_t stream) {
+    set_error("");
+    if (!b || m < 0 || (m > 0 && (!d_X || !d_labels))) {
+        set_error("birch handle or buffers invalid");
+        return IGP_ERR_INPUT;
+    }
+    int64_t K = 0;
+    IGP_TRY(igp_birch_info(b, &K, nullptr, nullptr, nullptr));
+    if (K == 0) {
+        set_error("birch: predict on an empty tree");
+        return IGP_ERR_INPUT;
+    }
+    if (m == 0) return IGP_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int d = b->t.d;
+    double* cen = nullptr;
+    double* sqn = nullptr;
+    IGP_CUDA(cudaMallocAsync((void**)&cen, 8 * (size_t)K * d, s), "alloc");
+    IGP_CUDA(cudaMallocAsync((void**)&sqn, 8 * (size_t)K, s), "alloc");
+    igp_status st = igp_birch_clusters(b, cen, sqn, nullptr, nullptr, nullptr, stream);
+    if (st == IGP_OK) {
+        const size_t smem = sizeof(double) * ((size_t)kPredThreads * (d + 1) + (size_t)kPT * d);
+        st = cuda_status(cudaFuncSetAttribute(birch_predict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem),
+                         "predict smem attribute");
+        if (st == IGP_OK) {
+            const int64_t grid = (m + kPredThreads - 1) / kPredThreads;
+            birch_predict_kernel<<<(unsigned)grid, kPredThreads, smem, s>>>(cen, sqn, K, d, d_X, m, d_labels);
+            st = launch_status("birch_predict_kernel");
+        }
+    }
+    cudaFreeAsync(cen, s);
+    cudaFreeAsync(sqn, s);
+    return st;
+}
+
+igp_status igp_birch_destroy(igp_birch_t b) {
+    if (!b) return IGP_OK;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != b->device) cudaSetDevice(b->device);
+    cudaStreamSynchronize(0);
+    if (b->pool) cudaFree(b->pool);
+    if (prev >= 0 && prev != b->device) cudaSetDevice(prev);
+    delete b;
+    return IGP_OK;
+}
+
+}  // extern "C"

@@ -505,6 +505,20 @@ int grid_for(int64_t work, int threads, int num_sms, int per_sm) {
 
 }  // namespace
 
+namespace {
+__global__ void degrees_kernel(const int32_t* __restrict__ rp, int32_t n, int32_t* __restrict__ deg) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) deg[i] = rp[i + 1] - rp[i];
+}
+}  // namespace
+
+igp_status launch_degrees(const int32_t* rp, int32_t n, int32_t* deg, cudaStream_t s) {
+    DeviceInfo di;
+    if (!device_info(&di)) return IGP_ERR_CUDA;
+    degrees_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(rp, n, deg);
+    return launch_status("degrees_kernel");
+}
+
 igp_status scan_exclusive(const int32_t* in, int32_t* out, int32_t n, cudaStream_t s) {
     const int32_t nb = (n + kScanTile - 1) / kScanTile;
     int32_t* bsum = nullptr;
@@ -617,20 +631,36 @@ igp_status stable_sort_pairs(int32_t n, int key_bits, const PairSortScratch& sc,
 
 }  // namespace
 
-// merge support: row counts start at the base graph's degrees, and the base rows are
-// copied into the front of each bucket before the new edges are scattered behind them
-__global__ void base_degree_kernel(const int32_t* __restrict__ rp, int32_t n, int32_t* __restrict__ cnt) {
+// Streaming merge (Alg. 2 l.1): row r of the union = the sorted, duplicate-free
+// merge of the base graph's canonical row (sorted, unique) and the new edges' row (sorted and
+// deduplicated on their own first).  One thread per row, two-pointer merge; a counting pass
+// sizes the rows, a writing pass fills the final CSR directly.
+template <bool WRITE>
+__global__ void merge_rows_kernel(const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                                  const int32_t* __restrict__ noff, const int32_t* __restrict__ ndata,
+                                  const int32_t* __restrict__ ncnt, int32_t n, int32_t* __restrict__ ucnt,
+                                  const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) cnt[i] = rp[i + 1] - rp[i];
-}
-
-__global__ void base_copy_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, int32_t n,
-                                 const int32_t* __restrict__ off, int32_t* __restrict__ tmp) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
-        const int32_t src = rp[r], len = rp[r + 1] - src, dst = off[r];
-        for (int32_t k = lane; k < len; k += 32) tmp[dst + k] = ci[src + k];
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += stride) {
+        int32_t i = brp[r];
+        const int32_t i1 = brp[r + 1];
+        int32_t j = noff[r];
+        const int32_t j1 = j + ncnt[r];
+        int32_t k = WRITE ? row_ptr[r] : 0;
+        const int32_t k0 = k;
+        while (i < i1 && j < j1) {
+            const int32_t x = bci[i], y = ndata[j];
+            const int32_t v = x < y ? x : y;
+            i += x <= y;
+            j += y <= x;
+            if (WRITE) col_idx[k] = v;
+            ++k;
+        }
+        for (; i < i1; ++i, ++k)
+            if (WRITE) col_idx[k] = bci[i];
+        for (; j < j1; ++j, ++k)
+            if (WRITE) col_idx[k] = ndata[j];
+        if (!WRITE) ucnt[r] = k - k0;
     }
 }
 
@@ -683,6 +713,7 @@ void free_csr(const CsrDevice& c, cudaStream_t s) {
     free_async(c.col_idx, s);
     free_async(c.order, s);
     free_async(c.meta, s);
+    free_async(c.labels, s);
     if (!c.perm_alias) {
         free_async(c.rp_perm, s);
         free_async(c.col_perm, s);
@@ -759,6 +790,8 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     if (st == IGP_OK && reorder)
         st = cuda_status(alloc_async((void**)&c.rp_perm, sizeof(int32_t) * ((size_t)n + 1 + kRpPad), s), "alloc");
     if (st == IGP_OK && reorder) st = cuda_status(alloc_async((void**)&c.col_perm, cbytes, s), "col_perm alloc");
+    if (st == IGP_OK && community)
+        st = cuda_status(alloc_async((void**)&c.labels, sizeof(int32_t) * (size_t)n, s), "labels alloc");
     if (!reorder) c.perm_alias = true;
     cudaEvent_t ev_csr = nullptr, ev_lp = nullptr;  // community order: side-stream fork / join
     auto fail = [&](igp_status e) {
@@ -784,13 +817,8 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         IGP_STEP(cuda_status(cudaMemsetAsync(c.meta, 0, 4 * sizeof(int32_t), s), "memset"));
     IGP_STEP(cuda_status(cudaMemsetAsync(c.col_idx + raw, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
     if (reorder) IGP_STEP(cuda_status(cudaMemsetAsync(c.col_perm + raw, 0, sizeof(int32_t) * kColPad, s), "pad memset"));
-    // B1-B3: count, scan, scatter both orientations into row buckets (behind the base rows)
-    if (base) {
-        base_degree_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(base->row_ptr, n, cnt);
-        IGP_STEP(launch_status("base_degree_kernel"));
-    } else {
-        IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
-    }
+    // B1-B3: count, scan, scatter both orientations of the NEW edges into row buckets
+    IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
     const int eg = grid_for(E, 256, di.num_sms, 16);
     if (E > 0) {
         count_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, cnt, c.meta);
@@ -799,24 +827,31 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     IGP_STEP(scan_exclusive(cnt, off, n, s));
     IGP_STEP(cuda_status(cudaMemsetAsync(c.row_ptr + n + 1, 0, kRpPad * sizeof(int32_t), s), "pad memset"));
     const int rg = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
-    if (base) {
-        base_copy_kernel<<<rg, 256, 0, s>>>(base->row_ptr, base->col_idx, n, off, tmp);
-        IGP_STEP(launch_status("base_copy_kernel"));
-        base_degree_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(base->row_ptr, n, cnt);
-        IGP_STEP(launch_status("base_degree_kernel"));
-    } else if (E > 0) {
-        IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
-    }
     if (E > 0) {
+        IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
         scatter_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, off, cnt, tmp);
         IGP_STEP(launch_status("scatter_kernel"));
     }
-    // B4-B5: per-row sort + dedup, row pointers, compaction
-    IGP_STEP(segmented_sort(off, tmp, ucnt, n, raw, n, sc, s, di));
-    IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
-    if (raw > 0) {
-        compact_kernel<<<rg, 256, 0, s>>>(off, tmp, c.row_ptr, c.col_idx, n);
-        IGP_STEP(launch_status("compact_kernel"));
+    // B4: per-row sort + dedup of the new entries
+    IGP_STEP(segmented_sort(off, tmp, base ? cnt : ucnt, n, 2 * E, n, sc, s, di));
+    if (base) {
+        // streaming merge: the base rows are already canonical; merge each with its sorted new
+        // run (no re-sort of the base), counting first, then writing the final rows
+        const int tg = grid_for(n, 256, di.num_sms, 8);
+        merge_rows_kernel<false><<<tg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, ucnt, nullptr,
+                                                    nullptr);
+        IGP_STEP(launch_status("merge_rows_kernel<count>"));
+        IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
+        merge_rows_kernel<true><<<tg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, nullptr,
+                                                   c.row_ptr, c.col_idx);
+        IGP_STEP(launch_status("merge_rows_kernel<write>"));
+    } else {
+        // B5: row pointers, compaction
+        IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
+        if (raw > 0) {
+            compact_kernel<<<rg, 256, 0, s>>>(off, tmp, c.row_ptr, c.col_idx, n);
+            IGP_STEP(launch_status("compact_kernel"));
+        }
     }
     if (!reorder) {  // the filter steps run on the canonical CSR itself
         iota_kernel<<<grid_for(n, 256, di.num_sms, 8), 256, 0, s>>>(c.order, n);  // identity labelling
@@ -842,11 +877,22 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         IGP_STEP(cuda_status(cudaEventRecord(ev_csr, s), "event record"));
         IGP_STEP(cuda_status(cudaStreamWaitEvent(ss, ev_csr, 0), "stream wait"));
         const int ng = grid_for(n, 256, di.num_sms, 8);
-        // sweep 1 from the identity labels in closed form: every label counts once, so the tie rule
-        // picks the smallest of {i} and the first <= 31 neighbours, i.e. min(i, first neighbour)
-        lp_first_sweep_kernel<<<ng, 256, 0, ss>>>(c.row_ptr, c.col_idx, n, lab0);
-        igp_status lst = launch_status("lp_first_sweep_kernel");
-        for (int it = 1; it < kLabelPropIters && lst == IGP_OK; ++it) {
+        igp_status lst = IGP_OK;
+        int sweeps = kLabelPropIters;
+        if (base && base->labels) {
+            // streaming merge: warm start from the previous graph's communities (the new edges
+            // only move labels locally), a few sweeps instead of a full propagation
+            lst = cuda_status(cudaMemcpyAsync(lab0, base->labels, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice,
+                                              ss),
+                              "labels copy");
+            sweeps = kLabelPropWarmIters + 1;
+        } else {
+            // sweep 1 from the identity labels in closed form: every label counts once, so the tie rule
+            // picks the smallest of {i} and the first <= 31 neighbours, i.e. min(i, first neighbour)
+            lp_first_sweep_kernel<<<ng, 256, 0, ss>>>(c.row_ptr, c.col_idx, n, lab0);
+            lst = launch_status("lp_first_sweep_kernel");
+        }
+        for (int it = 1; it < sweeps && lst == IGP_OK; ++it) {
             label_prop_kernel<<<grid_for((int64_t)n * 32, 256, di.num_sms, 8), 256, 0, ss>>>(c.row_ptr, c.col_idx, n,
                                                                                              lab0, lab1);
             lst = launch_status("label_prop_kernel");
@@ -854,6 +900,9 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
             lab0 = lab1;
             lab1 = t;
         }
+        if (lst == IGP_OK)  // kept with the graph: the next merge's warm start
+            lst = cuda_status(cudaMemcpyAsync(c.labels, lab0, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, ss),
+                              "labels copy");
         if (lst == IGP_OK) lst = cuda_status(cudaEventRecord(lp, ss), "event record");
         if (lst != IGP_OK) {  // drain what was enqueued on the side stream before freeing anything
             cudaStreamSynchronize(ss);

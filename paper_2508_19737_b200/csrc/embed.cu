@@ -138,17 +138,21 @@ struct LayerArgs {
     int32_t n;
     float theta, alpha;
     int linear;
+    int ddof;       // ZNorm std: 0 population (reading A2), 1 sample
     double grid_c;  // 1.5 * 2^(52-g): (x + grid_c) - grid_c rounds x to the 2^-g grid
     float idx_ef;   // fraction of index-stream loads marked L2 evict_first
     float st_ef;    // fraction of output stores marked L2 evict_first
 };
 
-// (mu, 1/sigma) of column c from exact sums; population std (reading A2), floor 1e-8 -> 0 (A3)
-__device__ __forceinline__ void column_stats(const double* sums, int c, int W, int32_t n, double& mu, double& isg) {
+// (mu, 1/sigma) of column c from exact sums; std with ddof (0 = population, reading A2; the
+// sample std for ddof = 1), floor 1e-8 -> 0 (A3); N <= ddof counts as a zero std
+__device__ __forceinline__ void column_stats(const double* sums, int c, int W, int32_t n, int ddof, double& mu,
+                                             double& isg) {
     const double invN = 1.0 / (double)n;
     const double m = sums[c] * invN;
     double var = sums[W + c] * invN - m * m;
     var = var > 0.0 ? var : 0.0;
+    if (ddof != 0) var = n > ddof ? var * ((double)n / (double)(n - ddof)) : 0.0;
     const double sd = sqrt(var);
     mu = m;
     isg = sd < 1e-8 ? 0.0 : 1.0 / sd;
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int c = threadIdx.x; c < W; c += kThreads) {
         double m = 0.0, is = 1.0;
-        if (p.sums_in) column_stats(p.sums_in, c, W, p.n, m, is);
+        if (p.sums_in) column_stats(p.sums_in, c, W, p.n, p.ddof, m, is);
         st[c + c / 8] = make_double2(m, is);  // one pad slot per 8 columns: the 8-column groups of the
                                               // lanes of a row start in distinct banks
     }
@@ -506,7 +510,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
 template <int W>
 __global__ void output_kernel(const float4* __restrict__ y, const float2* __restrict__ sr,
                               const double* __restrict__ sums, const int32_t* __restrict__ order, int32_t n, int d,
-                              int col0, int mode, float* __restrict__ out) {
+                              int col0, int mode, int ddof, float* __restrict__ out) {
     constexpr int LPR = W / 4;
     const int64_t total = (int64_t)n * LPR;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -523,7 +527,7 @@ __global__ void output_kernel(const float4* __restrict__ y, const float2* __rest
                 a[k] = t;
             } else {
                 double mu = 0.0, isg = 1.0;
-                if (sums) column_stats(sums, 4 * q + k, W, n, mu, isg);
+                if (sums) column_stats(sums, 4 * q + k, W, n, ddof, mu, isg);
                 const float z = (float)(((double)t - mu) * isg);
                 a[k] = (mode == IGP_MODE_FULL) ? 1.0f / (1.0f + expf(-z)) : z;
             }
@@ -720,6 +724,7 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 a.theta = o.theta;
                 a.alpha = o.alpha;
                 a.linear = linear;
+                a.ddof = o.ddof;
                 a.grid_c = grid_c;
                 a.idx_ef = idx_ef;
                 a.st_ef = st_ef;
@@ -742,7 +747,7 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
             if (ts) cudaEventRecord(ts->ev1, s);
             const double* sfin = (linear || L == 0) ? nullptr : sk + (size_t)L * 2 * W;
             output_kernel<W><<<simple_grid((int64_t)n * (W / 4), 256, di), 256, 0, s>>>(ybuf[L & 1], sr, sfin, g.order, n,
-                                                                                        d, col0, o.mode, out);
+                                                                                        d, col0, o.mode, o.ddof, out);
             if ((rc = launch_status("output_kernel")) != IGP_OK) break;
             if (hc && !(o.flags & IGP_FLAG_ROW_L2)) {  // this slice's columns are final: copy them
                                                           // out behind the remaining slices

@@ -45,20 +45,53 @@ bool device_info(DeviceInfo* out) {
         n.max_smem_optin = v;
         cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
         n.l2_bytes = (size_t)v;
-        // keep freed stream-ordered memory in the default pool (repeated embeds reuse it)
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
         di = n;
     }
     *out = di;
     return true;
 }
 
+// the library's private stream-ordered pool of a device: freed blocks stay cached for the next
+// build / embed (release threshold raised on THIS pool only; the device's default pool and other
+// allocators in the process are untouched); igp_trim_memory returns them to the driver
+static cudaMemPool_t library_pool(int dev) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    cudaMemPool_t& p = pools[dev & 63];
+    if (!p) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+            p = nullptr;
+            return nullptr;
+        }
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return p;
+}
+
 cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s) {
-    return cudaMallocAsync(p, bytes > 0 ? bytes : 16, s);
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaMemPool_t pool = library_pool(dev);
+    if (!pool) return cudaErrorMemoryAllocation;
+    return cudaMallocFromPoolAsync(p, bytes > 0 ? bytes : 16, pool, s);
+}
+
+cudaError_t trim_pool() {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaMemPool_t pool = library_pool(dev);
+    if (!pool) return cudaErrorMemoryAllocation;
+    e = cudaDeviceSynchronize();
+    return e != cudaSuccess ? e : cudaMemPoolTrimTo(pool, 0);
 }
 
 void free_async(void* p, cudaStream_t s) {
@@ -188,10 +221,34 @@ static igp_status check_opts(const igp_embed_opts* o) {
         set_error("unknown mode");
         return IGP_ERR_INPUT;
     }
+    if (o->ddof < 0 || o->ddof > 1) {
+        set_error("ddof must be 0 (population std) or 1 (sample std)");
+        return IGP_ERR_INPUT;
+    }
+    if ((reinterpret_cast<uintptr_t>(o->d_z0) & 15) != 0) {
+        set_error("opts.d_z0 must be 16-byte aligned");
+        return IGP_ERR_INPUT;
+    }
     if (o->d < 16 || o->d > kMaxD || o->d % 16 != 0) {
         set_error("d must be a multiple of 16 in [16, 1024]");
         return IGP_ERR_UNSUPPORTED;
     }
+    return IGP_OK;
+}
+
+// remember that `s` uses g (an event recorded behind the work just enqueued on s)
+static igp_status note_use(igp_graph_s* g, cudaStream_t s) {
+    std::lock_guard<std::mutex> lock(g->use_mu);
+    for (auto& u : g->uses)
+        if (u.stream == s) return cuda_status(cudaEventRecord(u.ev, s), "event record");
+    igp_graph_s::Use u{s, nullptr};
+    IGP_CUDA(cudaEventCreateWithFlags(&u.ev, cudaEventDisableTiming), "event");
+    igp_status st = cuda_status(cudaEventRecord(u.ev, s), "event record");
+    if (st != IGP_OK) {
+        cudaEventDestroy(u.ev);
+        return st;
+    }
+    g->uses.push_back(u);
     return IGP_OK;
 }
 
@@ -248,8 +305,8 @@ igp_status igp_build_graph_ex(const int32_t* d_edges, int64_t num_edges, int32_t
         set_error("2*num_edges exceeds the int32 CSR index range");
         return IGP_ERR_UNSUPPORTED;
     }
-    if (num_nodes > kMaxEntries) {  // row_ptr[N] and the row loops stay inside int32 with headroom
-        set_error("num_nodes exceeds INT32_MAX - 64");
+    if (num_nodes > kMaxNodes) {  // the builder's int32 scans / digit histograms cover ~2N entries
+        set_error("num_nodes exceeds 2^30 - 4096");
         return IGP_ERR_UNSUPPORTED;
     }
     igp_graph_s* g = new (std::nothrow) igp_graph_s();
@@ -357,7 +414,8 @@ igp_status igp_graph_info(igp_graph_t g, int32_t* num_nodes, int64_t* nnz, int64
     return IGP_OK;
 }
 
-igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t* d_col_idx, igp_stream_t stream) {
+igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t* d_col_idx, int32_t* d_deg,
+                              igp_stream_t stream) {
     if (!g || !d_row_ptr) {
         set_error("graph or output pointer is NULL");
         return IGP_ERR_INPUT;
@@ -375,12 +433,14 @@ igp_status igp_graph_copy_csr(igp_graph_t g, int32_t* d_row_ptr, int32_t* d_col_
         IGP_CUDA(cudaMemcpyAsync(d_col_idx, g->csr.col_idx, sizeof(int32_t) * (size_t)g->nnz,
                                  cudaMemcpyDeviceToDevice, s),
                  "copy col_idx");
+    if (d_deg) IGP_TRY(launch_degrees(g->csr.row_ptr, g->csr.n, d_deg, s));
     return IGP_OK;
 }
 
 static void release_graph(igp_graph_t g, cudaStream_t s) {
     free_csr(g->csr, s);
     if (g->ready) cudaEventDestroy(g->ready);  // deferred by the runtime until the event completes
+    for (auto& u : g->uses) cudaEventDestroy(u.ev);
     delete g;
 }
 
@@ -389,19 +449,32 @@ igp_status igp_destroy_graph(igp_graph_t g) {
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != g->device) cudaSetDevice(g->device);
-    cudaDeviceSynchronize();  // no stream may still read the CSR
-    release_graph(g, (cudaStream_t)0);
-    if (prev >= 0) cudaSetDevice(prev);
-    return IGP_OK;
+    // wait for the graph's own build / merges and embeds only (not the whole device), then
+    // release in stream order on the library's private status stream
+    igp_status st = cuda_status(cudaEventSynchronize(g->ready), "graph build");
+    {
+        std::lock_guard<std::mutex> lock(g->use_mu);
+        for (auto& u : g->uses)
+            if (st == IGP_OK) st = cuda_status(cudaEventSynchronize(u.ev), "graph use");
+    }
+    release_graph(g, status_stream(g->device));
+    if (prev >= 0 && prev != g->device) cudaSetDevice(prev);
+    return st;
 }
 
 igp_status igp_destroy_graph_async(igp_graph_t g, igp_stream_t stream) {
     if (!g) return IGP_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    cudaStreamWaitEvent(s, g->ready, 0);  // never free under an unfinished build / merge
+    cudaStreamWaitEvent(s, g->ready, 0);  // never free under an unfinished build / merge ...
+    {
+        std::lock_guard<std::mutex> lock(g->use_mu);
+        for (auto& u : g->uses) cudaStreamWaitEvent(s, u.ev, 0);  // ... or an embed on another stream
+    }
     release_graph(g, s);
     return IGP_OK;
 }
+
+igp_status igp_trim_memory(void) { return cuda_status(trim_pool(), "trim memory"); }
 
 void igp_embed_opts_default(igp_embed_opts* o) {
     if (!o) return;
@@ -410,6 +483,7 @@ void igp_embed_opts_default(igp_embed_opts* o) {
     o->alpha = 1.0f;
     o->eps = 1e-3f;
     o->mode = IGP_MODE_FULL;
+    o->ddof = 0;     // population std (reading A2)
 }
 
 igp_status igp_embed_ex(igp_graph_t g, const igp_embed_opts* opts, float* d_out, igp_stream_t stream) {
@@ -419,10 +493,16 @@ igp_status igp_embed_ex(igp_graph_t g, const igp_embed_opts* opts, float* d_out,
         return IGP_ERR_INPUT;
     }
     IGP_TRY(check_opts(opts));
+    if ((reinterpret_cast<uintptr_t>(d_out) & 15) != 0) {
+        set_error("d_out must be 16-byte aligned");
+        return IGP_ERR_INPUT;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     // order the embed behind the build / merge (a no-op wait when it is on the same stream)
     IGP_CUDA(cudaStreamWaitEvent(s, g->ready, 0), "stream wait");
-    return run_embed(g->csr, *opts, d_out, s);
+    igp_status st = run_embed(g->csr, *opts, d_out, s);
+    igp_status su = note_use(g, s);  // igp_destroy_graph waits for this embed (even after an error)
+    return st != IGP_OK ? st : su;
 }
 
 igp_status igp_embed(igp_graph_t g, float tau, int32_t d, int32_t steps, uint64_t seed, float* d_out,
@@ -479,12 +559,16 @@ igp_status igp_embed_host(const int32_t* h_edges, int64_t num_edges, int32_t num
     const size_t eb = sizeof(int32_t) * 2 * (size_t)num_edges;
     const size_t ob = sizeof(float) * (size_t)num_nodes * (size_t)opts->d;
     IGP_CUDA(alloc_async((void**)&d_edges, eb, s), "edges alloc");
-    if (eb) IGP_CUDA(cudaMemcpyAsync(d_edges, h_edges, eb, cudaMemcpyHostToDevice, s), "edges H2D");
+    igp_status st = eb ? cuda_status(cudaMemcpyAsync(d_edges, h_edges, eb, cudaMemcpyHostToDevice, s), "edges H2D")
+                       : IGP_OK;
     // everything is enqueued before the single wait at the end
     igp_graph_t g = nullptr;
-    igp_status st = igp_build_graph_ex(d_edges, num_edges, num_nodes, IGP_BUILD_ASYNC, stream, &g);
-    free_async(d_edges, s);
-    if (st != IGP_OK) return st;
+    if (st == IGP_OK) st = igp_build_graph_ex(d_edges, num_edges, num_nodes, IGP_BUILD_ASYNC, stream, &g);
+    free_async(d_edges, s);  // stream-ordered: after the build that reads it (or the failed copy)
+    if (st != IGP_OK) {
+        cudaStreamSynchronize(s);
+        return st;
+    }
     // each column slice is copied to h_out on a second stream as soon as it is final, so all
     // but the last slice's device->host transfer overlaps the remaining filter steps
     HostCopy hc;
@@ -495,18 +579,24 @@ igp_status igp_embed_host(const int32_t* h_edges, int64_t num_edges, int32_t num
     if (st == IGP_OK) st = cuda_status(alloc_async((void**)&d_out, ob, s), "out alloc");
     if (st == IGP_OK) st = cuda_status(cudaStreamWaitEvent(s, g->ready, 0), "stream wait");
     if (st == IGP_OK) st = run_embed(g->csr, *opts, d_out, s, &hc);
-    cudaEvent_t copied = nullptr;
-    if (st == IGP_OK) st = cuda_status(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming), "event");
-    if (st == IGP_OK) st = cuda_status(cudaEventRecord(copied, hc.cs), "event record");
-    if (st == IGP_OK) st = cuda_status(cudaStreamWaitEvent(s, copied, 0), "stream wait");  // d_out freed after
-    free_async(d_out, s);
+    // d_out is released only after every slice copy queued on hc.cs has read it -- also when
+    // the embed failed after queuing some of them (then the copy stream is simply drained)
+    if (d_out) {
+        cudaEvent_t copied = nullptr;
+        bool ordered = hc.cs == nullptr;
+        if (!ordered && cudaEventCreateWithFlags(&copied, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventRecord(copied, hc.cs) == cudaSuccess && cudaStreamWaitEvent(s, copied, 0) == cudaSuccess)
+            ordered = true;
+        if (!ordered) cudaStreamSynchronize(hc.cs);
+        free_async(d_out, s);
+        if (copied) cudaEventDestroy(copied);  // released by the runtime once complete
+    }
     // the range check ran with the build (early on `s`); its flag is read after the work is queued
     if (st == IGP_OK) st = igp_graph_status(g);
     std::string msg = igp_last_error_message();
     igp_destroy_graph_async(g, stream);  // its only user is `s`
     igp_status st2 = cuda_status(cudaStreamSynchronize(s), "stream sync");
     if (hc.cs) cudaStreamSynchronize(hc.cs);
-    if (copied) cudaEventDestroy(copied);
     for (int k = 0; k < kMaxSlices; ++k)
         if (hc.ev[k]) cudaEventDestroy(hc.ev[k]);
     if (hc.cs) cudaStreamDestroy(hc.cs);

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/igp.h"
 
@@ -44,9 +45,11 @@ bool device_info(DeviceInfo* out);
 // every use joins back to the caller's stream before returning)
 cudaStream_t side_stream(int dev);
 
-// stream-ordered allocation helpers (default pool, release threshold raised once)
+// stream-ordered allocation helpers: a memory pool private to the library per device (freed
+// blocks are kept for reuse; igp_trim_memory releases them), never the device's default pool
 cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s);
 void free_async(void* p, cudaStream_t s);
+cudaError_t trim_pool();  // synchronises the device, then trims the current device's pool
 
 inline igp_status cuda_status(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return IGP_OK;
@@ -78,6 +81,8 @@ struct CsrDevice {
     int32_t* rp_perm = nullptr;  // [N+5] CSR of the relabelled graph (row r = node order[r]) ...
     int32_t* col_perm = nullptr; // [cap + kColPad]  ... neighbour ids relabelled, in canonical order
     int32_t* meta = nullptr;     // device [4]: [0] range-error flag (nnz is row_ptr[N])
+    int32_t* labels = nullptr;   // [N] label-propagation communities (community order only): the warm
+                                 // start of the next streaming merge's propagation
     bool perm_alias = false;     // no relabelling: rp_perm/col_perm alias row_ptr/col_idx, order = identity
     int32_t n = 0;
     int64_t cap = 0;             // allocated column entries (>= nnz; 2E + base entries before dedup)
@@ -91,14 +96,21 @@ constexpr int kRpPad = 64;
 // largest CSR entry count (before dedup): int32 offsets with headroom for the kernels' chunk
 // arithmetic (a chunk start + 2 chunks of 16 must not overflow)
 constexpr int64_t kMaxEntries = (int64_t)INT32_MAX - 64;
+// largest node count: the row-order sorts scan kDigits x ceil(N / kSortTile) ~ 2N int32 histogram
+// entries and scan lengths are padded by a 2048-element tile, all inside int32
+constexpr int64_t kMaxNodes = ((int64_t)1 << 30) - 4096;
 // row order of the relabelled CSR the filter steps traverse
 enum RowOrder { kOrderNone = 0, kOrderDegree = 1, kOrderCommunity = 2 };
 constexpr int kLabelPropIters = 8;  // label-propagation sweeps of the community order (measured best of
                                     // 4-14 on headline and Large: profiles/r01b/lp_sweep.txt)
+constexpr int kLabelPropWarmIters = 2;  // sweeps after a streaming merge, from the previous labels
 // canonical CSR of the new edges, merged with `base` (an existing canonical CSR on the same
 // node set) when base != nullptr
 igp_status build_csr(const int32_t* d_edges, int64_t num_edges, int32_t n, RowOrder order, cudaStream_t s,
                      CsrDevice* out, const CsrDevice* base = nullptr);
+
+// deg[i] = rp[i + 1] - rp[i] (the degree diagonal D) into a caller buffer
+igp_status launch_degrees(const int32_t* rp, int32_t n, int32_t* deg, cudaStream_t s);
 
 // exclusive scan of n int32 counts: out[0..n], out[n] = total (int32 range checked by caller)
 igp_status scan_exclusive(const int32_t* in, int32_t* out, int32_t n, cudaStream_t s);
@@ -134,6 +146,14 @@ igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cu
 
 struct igp_graph_s {
     igp::CsrDevice csr;
+    // embeds that read the graph: one event per stream used (recorded after the embed's work),
+    // so igp_destroy_graph waits for exactly the work that uses the graph
+    std::mutex use_mu;
+    struct Use {
+        cudaStream_t stream;
+        cudaEvent_t ev;
+    };
+    std::vector<Use> uses;
     igp::RowOrder order = igp::kOrderDegree;
     bool async = false;        // IGP_BUILD_ASYNC: nnz / range errors resolved lazily
     int device = 0;

@@ -60,7 +60,8 @@ def test_host_side_calls_without_device(igp):
     assert lib.igp_build_graph(None, 0, 0, None, ctypes.byref(h)) == 2
     assert lib.igp_build_graph(None, -1, 5, None, ctypes.byref(h)) == 2
     assert lib.igp_build_graph(ctypes.c_void_p(0x1000), 2**31, 5, None, ctypes.byref(h)) == 7  # not dereferenced
-    assert lib.igp_build_graph(None, 0, 2**31 - 1, None, ctypes.byref(h)) == 7                # N > INT32_MAX - 64
+    assert lib.igp_build_graph(None, 0, 2**31 - 1, None, ctypes.byref(h)) == 7                # N > 2^30 - 4096
+    assert lib.igp_build_graph(None, 0, 2**30 - 4095, None, ctypes.byref(h)) == 7             # just above the limit
     o = igp.make_opts(-1.0, 48, 10)
     assert lib.igp_embed_ex(None, ctypes.byref(o), None, None) == 2
     assert lib.igp_destroy_graph(None) == 0
@@ -79,7 +80,7 @@ def test_more_host_validated_errors(igp):
     assert lib.igp_graph_add_edges(None, None, 0, None) == 2
     assert lib.igp_graph_status(None) == 2
     assert lib.igp_graph_info(None, None, None, None) == 2
-    assert lib.igp_graph_copy_csr(None, None, None, None) == 2
+    assert lib.igp_graph_copy_csr(None, None, None, None, None) == 2
     assert lib.igp_destroy_graph_async(None, None) == 0
     assert lib.igp_philox_bits(0, 0, -1, None, None) == 2
     assert lib.igp_philox_normal(0, 0, 6, None, None) == 2                               # not a multiple of 4
@@ -91,6 +92,17 @@ def test_more_host_validated_errors(igp):
     o.flags = 0
     o.eps = 0.0
     assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o), out, None) == 2               # eps must be > 0
+    o.eps = 1e-3
+    o.ddof = 2
+    assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o), out, None) == 2               # ddof in {0, 1}
+    o.ddof = 0
+    o.d_z0 = 0x1004
+    assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o), out, None) == 2               # d_z0 not 16-B aligned
+    assert lib.igp_birch_create(0, 0.5, 50, ctypes.byref(h)) == 2                        # BIRCH arguments
+    assert lib.igp_birch_create(4, -1.0, 50, ctypes.byref(h)) == 2
+    assert lib.igp_birch_create(4, 0.5, 64, ctypes.byref(h)) == 2
+    assert lib.igp_birch_partial_fit(None, None, 3, None) == 2
+    assert lib.igp_birch_destroy(None) == 0
     for bad_d in (40, 8, 2048):                                                          # multiple of 16 in [16, 1024]
         o2 = igp.make_opts(-1.0, bad_d, 3)
         assert lib.igp_embed_host(None, 0, 4, ctypes.byref(o2), out, None) == 7

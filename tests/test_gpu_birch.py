@@ -1,0 +1,152 @@
+"""GPU BIRCH (igp_birch_*, csrc/birch.cu) against the oracle's BIRCH (oracle/birch_oracle.c).
+
+The bar: bit-exact.  Both sides build the CF tree by the same sequential insertions with the
+same fp64 operation order (readings B1-B6), so the clusters (n, LS, SS, centroid,
+|centroid|^2 of every leaf entry, in label order) and every predicted label must be
+identical, not merely close.  Inputs are the same fp32 values on both sides (the GPU widens
+them to fp64 exactly; the oracle receives the widened values).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import record
+from synth.dcsbm import CONFIGS, generate
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def igp():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test requires CUDA (no CPU fallback)")
+    import paper_2508_19737_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def headline(igp):
+    c = CONFIGS["headline"]
+    edges, _ = generate(c)
+    return c, edges
+
+
+def f32(X):
+    return np.ascontiguousarray(np.asarray(X, dtype=np.float32))
+
+
+def check_same_tree(igp, X, T, B, pieces=1):
+    """fit (in `pieces` partial fits) on both sides; clusters and labels bit-identical."""
+    X = f32(X)
+    n, d = X.shape
+    g = igp.Birch(d, T, B)
+    o = oracle.Birch(d, T, B)
+    cuts = np.linspace(0, n, pieces + 1).astype(int)
+    Xg = torch.from_numpy(X).cuda()
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        g.partial_fit(Xg[a:b])
+        o.partial_fit(X[a:b].astype(np.float64))
+    K, dep, nodes, pts = g.info()
+    ocen, osqn, on, ols, oss = o.clusters()
+    assert K == ocen.shape[0] and pts == n
+    odep, onodes, opts = o.shape()
+    assert dep == odep and nodes == onodes
+    cen, sqn, cnt, ls, ss = (t.cpu().numpy() for t in g.clusters())
+    for name, a, b in (("n", cnt, on), ("LS", ls, ols), ("SS", ss, oss), ("centroid", cen, ocen), ("sqn", sqn, osqn)):
+        assert np.array_equal(a, b), f"{name} differs (max |diff| {np.abs(a - b).max():.3e})"
+    lab = g.predict(Xg).cpu().numpy()
+    olab = oracle.birch_predict(ocen, osqn, X.astype(np.float64))
+    assert np.array_equal(lab, olab)
+    g.close()
+    return K, dep
+
+
+def datasets():
+    rng = np.random.default_rng(11)
+    C = rng.random((12, 8))
+    return [
+        ("blobs8", C[rng.integers(0, 12, 2000)] + rng.normal(0, 0.05, (2000, 8)), 0.1, 50),
+        ("uniform_deep_B3", rng.random((1500, 8)), 0.01, 3),  # every point a leaf entry; many splits
+        ("sigmoid64_T1", 1 / (1 + np.exp(-rng.normal(0, 1, (3000, 64)))), 1.0, 50),
+        ("sigmoid64_T05_B10", 1 / (1 + np.exp(-rng.normal(0, 1, (2000, 64)))), 0.5, 10),
+        ("sigmoid16_B5", 1 / (1 + np.exp(-rng.normal(0, 1, (3000, 16)))), 0.3, 5),
+        ("odd_width_d37", 1 / (1 + np.exp(-rng.normal(0, 1, (1200, 37)))), 0.4, 7),
+        ("wide_d200_B63", rng.random((800, 200)), 2.0, 63),
+        ("single_point", np.array([[0.25, -0.5, 0.75]]), 0.5, 50),
+        ("duplicates", np.repeat(rng.random((5, 6)), 40, axis=0), 0.05, 4),
+    ]
+
+
+@pytest.mark.parametrize("name,X,T,B", datasets(), ids=[d[0] for d in datasets()])
+def test_birch_bit_exact(igp, name, X, T, B):
+    K, dep = check_same_tree(igp, X, T, B)
+    record(f"birch_{name}_K", K)
+
+
+def test_birch_partial_fit_pieces_and_pool_growth(igp):
+    """Alg. 2 l.9: partial fits in stages equal the oracle's; the uniform B = 3 case outgrows the
+    initial pools (1024 entries / 256 nodes) several times."""
+    rng = np.random.default_rng(5)
+    X = rng.random((6000, 8))
+    K, dep = check_same_tree(igp, X, 0.005, 3, pieces=7)
+    assert K > 4000 and dep >= 6
+
+
+def test_birch_on_embeddings_medium(igp):
+    """The paper's pipeline at the Medium config: GPU embed (Alg. 1 l.1-6), then BIRCH on the
+    same fp32 rows on both sides (T = 1.0, B = 50, reading B1)."""
+    c = CONFIGS["medium"]
+    edges, labels = generate(c)
+    e = torch.from_numpy(edges).cuda()
+    g = igp.build_graph(e, c.num_nodes)
+    Z = igp.embed(g, c.tau, c.d, c.steps, c.seed).cpu().numpy()
+    K, dep = check_same_tree(igp, Z, 1.0, 50)
+    record("birch_medium_T1_K", K)
+    K2, dep2 = check_same_tree(igp, Z[:8000], 0.5, 50)  # the library default threshold: many clusters
+    record("birch_medium8k_T05_K", K2)
+
+
+def test_birch_errors(igp):
+    with pytest.raises(igp.IGPError):
+        igp.Birch(8, 0.0, 50)
+    with pytest.raises(igp.IGPError):
+        igp.Birch(8, 0.5, 64)  # branching above the device limit (B + 1 entries <= 64)
+    b = igp.Birch(4, 0.5, 50)
+    with pytest.raises(igp.IGPError):
+        b.predict(torch.zeros((3, 4), device="cuda"))  # empty tree
+    bad = torch.zeros((5, 4), device="cuda")
+    bad[2, 1] = float("nan")
+    with pytest.raises(igp.IGPError):
+        b.partial_fit(bad)
+    assert b.info()[3] == 0  # unchanged
+    b.partial_fit(torch.zeros((0, 4), device="cuda"))
+    b.partial_fit(torch.ones((2, 4), device="cuda"))
+    assert b.info()[:1] == (1,)
+    b.close()
+
+
+def test_birch_headline_full_size(igp, headline):
+    """The bench's clustering step at the Headline size (N = 1M): GPU fit + predict on the GPU
+    embedding vs the oracle on the same rows, bit-exact; times recorded."""
+    c, edges = headline
+    e = torch.from_numpy(edges).cuda()
+    g = igp.build_graph(e, c.num_nodes)
+    Zg = igp.embed(g, c.tau, c.d, c.steps, c.seed)
+    torch.cuda.synchronize()
+    import time
+    t0 = time.perf_counter()
+    b = igp.Birch(c.d, 1.0, 50).partial_fit(Zg)
+    lab = b.predict(Zg)
+    torch.cuda.synchronize()
+    record("birch_headline_gpu_s", time.perf_counter() - t0)
+    Z = Zg.cpu().numpy().astype(np.float64)
+    t0 = time.perf_counter()
+    o = oracle.Birch(c.d, 1.0, 50).fit(Z)
+    ocen, osqn, on, ols, oss = o.clusters()
+    olab = oracle.birch_predict(ocen, osqn, Z)
+    record("birch_headline_oracle_s", time.perf_counter() - t0)
+    cen, sqn, cnt, ls, ss = (t.cpu().numpy() for t in b.clusters())
+    record("birch_headline_K", int(cen.shape[0]))
+    assert np.array_equal(cen, ocen) and np.array_equal(cnt, on) and np.array_equal(ss, oss)
+    assert np.array_equal(lab.cpu().numpy(), olab)

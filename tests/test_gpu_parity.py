@@ -479,12 +479,13 @@ def test_large_csr_bit_exact(igp, large):
 
 
 def test_large_parity_reduced_steps(igp, large):
-    """Full N = 5M / nnz ~ 200M / d = 128 with the bench's kernels and grid; L = 2 so the fp64
-    oracle (~10x the headline's work per layer) fits the test budget."""
+    """Full N = 5M / nnz ~ 200M / d = 128 with the bench's kernels and grid; L = 5 (SURVEY.md
+    §8(d): the fp64 oracle does ~10x the headline's work per layer)."""
     c, edges = large
-    z, ref = run_parity(igp, edges, c.num_nodes, c.d, 2, c.tau)
+    L = 2 if QUICK else 5
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, L, c.tau)
     err = row_rel_err(z, ref)
-    record("large_L2", err)
+    record(f"large_L{L}", err)
     assert err <= TOL
 
 
@@ -530,7 +531,7 @@ def test_paper_settings_full_parity(igp, cfg):
     assert err <= TOL
 
 
-LAYER_TOL_CHAOTIC = 1e-3  # DESIGN.md reading A16
+FLOOR_MARGIN = 2.0  # DESIGN.md reading A16: the GPU error may not exceed twice the fp32-twin floor
 
 
 @pytest.mark.parametrize("cfg", ["paper_50k", "paper_stream_100k", "paper_1m"])
@@ -540,7 +541,9 @@ def test_paper_settings_chaotic_tau_layerwise(igp, cfg):
     trajectories separate after 2-3 layers (reading A16).  Checked instead: layer 1 from the
     exact Philox input at the 1e-4 bar; one layer from seeded layer states Z (synth/states.py,
     generic and tanh-saturated shapes; the same fp32 values go to the CUDA path via d_z0 and to
-    the oracle via Z0) at 1e-3; full-L properties."""
+    the oracle via Z0) at FLOOR_MARGIN x the oracle's fp32-twin error on the same state (measured:
+    the GPU error equals that floor to 5 digits, so it is fp32 itself, not the kernel's deferred
+    z-score algebra); full-L properties."""
     from synth.dcsbm import PAPER_CONFIGS
     from synth.states import layer_state
     c = PAPER_CONFIGS[cfg]
@@ -562,9 +565,10 @@ def test_paper_settings_chaotic_tau_layerwise(igp, cfg):
             twin = oracle.embed(rp, ci, c.num_nodes, c.d, 1, c.tau, Z0=zs.astype(np.float64), mode=om,
                                 nthreads=NTHREADS, fp32_twin=True)
             err = row_rel_err(zl, ref)
+            floor = row_rel_err(twin, ref)
             record(f"{cfg}_one_layer_from_{kind}_state_{mode}", err)
-            record(f"{cfg}_one_layer_from_{kind}_state_{mode}_fp32_floor", row_rel_err(twin, ref))
-            assert err <= LAYER_TOL_CHAOTIC, (kind, mode)
+            record(f"{cfg}_one_layer_from_{kind}_state_{mode}_fp32_floor", floor)
+            assert err <= max(TOL, FLOOR_MARGIN * floor), (kind, mode, err, floor)
     za = igp.embed(g, c.tau, c.d, c.steps, 0)
     zb = igp.embed(g, c.tau, c.d, c.steps, 0)
     assert torch.equal(za, zb)
@@ -848,3 +852,57 @@ def test_maximum_csr_size_circulant(igp):
     zf = igp.embed(g, tau, d, 2, seed)
     assert float(zf.min()) > 0.0 and float(zf.max()) < 1.0
     g.close()
+
+
+# ------------------------------------------------------------------ round-2 boundary additions (§8(b))
+def test_embed_sample_std_ddof(igp):
+    """igp_embed_opts.ddof = 1 (sample std in ZNorm, the other reading of PAPER.md:166) against
+    the oracle with the same ddof; ddof = 0 and 1 really differ."""
+    c = CONFIGS["tiny"]
+    edges, _ = generate(c)
+    z1, ref1 = run_parity(igp, edges, c.num_nodes, c.d, c.steps, c.tau, ddof=1)
+    err = row_rel_err(z1, ref1)
+    record("tiny_ddof1", err)
+    assert err <= TOL
+    z0, _ = run_parity(igp, edges, c.num_nodes, c.d, c.steps, c.tau)
+    assert np.abs(z1 - z0).max() > 1e-6
+
+
+def test_embed_rejects_misaligned_buffers(igp):
+    c = CONFIGS["tiny"]
+    edges, _ = generate(c)
+    g = gpu_graph(igp, edges, c.num_nodes)
+    buf = torch.empty(c.num_nodes * c.d + 4, dtype=torch.float32, device="cuda")
+    with pytest.raises(igp.IGPError):
+        igp.embed(g, c.tau, c.d, 2, 0, out=buf[1:1 + c.num_nodes * c.d].view(c.num_nodes, c.d))
+    z0 = torch.zeros(c.num_nodes * c.d + 4, dtype=torch.float32, device="cuda")[2:2 + c.num_nodes * c.d]
+    with pytest.raises(igp.IGPError):
+        igp.embed(g, c.tau, c.d, 2, 0, z0=z0.view(c.num_nodes, c.d))
+    g.close()
+
+
+def test_copy_csr_degrees(igp):
+    c = CONFIGS["tiny"]
+    edges, _ = generate(c)
+    g = gpu_graph(igp, edges, c.num_nodes)
+    rp, ci, deg = g.csr(degrees=True)
+    torch.cuda.synchronize()
+    rp_o, ci_o, _ = oracle.build_csr(edges, c.num_nodes)
+    assert np.array_equal(deg.cpu().numpy(), np.diff(rp_o))
+    g.close()
+
+
+def test_destroy_waits_for_embeds_on_other_streams_and_trim(igp):
+    """igp_destroy_graph waits for the graph's own uses (embeds on any stream), not the device:
+    destroying right after enqueueing an embed on a side stream leaves that embed intact."""
+    c = CONFIGS["medium"]
+    edges, _ = generate(c)
+    g = gpu_graph(igp, edges, c.num_nodes)
+    ref = igp.embed(g, c.tau, c.d, 5, 0).clone()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        z = igp.embed(g, c.tau, c.d, 5, 0, stream=side)
+    g.close()  # must not free the CSR under the side-stream embed
+    side.synchronize()
+    assert torch.equal(z, ref)
+    igp.trim_memory()

@@ -52,3 +52,24 @@ def test_aggregate_single():
     import bench
     v, t = bench.aggregate([10.0], [5e8])
     assert t == 10.0 and v == pytest.approx(5e10)
+
+
+def test_bench_gpus_flag_relaunches_ranks_cpu():
+    """`python bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (one process per
+    GPU); the CPU self-test runs the GPU arm's multi-rank skeleton (init, barrier, per-rank timing
+    all_gather, max-over-ranks aggregation) on gloo and reports n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--selftest-cpu",
+                        "--config", "tiny", "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
+                       env=env, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and len(line["per_rank_ms"]) == 2
+    assert line["ms_per_step"] == pytest.approx(max(line["per_rank_ms"]))
+    assert line["value"] == pytest.approx(3e6 / (max(line["per_rank_ms"]) / 1e3) / 1e9)

@@ -178,3 +178,13 @@ def test_zscore_properties():
     # population (1/N), not sample (1/(N-1)) — reading A2
     col = np.array([0.0, 2.0])
     assert np.allclose(oracle.zscore_columns(col)[:, 0], [-1.0, 1.0])
+
+
+def test_zscore_sample_std_golden():
+    """ddof = 1 (sample std, the other reading of PAPER.md:166): [1,2,3] has s = 1, so the
+    column becomes [-1, 0, 1]; a single row (N = 1 <= ddof) is treated as constant (0)."""
+    out = oracle.zscore_columns(np.array([1.0, 2.0, 3.0])[:, None], ddof=1)[:, 0]
+    np.testing.assert_allclose(out, [-1.0, 0.0, 1.0], atol=1e-15)
+    assert oracle.zscore_columns(np.array([[5.0, -2.0]]), ddof=1).tolist() == [[0.0, 0.0]]
+    T = np.random.default_rng(0).standard_normal((50, 3))
+    np.testing.assert_allclose(oracle.zscore_columns(T, ddof=1), (T - T.mean(0)) / T.std(0, ddof=1), atol=1e-14)

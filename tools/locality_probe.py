@@ -49,5 +49,5 @@ for name, order in orders.items():
         torch.cuda.synchronize()
         lms, nl = igp.layer_timer_read()
         print(f"{name:38s} W={w:3d}: filter step {lms / cfg.steps:7.3f} ms  "
-              f"gather {4 * g.nnz * cfg.d / (lms / cfg.steps) / 1e9:8.0f} GB/s", flush=True)
+              f"gather {4 * g.nnz * cfg.d / (lms / cfg.steps / 1e3) / 1e12:6.2f} TB/s", flush=True)
     g.close()
