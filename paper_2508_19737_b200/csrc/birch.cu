@@ -6,14 +6,14 @@
 // leaf entries being the K-agnostic clusters, then every row labelled by its nearest leaf
 // centroid.  Insertion is inherently sequential (each point's path depends on every earlier
 // point), so the fit runs as ONE persistent CTA that inserts the points one after another
-// with all of its 512 threads on each insertion:
-//   - the distances from x to a node's <= B + 1 entry centroids: one 8-lane group per entry,
-//     lane r accumulating k = r (mod 8) with fma, the 8 partials combined by a fixed shuffle
-//     tree -- the oracle's dot order (reading B6), so every distance is bit-identical;
+// with all of its 128 threads on each insertion:
+//   - the distances from x to a node's <= B + 1 entry centroids: one 2-lane group per entry,
+//     the eight fma partials over k mod 8 split between the two lanes and combined in the
+//     oracle's fixed order (reading B6), so every distance is bit-identical;
 //   - first-minimum argmin over the entries (warp shuffles + one shared-memory round);
 //   - the leaf's merge test (radius^2 <= T^2) and the CF updates of the path, parallel over
 //     the d coordinates;
-//   - node splits: all pairwise entry distances (upper triangle, 8 lanes per pair), the first
+//   - node splits: all pairwise entry distances (upper triangle, 2 lanes per pair), the first
 //     farthest pair, the two halves' CF sums in entry order.
 // Everything is fp64 and follows oracle/birch_oracle.c step for step (same formulas, same
 // operation order), so the tree -- and hence the clusters and labels -- are bit-identical to
@@ -34,11 +34,16 @@
 namespace igp {
 namespace {
 
-constexpr int kFitThreads = 512;  // 64 groups of 8 lanes: one node's <= B + 1 <= 64 entries at once
+constexpr int kFitThreads = 128;  // 64 groups of 2 lanes: one node's <= B + 1 <= 64 entries at once
 constexpr int kMaxDepth = 64;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kMaxBirchD = 1024;
 constexpr int kMaxBirchBranching = 63;
+
+// rows of X staged in shared memory ahead of the insertions (two chunks of ring_rows(d) rows, by
+// cp.async): the next rows' loads overlap the current insertions instead of one DRAM round trip
+// sitting on every insertion's critical path
+__host__ __device__ constexpr int ring_rows(int d) { return 8192 / d < 2 ? 2 : (8192 / d > 64 ? 64 : 8192 / d); }
 
 // tree header (device int64 words)
 enum { H_NS = 0, H_NN, H_ROOT, H_FIRST_LEAF, H_NPOINTS, H_STOP, H_DEPTH, H_WORDS };
@@ -64,21 +69,29 @@ struct TreeDev {
     long long* hdr;
 };
 
-// full 8-way dot of a and b on the 8 lanes of the calling group (lane r = threadIdx.x & 7):
-// p_r = fma-sum over k = r (mod 8), combined ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7))
-// `mask`: the lanes of the warp that call (whole groups of 8)
-__device__ __forceinline__ double dot8(const double* a, const double* b, int d, int r, unsigned mask = kFullMask) {
-    double acc = 0.0;
-    for (int k = r; k < d; k += 8) acc = __fma_rn(a[k], b[k], acc);
-    acc = __dadd_rn(acc, __shfl_xor_sync(mask, acc, 1));
-    acc = __dadd_rn(acc, __shfl_xor_sync(mask, acc, 2));
-    acc = __dadd_rn(acc, __shfl_xor_sync(mask, acc, 4));
-    return acc;
+// dot(a, b) in the oracle's order (reading B6: eight fma partials p_r over k = r (mod 8), k
+// ascending, combined ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7))) on the 2 lanes of the calling group:
+// lane h accumulates the partials r = h, h+2, h+4, h+6; one shuffle forms the pair sums
+// p_{2q} + p_{2q+1}, the rest is local.  Both lanes return the full dot.  `mask`: the calling lanes.
+__device__ __forceinline__ double dot2(const double* a, const double* b, int d, int h, unsigned mask = kFullMask) {
+    double p[4] = {0.0, 0.0, 0.0, 0.0};  // p[q] = partial r = 2q + h
+    int k0 = 0;
+    for (; k0 + 8 <= d; k0 += 8) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) p[q] = __fma_rn(a[k0 + 2 * q + h], b[k0 + 2 * q + h], p[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (k0 + 2 * q + h < d) p[q] = __fma_rn(a[k0 + 2 * q + h], b[k0 + 2 * q + h], p[q]);
+    double sq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sq[q] = __dadd_rn(p[q], __shfl_xor_sync(mask, p[q], 1));
+    return __dadd_rn(__dadd_rn(sq[0], sq[1]), __dadd_rn(sq[2], sq[3]));
 }
 
 struct FitShared {
     double best_d[kFitThreads / 32];
-    int best_j[kFitThreads / 32];
+    int best_j[kFitThreads / 32 > 8 ? kFitThreads / 32 : 8];  // per-warp argmin; split_node's 5 results
     int path_node[kMaxDepth];
     int path_j[kMaxDepth];
     int depth;
@@ -90,8 +103,8 @@ struct FitShared {
 // argmin over groups g < cnt of dist (held by lane r == 0 of each group); first minimum
 __device__ int block_argmin(double dist, int g, int cnt, FitShared& sh) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double bd = (g < cnt && (threadIdx.x & 7) == 0) ? dist : INFINITY;
-    int bj = (g < cnt && (threadIdx.x & 7) == 0) ? g : 0x7fffffff;
+    double bd = (g < cnt && (threadIdx.x & 1) == 0) ? dist : INFINITY;
+    int bj = (g < cnt && (threadIdx.x & 1) == 0) ? g : 0x7fffffff;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const double od = __shfl_xor_sync(kFullMask, bd, o);
@@ -132,8 +145,8 @@ __device__ void cf_add_point(const TreeDev& t, int s, const double* xs, double x
         t.cen[(int64_t)s * d + k] = l / nn;
     }
     __syncthreads();
-    if (threadIdx.x < 8) {
-        const double q = dot8(t.cen + (int64_t)s * d, t.cen + (int64_t)s * d, d, threadIdx.x, 0xffu);
+    if (threadIdx.x < 2) {
+        const double q = dot2(t.cen + (int64_t)s * d, t.cen + (int64_t)s * d, d, threadIdx.x, 0x3u);
         if (threadIdx.x == 0) {
             t.n[s] = nn;
             t.ss[s] = t.ss[s] + xx;
@@ -165,10 +178,10 @@ __device__ void split_node(const TreeDev& t, int v, double* D, FitShared& sh, in
     const int d = t.d, B1 = t.B + 1;
     const int m = t.nsub[v];
     const int32_t* ent = t.sub + (int64_t)v * B1;
-    const int g = threadIdx.x >> 3, r = threadIdx.x & 7;
-    // pairwise d2 for a < b (one 8-lane group per pair), mirrored; diagonal 0
+    const int g = threadIdx.x >> 1, r = threadIdx.x & 1;
+    // pairwise d2 for a < b (one 2-lane group per pair), mirrored; diagonal 0
     const int P = m * (m - 1) / 2;
-    for (int p0 = 0; p0 < P; p0 += kFitThreads / 8) {
+    for (int p0 = 0; p0 < P; p0 += kFitThreads / 2) {
         const int p = p0 + g;
         int a = 0, b = 0;
         if (p < P) {  // pair index p -> (a, b) in row-major order of the upper triangle
@@ -181,7 +194,7 @@ __device__ void split_node(const TreeDev& t, int v, double* D, FitShared& sh, in
             b = a + 1 + rem;
         }
         const int sa = ent[a], sb = ent[b];  // (a, b) = (0, 0) past the last pair: computed, discarded
-        const double x = dot8(t.cen + (int64_t)sa * d, t.cen + (int64_t)sb * d, d, r);
+        const double x = dot2(t.cen + (int64_t)sa * d, t.cen + (int64_t)sb * d, d, r);
         if (p < P && r == 0) {
             double v2 = __dadd_rn(__dadd_rn(-2.0 * x, t.sqn[sa]), t.sqn[sb]);
             v2 = v2 > 0.0 ? v2 : 0.0;
@@ -279,10 +292,10 @@ __device__ void split_node(const TreeDev& t, int v, double* D, FitShared& sh, in
         t.cen[(int64_t)s2 * d + k] = l2 / t.n[s2];
     }
     __syncthreads();
-    if (threadIdx.x < 16) {
-        const int s = threadIdx.x < 8 ? s1 : s2;
-        const double q = dot8(t.cen + (int64_t)s * d, t.cen + (int64_t)s * d, d, threadIdx.x & 7, 0xffffu);
-        if ((threadIdx.x & 7) == 0) t.sqn[s] = q;
+    if (threadIdx.x < 4) {
+        const int s = threadIdx.x < 2 ? s1 : s2;
+        const double q = dot2(t.cen + (int64_t)s * d, t.cen + (int64_t)s * d, d, threadIdx.x & 1, 0xfu);
+        if ((threadIdx.x & 1) == 0) t.sqn[s] = q;
     }
     __syncthreads();
     h_out[0] = s1;
@@ -329,7 +342,9 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
     double* xs = fit_smem;              // [d] the point
     double* tmp = fit_smem + d;         // [2d] merge candidate LS', c'
     double* D = fit_smem + 3 * d;       // [(B+1)^2] split distances
-    const int g = threadIdx.x >> 3, r = threadIdx.x & 7;
+    float* xring = reinterpret_cast<float*>(D + (size_t)B1 * B1);  // [2][CH][d] staged rows
+    const int CH = ring_rows(d);
+    const int g = threadIdx.x >> 1, r = threadIdx.x & 1;
     // shared-memory pool (if it holds the tree with room for at least a few hundred inserts)
     TreeDev T = t;
     if (threadIdx.x == 0) {
@@ -338,7 +353,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
     }
     __syncthreads();
     if (use_sm) {
-        char* p = reinterpret_cast<char*>(D + (size_t)B1 * B1);
+        char* p = reinterpret_cast<char*>(xring + (size_t)2 * CH * d);
         T.n = reinterpret_cast<double*>(p);
         T.ss = T.n + cap_s_sm;
         T.sqn = T.ss + cap_s_sm;
@@ -357,7 +372,23 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
         __syncthreads();
     }
     if (threadIdx.x == 0) T.hdr[H_STOP] = m;
+    auto issue_chunk = [&](int64_t c) {  // rows [start + c CH, ...) into ring slot c & 1
+        const int64_t r0 = start + c * CH;
+        const int64_t r1 = r0 + CH < m ? r0 + CH : m;
+        float* dst = xring + (size_t)(c & 1) * CH * d;
+        const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(dst);
+        for (int64_t e = threadIdx.x; e < (r1 - r0) * d; e += kFitThreads)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sdst + 4u * (uint32_t)e), "l"(X + r0 * d + e)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue_chunk(0);
     for (int64_t i = start; i < m; ++i) {
+        const int64_t c = (i - start) / CH;
+        if ((i - start) % CH == 0) {  // entering chunk c: queue chunk c + 1, wait for chunk c
+            issue_chunk(c + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        }
         // capacity (all threads read the same header values)
         __syncthreads();
         const long long ns = T.hdr[H_NS], nn = T.hdr[H_NN], dep = T.hdr[H_DEPTH];
@@ -365,16 +396,19 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
             if (threadIdx.x == 0) T.hdr[H_STOP] = i;
             break;
         }
-        for (int k = threadIdx.x; k < d; k += kFitThreads) xs[k] = (double)X[i * d + k];
+        {
+            const float* xr = xring + (size_t)(c & 1) * CH * d + (size_t)((i - start) - c * CH) * d;
+            for (int k = threadIdx.x; k < d; k += kFitThreads) xs[k] = (double)xr[k];
+        }
         __syncthreads();
         double xx = 0.0;
-        if (threadIdx.x < 8) xx = dot8(xs, xs, d, threadIdx.x, 0xffu);
+        if (threadIdx.x < 2) xx = dot2(xs, xs, d, threadIdx.x, 0x3u);
         if (threadIdx.x == 0) sh.scal[0] = xx;
         __syncthreads();
         xx = sh.scal[0];
         const int root = (int)T.hdr[H_ROOT];
         if (T.nsub[root] == 0) {  // the empty root leaf takes the first point
-            if (threadIdx.x == 0) sh.cur = new_entry(t);
+            if (threadIdx.x == 0) sh.cur = new_entry(T);
             __syncthreads();
             const int s = sh.cur;
             for (int k = threadIdx.x; k < d; k += kFitThreads) T.ls[(int64_t)s * d + k] = 0.0;
@@ -392,7 +426,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
             const int cnt = T.nsub[v];
             // every group computes (groups past the node's entries on entry 0, discarded)
             const int s = T.sub[(int64_t)v * B1 + (g < cnt ? g : 0)];
-            const double dt = dot8(T.cen + (int64_t)s * d, xs, d, r);
+            const double dt = dot2(T.cen + (int64_t)s * d, xs, d, r);
             const double dist = __dadd_rn(T.sqn[s], -2.0 * dt);
             const int j = block_argmin(dist, g, cnt, sh);
             if (threadIdx.x == 0) {
@@ -415,8 +449,8 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
             tmp[d + k] = inv * l;
         }
         __syncthreads();
-        if (threadIdx.x < 8) {
-            const double nsq = dot8(tmp + d, tmp + d, d, threadIdx.x, 0xffu);
+        if (threadIdx.x < 2) {
+            const double nsq = dot2(tmp + d, tmp + d, d, threadIdx.x, 0x3u);
             if (threadIdx.x == 0) {
                 const double nss = T.ss[sj] + xx;
                 const double r2 = nss / nn1 - nsq;
@@ -439,7 +473,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
             }
             __syncthreads();
         } else {
-            if (threadIdx.x == 0) sh.cur = new_entry(t);
+            if (threadIdx.x == 0) sh.cur = new_entry(T);
             __syncthreads();
             const int s = sh.cur;
             for (int k = threadIdx.x; k < d; k += kFitThreads) T.ls[(int64_t)s * d + k] = 0.0;
@@ -479,6 +513,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
         }
         if (threadIdx.x == 0) T.hdr[H_NPOINTS]++;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     if (use_sm) {
         __syncthreads();
         copy_tree(t, T, T.hdr[H_NS], T.hdr[H_NN]);
@@ -516,7 +551,7 @@ __global__ void birch_gather_kernel(TreeDev t, const int32_t* __restrict__ idx, 
     }
 }
 
-// label_i = argmin_j sqn_j - 2 dot8(c_j, x_i) (first minimum).  128 points per block (one per
+// label_i = argmin_j sqn_j - 2 dot(c_j, x_i) (first minimum; the oracle's dot order).  128 points per block (one per
 // thread), cluster tiles of kPT centroids staged in shared memory; the point's row lives in
 // shared memory too (stride d + 1).
 constexpr int kPredThreads = 128;
@@ -589,7 +624,9 @@ struct igp_birch_s {
 
 namespace {
 
-size_t smem_fit(int d, int B) { return sizeof(double) * ((size_t)3 * d + (size_t)(B + 1) * (B + 1)); }
+size_t smem_fit(int d, int B) {
+    return sizeof(double) * ((size_t)3 * d + (size_t)(B + 1) * (B + 1)) + sizeof(float) * 2 * (size_t)ring_rows(d) * d;
+}
 // shared-memory pool capacities (entries, nodes) that fit beside the fit kernel's scratch
 void smem_pool_caps(int d, int B, int max_optin, int64_t* cs, int64_t* cn, size_t* bytes) {
     const size_t base = smem_fit(d, B) + 2048;  // + static shared memory
