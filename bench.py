@@ -456,6 +456,18 @@ def run_gpu(args, cfg):
         st_merge = [starts[t].elapsed_time(stage_ev[t][0]) for t in range(10)]
         stages = [{"stage": t, "nnz": stage_nnz[t], "build_or_merge_ms": st_merge[t], "embed_ms": st_embed[t]}
                   for t in range(10)]
+        # reference for the merges: a fresh build of the final (stage-9) graph from all its edges
+        all_edges = torch.cat(batches)
+        fb = []
+        for _ in range(4):
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            gf = igp.build_graph(all_edges, N, stream=stream, async_build=True)
+            f1.record(stream)
+            gf.close(stream=stream)
+            torch.cuda.synchronize(dev)
+            fb.append(f0.elapsed_time(f1))
+        fresh_build_ms = float(np.median(fb[1:]))
 
     # embed-only timing (no build), same stream, for the breakdown (static configs)
     embed_ms = None
@@ -520,6 +532,8 @@ def run_gpu(args, cfg):
         extra.update({"embed_ms": embed_ms, "build_ms": t_max / args.steps - embed_ms})
     if stages is not None:
         extra["stages"] = stages
+        extra["fresh_build_of_final_graph_ms"] = fresh_build_ms
+        extra["merge_stage9_vs_fresh_build"] = stages[9]["build_or_merge_ms"] / fresh_build_ms
         extra["units_per_step"] = "sum over the 10 stages of nnz_t x d x L"
     line = base_line(args, cfg, world, value, t_max / args.steps, "f32", nnz, extra)
     line.update({"roofline": roof, "gpu_launches": launches, "clocks": clock_rec})

@@ -71,27 +71,41 @@ struct TreeDev {
 
 // dot(a, b) in the oracle's order (reading B6: eight fma partials p_r over k = r (mod 8), k
 // ascending, combined ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7))) on the 2 lanes of the calling group:
-// lane h accumulates the partials r = h, h+2, h+4, h+6; one shuffle forms the pair sums
-// p_{2q} + p_{2q+1}, the rest is local.  Both lanes return the full dot.  `mask`: the calling lanes.
+// lane h accumulates the partials r = 4h .. 4h+3 (contiguous k: 16-byte vector loads), forms its
+// half of the tree locally, and one shuffle adds the two halves.  Both lanes return the full dot.
+// `mask`: the calling lanes.
 __device__ __forceinline__ double dot2(const double* a, const double* b, int d, int h, unsigned mask = kFullMask) {
-    double p[4] = {0.0, 0.0, 0.0, 0.0};  // p[q] = partial r = 2q + h
+    double p[4] = {0.0, 0.0, 0.0, 0.0};  // p[q] = partial r = 4h + q
     int k0 = 0;
-    for (; k0 + 8 <= d; k0 += 8) {
+    if ((d & 1) == 0) {  // rows start 16-byte aligned: two double2 loads per operand and block
+        for (; k0 + 8 <= d; k0 += 8) {
+            const double2 a0 = *reinterpret_cast<const double2*>(a + k0 + 4 * h);
+            const double2 a1 = *reinterpret_cast<const double2*>(a + k0 + 4 * h + 2);
+            const double2 b0 = *reinterpret_cast<const double2*>(b + k0 + 4 * h);
+            const double2 b1 = *reinterpret_cast<const double2*>(b + k0 + 4 * h + 2);
+            p[0] = __fma_rn(a0.x, b0.x, p[0]);
+            p[1] = __fma_rn(a0.y, b0.y, p[1]);
+            p[2] = __fma_rn(a1.x, b1.x, p[2]);
+            p[3] = __fma_rn(a1.y, b1.y, p[3]);
+        }
+    } else {
+        for (; k0 + 8 <= d; k0 += 8) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) p[q] = __fma_rn(a[k0 + 2 * q + h], b[k0 + 2 * q + h], p[q]);
+            for (int q = 0; q < 4; ++q) p[q] = __fma_rn(a[k0 + 4 * h + q], b[k0 + 4 * h + q], p[q]);
+        }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-        if (k0 + 2 * q + h < d) p[q] = __fma_rn(a[k0 + 2 * q + h], b[k0 + 2 * q + h], p[q]);
-    double sq[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) sq[q] = __dadd_rn(p[q], __shfl_xor_sync(mask, p[q], 1));
-    return __dadd_rn(__dadd_rn(sq[0], sq[1]), __dadd_rn(sq[2], sq[3]));
+        if (k0 + 4 * h + q < d) p[q] = __fma_rn(a[k0 + 4 * h + q], b[k0 + 4 * h + q], p[q]);
+    const double half = __dadd_rn(__dadd_rn(p[0], p[1]), __dadd_rn(p[2], p[3]));
+    return __dadd_rn(half, __shfl_xor_sync(mask, half, 1));  // left + right on both lanes (commutative)
 }
 
 struct FitShared {
     double best_d[kFitThreads / 32];
-    int best_j[kFitThreads / 32 > 8 ? kFitThreads / 32 : 8];  // per-warp argmin; split_node's 5 results
+    int best_j[kFitThreads / 32 > 8 ? kFitThreads / 32 : 8];  // per-warp argmax (splits); split results
+    double am_d[2][kFitThreads / 32];                           // per-warp argmin, two alternating slots
+    int am_j[2][kFitThreads / 32];
     int path_node[kMaxDepth];
     int path_j[kMaxDepth];
     int depth;
@@ -100,8 +114,10 @@ struct FitShared {
     double scal[4];
 };
 
-// argmin over groups g < cnt of dist (held by lane r == 0 of each group); first minimum
-__device__ int block_argmin(double dist, int g, int cnt, FitShared& sh) {
+// argmin over groups g < cnt of dist (held by lane r == 0 of each group); first minimum.  One
+// barrier: every thread reduces the per-warp results itself; the per-warp slots alternate between
+// calls (`slot` toggles), and consecutive calls are separated by at least one other barrier.
+__device__ int block_argmin(double dist, int g, int cnt, FitShared& sh, int& slot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double bd = (g < cnt && (threadIdx.x & 1) == 0) ? dist : INFINITY;
     int bj = (g < cnt && (threadIdx.x & 1) == 0) ? g : 0x7fffffff;
@@ -115,24 +131,23 @@ __device__ int block_argmin(double dist, int g, int cnt, FitShared& sh) {
         }
     }
     if (lane == 0) {
-        sh.best_d[warp] = bd;
-        sh.best_j[warp] = bj;
+        sh.am_d[slot][warp] = bd;
+        sh.am_j[slot][warp] = bj;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double b = sh.best_d[0];
-        int j = sh.best_j[0];
-        for (int w = 1; w < kFitThreads / 32; ++w)
-            if (sh.best_d[w] < b || (sh.best_d[w] == b && sh.best_j[w] < j)) {
-                b = sh.best_d[w];
-                j = sh.best_j[w];
-            }
-        sh.cur = j;
+    double b = sh.am_d[slot][0];
+    int j = sh.am_j[slot][0];
+#pragma unroll
+    for (int w = 1; w < kFitThreads / 32; ++w) {
+        const double v = sh.am_d[slot][w];
+        const int jw = sh.am_j[slot][w];
+        if (v < b || (v == b && jw < j)) {
+            b = v;
+            j = jw;
+        }
     }
-    __syncthreads();
-    const int res = sh.cur;
-    __syncthreads();
-    return res;
+    slot ^= 1;
+    return j;
 }
 
 // CF_s += point x (n = 1, LS = x, SS = xx); c = LS / n, sqn = dot(c, c).  All threads.
@@ -342,7 +357,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
     double* xs = fit_smem;              // [d] the point
     double* tmp = fit_smem + d;         // [2d] merge candidate LS', c'
     double* D = fit_smem + 3 * d;       // [(B+1)^2] split distances
-    float* xring = reinterpret_cast<float*>(D + (size_t)B1 * B1);  // [2][CH][d] staged rows
+    float* xring = reinterpret_cast<float*>(D + (((size_t)B1 * B1 + 1) & ~(size_t)1));  // [2][CH][d] staged rows
     const int CH = ring_rows(d);
     const int g = threadIdx.x >> 1, r = threadIdx.x & 1;
     // shared-memory pool (if it holds the tree with room for at least a few hundred inserts)
@@ -383,6 +398,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     issue_chunk(0);
+    int am_slot = 0;
     for (int64_t i = start; i < m; ++i) {
         const int64_t c = (i - start) / CH;
         if ((i - start) % CH == 0) {  // entering chunk c: queue chunk c + 1, wait for chunk c
@@ -428,7 +444,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
             const int s = T.sub[(int64_t)v * B1 + (g < cnt ? g : 0)];
             const double dt = dot2(T.cen + (int64_t)s * d, xs, d, r);
             const double dist = __dadd_rn(T.sqn[s], -2.0 * dt);
-            const int j = block_argmin(dist, g, cnt, sh);
+            const int j = block_argmin(dist, g, cnt, sh, am_slot);
             if (threadIdx.x == 0) {
                 sh.path_node[depth] = v;
                 sh.path_j[depth] = j;
@@ -483,14 +499,12 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
             __syncthreads();
             split = T.nsub[leaf] > T.B;
         }
-        // back up the path: plain CF updates above the highest split, splits below it
-        for (int l = depth - 2; l >= 0; --l) {
+        // back up the path: splits bottom-up while they propagate, then one batched CF update of
+        // every remaining ancestor entry (distinct entries: their order does not matter)
+        int l = depth - 2;
+        for (; l >= 0 && split; --l) {
             const int pv = sh.path_node[l], pj = sh.path_j[l];
             const int se = T.sub[(int64_t)pv * B1 + pj];
-            if (!split) {
-                cf_add_point(T, se, xs, xx);
-                continue;
-            }
             int h[2];
             split_node(T, T.child[se], D, sh, h);
             if (threadIdx.x == 0) {
@@ -499,6 +513,29 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
             }
             __syncthreads();
             split = T.nsub[pv] > T.B;
+        }
+        if (l >= 0) {  // levels 0..l: CF_e += x, c = LS / n, sqn = |c|^2
+            const int nl = l + 1;
+            for (int idx = threadIdx.x; idx < nl * d; idx += kFitThreads) {
+                const int lv = idx / d, k = idx % d;
+                const int se = T.sub[(int64_t)sh.path_node[lv] * B1 + sh.path_j[lv]];
+                const double nn = T.n[se] + 1.0;
+                const double lsum = T.ls[(int64_t)se * d + k] + xs[k];
+                T.ls[(int64_t)se * d + k] = lsum;
+                T.cen[(int64_t)se * d + k] = lsum / nn;
+            }
+            __syncthreads();
+            for (int lv0 = 0; lv0 < nl; lv0 += kFitThreads / 2) {  // one 2-lane group per level
+                const int lv = lv0 + g;
+                const int se = T.sub[(int64_t)sh.path_node[lv < nl ? lv : 0] * B1 + sh.path_j[lv < nl ? lv : 0]];
+                const double q = dot2(T.cen + (int64_t)se * d, T.cen + (int64_t)se * d, d, r);
+                if (lv < nl && r == 0) {
+                    T.n[se] = T.n[se] + 1.0;
+                    T.ss[se] = T.ss[se] + xx;
+                    T.sqn[se] = q;
+                }
+            }
+            __syncthreads();
         }
         if (split) {  // the root itself split: a new internal root holds the two halves
             int h[2];
@@ -624,8 +661,11 @@ struct igp_birch_s {
 
 namespace {
 
+// dynamic shared memory of the fit kernel before the tree pool: x, the merge candidate, the split
+// distances (rounded to an even count: every array below stays 16-byte aligned), the staged rows
 size_t smem_fit(int d, int B) {
-    return sizeof(double) * ((size_t)3 * d + (size_t)(B + 1) * (B + 1)) + sizeof(float) * 2 * (size_t)ring_rows(d) * d;
+    const size_t dd = ((size_t)(B + 1) * (B + 1) + 1) & ~(size_t)1;
+    return sizeof(double) * ((size_t)3 * d + dd) + ((sizeof(float) * 2 * (size_t)ring_rows(d) * d + 15) & ~(size_t)15);
 }
 // shared-memory pool capacities (entries, nodes) that fit beside the fit kernel's scratch
 void smem_pool_caps(int d, int B, int max_optin, int64_t* cs, int64_t* cn, size_t* bytes) {
@@ -639,6 +679,7 @@ void smem_pool_caps(int d, int B, int max_optin, int64_t* cs, int64_t* cn, size_
     int64_t c = (int64_t)(avail / (per_e + per_n / 4 + 1));
     while (c > 0 && (size_t)c * per_e + (size_t)(c / 4 + 8) * per_n > avail) --c;
     if (c < 128) return;  // too small to be worth a launch-long residency
+    c &= ~(int64_t)3;     // even entry count: the LS / centroid rows stay 16-byte aligned
     *cs = c;
     *cn = c / 4 + 8;
     *bytes = (size_t)c * per_e + (size_t)(*cn) * per_n + sizeof(long long) * H_WORDS;

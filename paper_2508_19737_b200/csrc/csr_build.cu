@@ -253,6 +253,67 @@ __device__ __forceinline__ int warp_sort_dedup(int32_t* seg, int len, int lane) 
     return base;
 }
 
+// rows of <= 16 entries are sorted by one thread each (a 16-input bitonic network in registers,
+// INT_MAX padding), then deduplicated: a warp takes 32 rows at a time (streaming merges and
+// sparse graphs are mostly such rows); the warp's longer rows follow one at a time
+constexpr int kThreadSortCap = 16;
+
+__device__ __forceinline__ void cas(int32_t& a, int32_t& b, bool up) {
+    const int32_t lo = a < b ? a : b, hi = a < b ? b : a;
+    a = up ? lo : hi;
+    b = up ? hi : lo;
+}
+
+__device__ int thread_sort_dedup16(int32_t* row, int len) {
+    int32_t v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = k < len ? row[k] : INT_MAX;
+#pragma unroll
+    for (int k = 2; k <= 16; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int ixj = i ^ j;
+                if (ixj > i) cas(v[i], v[ixj], (i & k) == 0);
+            }
+    int u = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if (k < len && (k == 0 || v[k] != v[k - 1])) row[u++] = v[k];
+    return u;
+}
+
+__device__ void warp_sort_row(int32_t* __restrict__ tmp, int32_t* __restrict__ ucnt, int32_t* buf, int64_t r,
+                              int32_t o, int len, int lane) {
+    if (len <= 256) {  // registers: up to 8 elements per lane, bitonic network over shuffles
+        const int u = len <= 64    ? warp_sort_dedup<2>(tmp + o, len, lane)
+                      : len <= 128 ? warp_sort_dedup<4>(tmp + o, len, lane)
+                                   : warp_sort_dedup<8>(tmp + o, len, lane);  // len is warp-uniform
+        if (lane == 0) ucnt[r] = u;
+        return;
+    }
+    const int P = next_pow2(len);
+    for (int i = lane; i < P; i += 32) buf[i] = i < len ? tmp[o + i] : INT_MAX;
+    __syncwarp();
+    warp_bitonic(buf, P, lane);
+    int base = 0;
+    for (int i0 = 0; i0 < len; i0 += 32) {
+        const int i = i0 + lane;
+        bool keep = false;
+        int32_t v = 0;
+        if (i < len) {
+            v = buf[i];
+            keep = (i == 0) || (v != buf[i - 1]);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) tmp[o + base + __popc(m & lanemask_lt())] = v;
+        base += __popc(m);
+    }
+    if (lane == 0) ucnt[r] = base;
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(256) sort_rows_warp_kernel(const int32_t* __restrict__ off, int32_t* __restrict__ tmp,
                                                              int32_t* __restrict__ ucnt, int32_t n,
                                                              int32_t* __restrict__ big_list, int32_t* __restrict__ big_count,
@@ -262,46 +323,32 @@ __global__ void __launch_bounds__(256) sort_rows_warp_kernel(const int32_t* __re
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int32_t* buf = sbuf[warp];
     const int64_t nwarps = (int64_t)gridDim.x * 8;
-    for (int64_t r = (int64_t)blockIdx.x * 8 + warp; r < n; r += nwarps) {
-        const int32_t o = off[r];
-        const int len = off[r + 1] - o;
-        if (len > kWarpSortCap) {
-            if (lane == 0) {
-                if (len <= kBlockSortCap) big_list[atomicAdd(big_count, 1)] = r;
-                else giant_list[atomicAdd(giant_count, 1)] = r;
+    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * 32; r0 < n; r0 += nwarps * 32) {
+        // one row per lane: short rows sorted by their lane, the others collected
+        const int64_t r = r0 + lane;
+        int32_t o = 0;
+        int len = 0;
+        bool warp_row = false;
+        if (r < n) {
+            o = off[r];
+            len = off[r + 1] - o;
+            if (len > kWarpSortCap) {
+                if (len <= kBlockSortCap) big_list[atomicAdd(big_count, 1)] = (int32_t)r;
+                else giant_list[atomicAdd(giant_count, 1)] = (int32_t)r;
+            } else if (len <= kThreadSortCap) {
+                ucnt[r] = len <= 1 ? len : thread_sort_dedup16(tmp + o, len);
+            } else {
+                warp_row = true;
             }
-            continue;
         }
-        if (len <= 1) {
-            if (lane == 0) ucnt[r] = len;
-            continue;
+        unsigned pending = __ballot_sync(0xffffffffu, warp_row);
+        while (pending) {
+            const int src = __ffs(pending) - 1;
+            pending &= pending - 1;
+            const int32_t ro = __shfl_sync(0xffffffffu, o, src);
+            const int rl = __shfl_sync(0xffffffffu, len, src);
+            warp_sort_row(tmp, ucnt, buf, r0 + src, ro, rl, lane);
         }
-        if (len <= 256) {  // registers: up to 8 elements per lane, bitonic network over shuffles
-            const int u = len <= 64    ? warp_sort_dedup<2>(tmp + o, len, lane)
-                          : len <= 128 ? warp_sort_dedup<4>(tmp + o, len, lane)
-                                       : warp_sort_dedup<8>(tmp + o, len, lane);  // len is warp-uniform
-            if (lane == 0) ucnt[r] = u;
-            continue;
-        }
-        const int P = next_pow2(len);
-        for (int i = lane; i < P; i += 32) buf[i] = i < len ? tmp[o + i] : INT_MAX;
-        __syncwarp();
-        warp_bitonic(buf, P, lane);
-        int base = 0;
-        for (int i0 = 0; i0 < len; i0 += 32) {
-            const int i = i0 + lane;
-            bool keep = false;
-            int32_t v = 0;
-            if (i < len) {
-                v = buf[i];
-                keep = (i == 0) || (v != buf[i - 1]);
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep) tmp[o + base + __popc(m & lanemask_lt())] = v;
-            base += __popc(m);
-        }
-        if (lane == 0) ucnt[r] = base;
-        __syncwarp();
     }
 }
 
@@ -426,7 +473,14 @@ __device__ __forceinline__ int deg_key(const int32_t* rp, int32_t i) {
 // over the degree order), which must be deterministic.
 constexpr int kDigitBits = 12;
 constexpr int kDigits = 1 << kDigitBits;
-constexpr int kSortTile = 2048;
+constexpr int kSortTile = 2048;  // largest tile; graphs with few nodes use smaller tiles (more warps)
+
+// tile of the stable sort passes for n elements: enough tiles to give every SM several warps
+int sort_tile(int32_t n, int num_sms) {
+    int t = 256;
+    while (t < kSortTile && (int64_t)n / (2 * t) >= (int64_t)num_sms * 8) t *= 2;
+    return t;
+}
 
 __global__ void degree_keys_kernel(const int32_t* __restrict__ rp, int32_t n, int32_t* __restrict__ keys,
                                    int32_t* __restrict__ vals) {
@@ -447,30 +501,31 @@ __global__ void label_keys_kernel(const int32_t* __restrict__ order, const int32
     }
 }
 
+// `nd` digits of the pass (a power of 2 <= kDigits), `tile` elements per tile
 __global__ void __launch_bounds__(256) tile_digit_hist_kernel(const int32_t* __restrict__ keys, int32_t n, int shift,
-                                                              int32_t ntiles, int32_t* __restrict__ H) {
+                                                              int nd, int tile, int32_t ntiles, int32_t* __restrict__ H) {
     __shared__ int32_t h[kDigits];
-    for (int b = threadIdx.x; b < kDigits; b += blockDim.x) h[b] = 0;
+    for (int b = threadIdx.x; b < nd; b += blockDim.x) h[b] = 0;
     __syncthreads();
-    const int64_t t0 = (int64_t)blockIdx.x * kSortTile;
-    for (int i = threadIdx.x; i < kSortTile; i += blockDim.x)
-        if (t0 + i < n) atomicAdd(&h[(keys[t0 + i] >> shift) & (kDigits - 1)], 1);
+    const int64_t t0 = (int64_t)blockIdx.x * tile;
+    for (int i = threadIdx.x; i < tile; i += blockDim.x)
+        if (t0 + i < n) atomicAdd(&h[(keys[t0 + i] >> shift) & (nd - 1)], 1);
     __syncthreads();
-    for (int b = threadIdx.x; b < kDigits; b += blockDim.x) H[(int64_t)b * ntiles + blockIdx.x] = h[b];
+    for (int b = threadIdx.x; b < nd; b += blockDim.x) H[(int64_t)b * ntiles + blockIdx.x] = h[b];
 }
 
 __global__ void __launch_bounds__(32) tile_digit_scatter_kernel(const int32_t* __restrict__ keys,
                                                                 const int32_t* __restrict__ vals, int32_t n,
-                                                                int shift, int32_t ntiles,
+                                                                int shift, int nd, int tile, int32_t ntiles,
                                                                 const int32_t* __restrict__ Hs,
                                                                 int32_t* __restrict__ okeys,
                                                                 int32_t* __restrict__ ovals) {
     __shared__ int32_t cnt[kDigits];
     const int lane = threadIdx.x;
-    for (int b = lane; b < kDigits; b += 32) cnt[b] = 0;
+    for (int b = lane; b < nd; b += 32) cnt[b] = 0;
     __syncwarp();
-    const int64_t t0 = (int64_t)blockIdx.x * kSortTile;
-    for (int c = 0; c < kSortTile; c += 32) {
+    const int64_t t0 = (int64_t)blockIdx.x * tile;
+    for (int c = 0; c < tile; c += 32) {
         const int64_t i = t0 + c + lane;
         const bool act = i < n;
         const unsigned am = __ballot_sync(0xffffffffu, act);
@@ -479,7 +534,7 @@ __global__ void __launch_bounds__(32) tile_digit_scatter_kernel(const int32_t* _
         if (act) {
             key = keys[i];
             val = vals[i];
-            dg = (key >> shift) & (kDigits - 1);
+            dg = (key >> shift) & (nd - 1);
         }
         if (act) {
             const unsigned peers = __match_any_sync(am, dg);
@@ -613,15 +668,18 @@ struct PairSortScratch {
 // the key; the sorted values are written to `out` (which may be one of the scratch buffers)
 igp_status stable_sort_pairs(int32_t n, int key_bits, const PairSortScratch& sc, int32_t* out, cudaStream_t s,
                              const DeviceInfo& di) {
-    const int32_t ntiles = (n + kSortTile - 1) / kSortTile;
+    const int tile = sort_tile(n, di.num_sms);
+    const int32_t ntiles = (n + tile - 1) / tile;
     int cur = 0;
     for (int shift = 0; shift < key_bits; shift += kDigitBits) {
         const bool last = shift + kDigitBits >= key_bits;
-        tile_digit_hist_kernel<<<ntiles, 256, 0, s>>>(sc.keys[cur], n, shift, ntiles, sc.H);
+        const int bits = key_bits - shift < kDigitBits ? key_bits - shift : kDigitBits;
+        const int nd = 1 << bits;
+        tile_digit_hist_kernel<<<ntiles, 256, 0, s>>>(sc.keys[cur], n, shift, nd, tile, ntiles, sc.H);
         IGP_TRY(launch_status("tile_digit_hist_kernel"));
-        IGP_TRY(scan_exclusive(sc.H, sc.Hs, kDigits * ntiles, s));
+        IGP_TRY(scan_exclusive(sc.H, sc.Hs, nd * ntiles, s));
         int32_t* ov = last ? out : sc.vals[cur ^ 1];
-        tile_digit_scatter_kernel<<<ntiles, 32, 0, s>>>(sc.keys[cur], sc.vals[cur], n, shift, ntiles, sc.Hs,
+        tile_digit_scatter_kernel<<<ntiles, 32, 0, s>>>(sc.keys[cur], sc.vals[cur], n, shift, nd, tile, ntiles, sc.Hs,
                                                         sc.keys[cur ^ 1], ov);
         IGP_TRY(launch_status("tile_digit_scatter_kernel"));
         cur ^= 1;
@@ -747,7 +805,7 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     size_t o_bitmap = al(o_degp + sizeof(int32_t) * (size_t)n);
     size_t o_tmp = al(o_bitmap + sizeof(uint32_t) * (size_t)words * kGiantBlocks);
     // stable pair sorts of the row orders: keys / vals double buffers and tile digit histograms
-    const int32_t ntiles = (n + kSortTile - 1) / kSortTile;
+    const int32_t ntiles = (n + sort_tile(n, di.num_sms) - 1) / sort_tile(n, di.num_sms);
     const size_t hbytes = al(sizeof(int32_t) * ((size_t)kDigits * ntiles + 1));
     size_t o_psort = al(o_tmp + sizeof(int32_t) * (size_t)(raw > 0 ? raw : 1));
     size_t o_comm = o_psort + (reorder ? al(sizeof(int32_t) * (size_t)n) * 4 + 2 * hbytes : 0);
@@ -912,7 +970,8 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         ev_lp = lp;
     }
     // B6a: degree-descending order, ties by ascending id: one stable counting-sort pass of the
-    // ids by degree bucket
+    // ids by degree bucket (also after a streaming merge: measured, keeping the base graph's
+    // order instead slows the later stages' filter steps by up to 20%, profiles/r02)
     const int ng = grid_for(n, 256, di.num_sms, 8);
     degree_keys_kernel<<<ng, 256, 0, s>>>(c.row_ptr, n, psc.keys[0], psc.vals[0]);
     IGP_STEP(launch_status("degree_keys_kernel"));
