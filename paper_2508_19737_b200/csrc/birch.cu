@@ -55,7 +55,9 @@ struct TreeDev {
     double* n;
     double* ls;   // [cap_s][d]
     double* ss;
-    double* cen;  // [cap_s][d]
+    double* cen;  // [cap_s][ldc]
+    int ldc;      // centroid row stride (doubles): d in global memory; d + 2 in the shared pool for even d
+                  // (rows of consecutive entries then start in different bank groups)
     double* sqn;
     int32_t* child;
     int64_t cap_s;
@@ -157,11 +159,11 @@ __device__ void cf_add_point(const TreeDev& t, int s, const double* xs, double x
     for (int k = threadIdx.x; k < d; k += kFitThreads) {
         const double l = t.ls[(int64_t)s * d + k] + xs[k];
         t.ls[(int64_t)s * d + k] = l;
-        t.cen[(int64_t)s * d + k] = l / nn;
+        t.cen[(int64_t)s * t.ldc + k] = l / nn;
     }
     __syncthreads();
     if (threadIdx.x < 2) {
-        const double q = dot2(t.cen + (int64_t)s * d, t.cen + (int64_t)s * d, d, threadIdx.x, 0x3u);
+        const double q = dot2(t.cen + (int64_t)s * t.ldc, t.cen + (int64_t)s * t.ldc, d, threadIdx.x, 0x3u);
         if (threadIdx.x == 0) {
             t.n[s] = nn;
             t.ss[s] = t.ss[s] + xx;
@@ -209,7 +211,7 @@ __device__ void split_node(const TreeDev& t, int v, double* D, FitShared& sh, in
             b = a + 1 + rem;
         }
         const int sa = ent[a], sb = ent[b];  // (a, b) = (0, 0) past the last pair: computed, discarded
-        const double x = dot2(t.cen + (int64_t)sa * d, t.cen + (int64_t)sb * d, d, r);
+        const double x = dot2(t.cen + (int64_t)sa * t.ldc, t.cen + (int64_t)sb * t.ldc, d, r);
         if (p < P && r == 0) {
             double v2 = __dadd_rn(__dadd_rn(-2.0 * x, t.sqn[sa]), t.sqn[sb]);
             v2 = v2 > 0.0 ? v2 : 0.0;
@@ -303,13 +305,13 @@ __device__ void split_node(const TreeDev& t, int v, double* D, FitShared& sh, in
         }
         t.ls[(int64_t)s1 * d + k] = l1;
         t.ls[(int64_t)s2 * d + k] = l2;
-        t.cen[(int64_t)s1 * d + k] = l1 / t.n[s1];
-        t.cen[(int64_t)s2 * d + k] = l2 / t.n[s2];
+        t.cen[(int64_t)s1 * t.ldc + k] = l1 / t.n[s1];
+        t.cen[(int64_t)s2 * t.ldc + k] = l2 / t.n[s2];
     }
     __syncthreads();
     if (threadIdx.x < 4) {
         const int s = threadIdx.x < 2 ? s1 : s2;
-        const double q = dot2(t.cen + (int64_t)s * d, t.cen + (int64_t)s * d, d, threadIdx.x & 1, 0xfu);
+        const double q = dot2(t.cen + (int64_t)s * t.ldc, t.cen + (int64_t)s * t.ldc, d, threadIdx.x & 1, 0xfu);
         if ((threadIdx.x & 1) == 0) t.sqn[s] = q;
     }
     __syncthreads();
@@ -332,7 +334,7 @@ __device__ void copy_tree(const TreeDev& dst, const TreeDev& src, long long ns, 
     }
     for (long long e = threadIdx.x; e < ns * d; e += kFitThreads) {
         dst.ls[e] = src.ls[e];
-        dst.cen[e] = src.cen[e];
+        dst.cen[(e / d) * dst.ldc + e % d] = src.cen[(e / d) * src.ldc + e % d];
     }
     for (long long v = threadIdx.x; v < nn; v += kFitThreads) {
         dst.is_leaf[v] = src.is_leaf[v];
@@ -374,7 +376,8 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
         T.sqn = T.ss + cap_s_sm;
         T.ls = T.sqn + cap_s_sm;
         T.cen = T.ls + cap_s_sm * d;
-        T.hdr = reinterpret_cast<long long*>(T.cen + cap_s_sm * d);
+        T.ldc = (d & 1) ? d : d + 2;
+        T.hdr = reinterpret_cast<long long*>(T.cen + cap_s_sm * T.ldc);
         T.child = reinterpret_cast<int32_t*>(T.hdr + H_WORDS);
         T.is_leaf = T.child + cap_s_sm;
         T.nsub = T.is_leaf + cap_n_sm;
@@ -399,12 +402,16 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
     };
     issue_chunk(0);
     int am_slot = 0;
+    int64_t c = -1;  // current chunk of staged rows
+    int in_chunk = CH;
     for (int64_t i = start; i < m; ++i) {
-        const int64_t c = (i - start) / CH;
-        if ((i - start) % CH == 0) {  // entering chunk c: queue chunk c + 1, wait for chunk c
+        if (in_chunk == CH) {  // entering chunk c + 1: queue the one after, wait for this one
+            ++c;
+            in_chunk = 0;
             issue_chunk(c + 1);
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         }
+        const int row_in_chunk = in_chunk++;
         // capacity (all threads read the same header values)
         __syncthreads();
         const long long ns = T.hdr[H_NS], nn = T.hdr[H_NN], dep = T.hdr[H_DEPTH];
@@ -413,17 +420,19 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
             break;
         }
         {
-            const float* xr = xring + (size_t)(c & 1) * CH * d + (size_t)((i - start) - c * CH) * d;
+            const float* xr = xring + (size_t)(c & 1) * CH * d + (size_t)row_in_chunk * d;
             for (int k = threadIdx.x; k < d; k += kFitThreads) xs[k] = (double)xr[k];
         }
         __syncthreads();
-        double xx = 0.0;
-        if (threadIdx.x < 2) xx = dot2(xs, xs, d, threadIdx.x, 0x3u);
-        if (threadIdx.x == 0) sh.scal[0] = xx;
-        __syncthreads();
-        xx = sh.scal[0];
+        double xx = 0.0;  // |x|^2: computed beside the leaf's merge test (not on the descent's path)
         const int root = (int)T.hdr[H_ROOT];
         if (T.nsub[root] == 0) {  // the empty root leaf takes the first point
+            if (threadIdx.x < 2) {
+                xx = dot2(xs, xs, d, threadIdx.x, 0x3u);
+                if (threadIdx.x == 0) sh.scal[0] = xx;
+            }
+            __syncthreads();
+            xx = sh.scal[0];
             if (threadIdx.x == 0) sh.cur = new_entry(T);
             __syncthreads();
             const int s = sh.cur;
@@ -440,10 +449,14 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
         int depth = 0, v = root;
         while (true) {
             const int cnt = T.nsub[v];
-            // every group computes (groups past the node's entries on entry 0, discarded)
-            const int s = T.sub[(int64_t)v * B1 + (g < cnt ? g : 0)];
-            const double dt = dot2(T.cen + (int64_t)s * d, xs, d, r);
-            const double dist = __dadd_rn(T.sqn[s], -2.0 * dt);
+            // one 2-lane group per entry; groups past the node's entries stay idle
+            double dist = INFINITY;
+            const unsigned act = __ballot_sync(kFullMask, g < cnt);
+            if (g < cnt) {
+                const int s = T.sub[(int64_t)v * B1 + g];
+                const double dt = dot2(T.cen + (int64_t)s * T.ldc, xs, d, r, act);
+                dist = __dadd_rn(T.sqn[s], -2.0 * dt);
+            }
             const int j = block_argmin(dist, g, cnt, sh, am_slot);
             if (threadIdx.x == 0) {
                 sh.path_node[depth] = v;
@@ -466,8 +479,10 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
         }
         __syncthreads();
         if (threadIdx.x < 2) {
+            xx = dot2(xs, xs, d, threadIdx.x, 0x3u);  // independent of the next dot: the two overlap
             const double nsq = dot2(tmp + d, tmp + d, d, threadIdx.x, 0x3u);
             if (threadIdx.x == 0) {
+                sh.scal[0] = xx;
                 const double nss = T.ss[sj] + xx;
                 const double r2 = nss / nn1 - nsq;
                 sh.flag = r2 <= T.T2;
@@ -476,11 +491,12 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
             }
         }
         __syncthreads();
+        xx = sh.scal[0];
         int split = 0;
         if (sh.flag) {
             for (int k = threadIdx.x; k < d; k += kFitThreads) {
                 T.ls[(int64_t)sj * d + k] = tmp[k];
-                T.cen[(int64_t)sj * d + k] = tmp[d + k];
+                T.cen[(int64_t)sj * T.ldc + k] = tmp[d + k];
             }
             if (threadIdx.x == 0) {
                 T.n[sj] = nn1;
@@ -522,13 +538,13 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
                 const double nn = T.n[se] + 1.0;
                 const double lsum = T.ls[(int64_t)se * d + k] + xs[k];
                 T.ls[(int64_t)se * d + k] = lsum;
-                T.cen[(int64_t)se * d + k] = lsum / nn;
+                T.cen[(int64_t)se * T.ldc + k] = lsum / nn;
             }
             __syncthreads();
             for (int lv0 = 0; lv0 < nl; lv0 += kFitThreads / 2) {  // one 2-lane group per level
                 const int lv = lv0 + g;
                 const int se = T.sub[(int64_t)sh.path_node[lv < nl ? lv : 0] * B1 + sh.path_j[lv < nl ? lv : 0]];
-                const double q = dot2(T.cen + (int64_t)se * d, T.cen + (int64_t)se * d, d, r);
+                const double q = dot2(T.cen + (int64_t)se * T.ldc, T.cen + (int64_t)se * T.ldc, d, r);
                 if (lv < nl && r == 0) {
                     T.n[se] = T.n[se] + 1.0;
                     T.ss[se] = T.ss[se] + xx;
@@ -578,7 +594,7 @@ __global__ void birch_gather_kernel(TreeDev t, const int32_t* __restrict__ idx, 
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = e / d, k = e % d;
         const int s = idx[j];
-        if (cen) cen[e] = t.cen[(int64_t)s * d + k];
+        if (cen) cen[e] = t.cen[(int64_t)s * t.ldc + k];
         if (ls) ls[e] = t.ls[(int64_t)s * d + k];
         if (k == 0) {
             if (sqn) sqn[j] = t.sqn[s];
@@ -670,7 +686,8 @@ size_t smem_fit(int d, int B) {
 // shared-memory pool capacities (entries, nodes) that fit beside the fit kernel's scratch
 void smem_pool_caps(int d, int B, int max_optin, int64_t* cs, int64_t* cn, size_t* bytes) {
     const size_t base = smem_fit(d, B) + 2048;  // + static shared memory
-    const size_t per_e = sizeof(double) * (2 * (size_t)d + 3) + sizeof(int32_t);
+    const size_t ldc = (d & 1) ? (size_t)d : (size_t)d + 2;  // the kernel's padded centroid stride
+    const size_t per_e = sizeof(double) * ((size_t)d + ldc + 3) + sizeof(int32_t);
     const size_t per_n = sizeof(int32_t) * ((size_t)B + 1 + 4);
     *cs = *cn = 0;
     *bytes = 0;
@@ -780,6 +797,7 @@ igp_status igp_birch_create(int32_t d, double threshold, int32_t branching, igp_
     if (!b) return IGP_ERR_OOM;
     b->device = di.device;
     b->t.d = d;
+    b->t.ldc = d;
     b->t.B = branching;
     b->t.T2 = threshold * threshold;
     cudaStream_t s = 0;
