@@ -720,7 +720,7 @@ igp_status grow(igp_birch_s* b, int64_t cs, int64_t cn, cudaStream_t s) {
     const size_t o_next = off; off = al(off + 4 * (size_t)cn);
     const size_t o_hdr = off; off = al(off + 8 * (size_t)H_WORDS);
     char* p = nullptr;
-    IGP_CUDA(cudaMallocAsync((void**)&p, off, s), "birch pool alloc");
+    IGP_CUDA(alloc_async((void**)&p, off, s), "birch pool alloc");
     TreeDev n = b->t;
     n.n = (double*)(p + o_n);
     n.ls = (double*)(p + o_ls);
@@ -759,10 +759,10 @@ igp_status grow(igp_birch_s* b, int64_t cs, int64_t cn, cudaStream_t s) {
         if (e == cudaSuccess) e = cp(n.next, o.next, 4 * nn);
         if (e == cudaSuccess) e = cp(n.hdr, o.hdr, sizeof(h));
         if (e != cudaSuccess) {
-            cudaFreeAsync(p, s);
+            free_async(p, s);
             return cuda_status(e, "birch pool copy");
         }
-        cudaFreeAsync(b->pool, s);
+        free_async(b->pool, s);
     }
     b->pool = p;
     b->t = n;
@@ -814,7 +814,10 @@ igp_status igp_birch_create(int32_t d, double threshold, int32_t branching, igp_
         if (st == IGP_OK) st = cuda_status(cudaStreamSynchronize(s), "birch sync");
     }
     if (st != IGP_OK) {
-        if (b->pool) cudaFree(b->pool);
+        if (b->pool) {
+            free_async(b->pool, s);
+            cudaStreamSynchronize(s);
+        }
         delete b;
         return st;
     }
@@ -833,12 +836,12 @@ igp_status igp_birch_partial_fit(igp_birch_t b, const float* d_X, int64_t m, igp
     const int d = b->t.d;
     // non-finite rows are an input error: checked on the device before any insert
     int32_t* bad = nullptr;
-    IGP_CUDA(cudaMallocAsync((void**)&bad, sizeof(int32_t), s), "alloc");
+    IGP_CUDA(alloc_async((void**)&bad, sizeof(int32_t), s), "alloc");
     igp_status st = launch_nonfinite_check(d_X, m * (int64_t)d, bad, s);
     int32_t hbad = 0;
     if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s), "readback");
     if (st == IGP_OK) st = cuda_status(cudaStreamSynchronize(s), "sync");
-    cudaFreeAsync(bad, s);
+    free_async(bad, s);
     if (st != IGP_OK) return st;
     if (hbad) {
         set_error("birch: non-finite value in the rows");
@@ -877,13 +880,13 @@ igp_status igp_birch_info(igp_birch_t b, int64_t* num_clusters, int32_t* depth, 
     }
     cudaStream_t s = 0;
     long long* cnt = nullptr;
-    IGP_CUDA(cudaMallocAsync((void**)&cnt, sizeof(long long), s), "alloc");
+    IGP_CUDA(alloc_async((void**)&cnt, sizeof(long long), s), "alloc");
     birch_list_kernel<<<1, 32, 0, s>>>(b->t, nullptr, cnt);
     igp_status st = launch_status("birch_list_kernel");
     long long k = 0, h[H_WORDS] = {0};
     if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(&k, cnt, sizeof(k), cudaMemcpyDeviceToHost, s), "readback");
     if (st == IGP_OK) st = read_hdr(b, h, s);
-    cudaFreeAsync(cnt, s);
+    free_async(cnt, s);
     if (st != IGP_OK) return st;
     if (num_clusters) *num_clusters = k;
     if (depth) *depth = (int32_t)h[H_DEPTH];
@@ -905,8 +908,8 @@ igp_status igp_birch_clusters(igp_birch_t b, double* d_centroids, double* d_sqn,
     cudaStream_t s = (cudaStream_t)stream;
     int32_t* idx = nullptr;
     long long* cnt = nullptr;
-    IGP_CUDA(cudaMallocAsync((void**)&idx, 4 * (size_t)K, s), "alloc");
-    IGP_CUDA(cudaMallocAsync((void**)&cnt, sizeof(long long), s), "alloc");
+    IGP_CUDA(alloc_async((void**)&idx, 4 * (size_t)K, s), "alloc");
+    IGP_CUDA(alloc_async((void**)&cnt, sizeof(long long), s), "alloc");
     birch_list_kernel<<<1, 32, 0, s>>>(b->t, idx, cnt);
     igp_status st = launch_status("birch_list_kernel");
     if (st == IGP_OK) {
@@ -914,8 +917,8 @@ igp_status igp_birch_clusters(igp_birch_t b, double* d_centroids, double* d_sqn,
         birch_gather_kernel<<<grid, 256, 0, s>>>(b->t, idx, K, d_centroids, d_sqn, d_n, d_ls, d_ss);
         st = launch_status("birch_gather_kernel");
     }
-    cudaFreeAsync(idx, s);
-    cudaFreeAsync(cnt, s);
+    free_async(idx, s);
+    free_async(cnt, s);
     return st;
 }
 
@@ -936,8 +939,8 @@ igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m, int32_t
     const int d = b->t.d;
     double* cen = nullptr;
     double* sqn = nullptr;
-    IGP_CUDA(cudaMallocAsync((void**)&cen, 8 * (size_t)K * d, s), "alloc");
-    IGP_CUDA(cudaMallocAsync((void**)&sqn, 8 * (size_t)K, s), "alloc");
+    IGP_CUDA(alloc_async((void**)&cen, 8 * (size_t)K * d, s), "alloc");
+    IGP_CUDA(alloc_async((void**)&sqn, 8 * (size_t)K, s), "alloc");
     igp_status st = igp_birch_clusters(b, cen, sqn, nullptr, nullptr, nullptr, stream);
     if (st == IGP_OK) {
         const size_t smem = sizeof(double) * ((size_t)kPredThreads * (d + 1) + (size_t)kPT * d);
@@ -950,8 +953,8 @@ igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m, int32_t
             st = launch_status("birch_predict_kernel");
         }
     }
-    cudaFreeAsync(cen, s);
-    cudaFreeAsync(sqn, s);
+    free_async(cen, s);
+    free_async(sqn, s);
     return st;
 }
 
@@ -960,8 +963,8 @@ igp_status igp_birch_destroy(igp_birch_t b) {
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != b->device) cudaSetDevice(b->device);
-    cudaStreamSynchronize(0);
-    if (b->pool) cudaFree(b->pool);
+    cudaStreamSynchronize(0);  // the tree's calls are synchronous or ordered on the caller's stream
+    if (b->pool) free_async(b->pool, 0);
     if (prev >= 0 && prev != b->device) cudaSetDevice(prev);
     delete b;
     return IGP_OK;
