@@ -607,27 +607,35 @@ __global__ void birch_gather_kernel(TreeDev t, const int32_t* __restrict__ idx, 
 // label_i = argmin_j sqn_j - 2 dot(c_j, x_i) (first minimum; the oracle's dot order).  128 points per block (one per
 // thread), cluster tiles of kPT centroids staged in shared memory; the point's row lives in
 // shared memory too (stride d + 1).
-constexpr int kPredThreads = 128;
-constexpr int kPT = 16;
+constexpr int kPredThreads = 128;  // points per block (fewer for wide rows, see igp_birch_predict)
+constexpr int kPT = 16;            // centroids per shared-memory tile
+// XS: the block's rows are staged in shared memory (stride d + 1); otherwise (very wide rows)
+// each thread reads its row from global memory (L1-cached)
+template <bool XS>
 __global__ void __launch_bounds__(kPredThreads) birch_predict_kernel(const double* __restrict__ cen,
                                                                     const double* __restrict__ sqn, int64_t K, int d,
                                                                     const float* __restrict__ X, int64_t m,
                                                                     int32_t* __restrict__ labels) {
     extern __shared__ double pred_smem[];
-    double* xs = pred_smem;                              // [128][d + 1]
-    double* cs = pred_smem + (size_t)kPredThreads * (d + 1);  // [kPT][d]
-    const int64_t i0 = (int64_t)blockIdx.x * kPredThreads;
-    for (int e = threadIdx.x; e < kPredThreads * d; e += kPredThreads) {
-        const int p = e / d, k = e % d;
-        xs[p * (d + 1) + k] = (i0 + p < m) ? (double)X[(i0 + p) * d + k] : 0.0;
+    const int P = blockDim.x;
+    double* cs = pred_smem;                   // [kPT][d]
+    double* xs = pred_smem + (size_t)kPT * d;  // [P][d + 1] (XS)
+    const int64_t i0 = (int64_t)blockIdx.x * P;
+    if (XS) {
+        for (int e = threadIdx.x; e < P * d; e += P) {
+            const int p = e / d, k = e % d;
+            xs[p * (d + 1) + k] = (i0 + p < m) ? (double)X[(i0 + p) * d + k] : 0.0;
+        }
     }
-    const double* x = xs + threadIdx.x * (d + 1);
+    const int64_t row = i0 + threadIdx.x < m ? i0 + threadIdx.x : m - 1;
+    const double* x = XS ? xs + threadIdx.x * (d + 1) : nullptr;
+    const float* xg = X + row * d;
     double best = INFINITY;
     int64_t bj = 0;
     for (int64_t j0 = 0; j0 < K; j0 += kPT) {
         const int nt = (int)(K - j0 < kPT ? K - j0 : kPT);
         __syncthreads();
-        for (int e = threadIdx.x; e < nt * d; e += kPredThreads) cs[e] = cen[j0 * d + e];
+        for (int e = threadIdx.x; e < nt * d; e += P) cs[e] = cen[j0 * d + e];
         __syncthreads();
         for (int jj = 0; jj < nt; ++jj) {
             const double* c = cs + jj * d;
@@ -635,9 +643,9 @@ __global__ void __launch_bounds__(kPredThreads) birch_predict_kernel(const doubl
             int k = 0;
             for (; k + 8 <= d; k += 8) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) p[q] = __fma_rn(c[k + q], x[k + q], p[q]);
+                for (int q = 0; q < 8; ++q) p[q] = __fma_rn(c[k + q], XS ? x[k + q] : (double)xg[k + q], p[q]);
             }
-            for (; k < d; ++k) p[k & 7] = __fma_rn(c[k], x[k], p[k & 7]);
+            for (; k < d; ++k) p[k & 7] = __fma_rn(c[k], XS ? x[k] : (double)xg[k], p[k & 7]);
             const double dt = __dadd_rn(__dadd_rn(__dadd_rn(p[0], p[1]), __dadd_rn(p[2], p[3])),
                                         __dadd_rn(__dadd_rn(p[4], p[5]), __dadd_rn(p[6], p[7])));
             const double dist = __dadd_rn(sqn[j0 + jj], -2.0 * dt);
@@ -943,13 +951,19 @@ igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m, int32_t
     IGP_CUDA(alloc_async((void**)&sqn, 8 * (size_t)K, s), "alloc");
     igp_status st = igp_birch_clusters(b, cen, sqn, nullptr, nullptr, nullptr, stream);
     if (st == IGP_OK) {
-        const size_t smem = sizeof(double) * ((size_t)kPredThreads * (d + 1) + (size_t)kPT * d);
-        st = cuda_status(cudaFuncSetAttribute(birch_predict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)smem),
+        // points per block: as many (<= 128, multiple of 32) as fit in shared memory with their rows
+        const size_t budget = 200 * 1024, tile = sizeof(double) * (size_t)kPT * d;
+        int P = kPredThreads;
+        while (P > 32 && tile + sizeof(double) * (size_t)P * (d + 1) > budget) P -= 32;
+        const bool xs = tile + sizeof(double) * (size_t)P * (d + 1) <= budget;
+        if (!xs) P = kPredThreads;
+        const size_t smem = tile + (xs ? sizeof(double) * (size_t)P * (d + 1) : 0);
+        auto kern = xs ? birch_predict_kernel<true> : birch_predict_kernel<false>;
+        st = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                          "predict smem attribute");
         if (st == IGP_OK) {
-            const int64_t grid = (m + kPredThreads - 1) / kPredThreads;
-            birch_predict_kernel<<<(unsigned)grid, kPredThreads, smem, s>>>(cen, sqn, K, d, d_X, m, d_labels);
+            const int64_t grid = (m + P - 1) / P;
+            kern<<<(unsigned)grid, P, smem, s>>>(cen, sqn, K, d, d_X, m, d_labels);
             st = launch_status("birch_predict_kernel");
         }
     }

@@ -73,6 +73,8 @@ def datasets():
         ("sigmoid16_B5", 1 / (1 + np.exp(-rng.normal(0, 1, (3000, 16)))), 0.3, 5),
         ("odd_width_d37", 1 / (1 + np.exp(-rng.normal(0, 1, (1200, 37)))), 0.4, 7),
         ("wide_d200_B63", rng.random((800, 200)), 2.0, 63),
+        ("wide_d256", rng.random((700, 256)), 3.0, 20),     # predict: fewer rows per block
+        ("max_d1024", rng.random((300, 1024)), 6.0, 10),    # predict rows from global memory; no shared pool
         ("single_point", np.array([[0.25, -0.5, 0.75]]), 0.5, 50),
         ("duplicates", np.repeat(rng.random((5, 6)), 40, axis=0), 0.05, 4),
     ]
