@@ -354,6 +354,33 @@ def run_selftest_cpu(args, cfg):
     return 0
 
 
+def birch_leg(args, igp, out, stream, dev, N, d, oracle_ref):
+    """igp_birch_partial_fit + igp_birch_predict on the step's embedding (Alg. 1 l.7)."""
+    import torch
+    torch.cuda.synchronize(dev)
+    b0 = time.perf_counter()
+    bt = igp.Birch(d, args.birch_threshold, args.birch_branching, device=dev).partial_fit(out, stream=stream)
+    fit_s = time.perf_counter() - b0
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    bt.predict(out, stream=stream)
+    p1.record(stream)
+    torch.cuda.synchronize(dev)
+    K, depth, nodes, pts = bt.info()
+    bt.close()
+    rec = {"fit_s": fit_s, "predict_ms": p0.elapsed_time(p1), "clusters": K, "depth": depth,
+           "threshold": args.birch_threshold, "branching": args.birch_branching, "rows": pts,
+           "us_per_row": fit_s / max(pts, 1) * 1e6,
+           "what": "igp_birch_partial_fit (CF-tree build, one persistent CTA, fp64) + igp_birch_predict on the "
+                   "step's embedding; not part of the timed step"}
+    if oracle_ref:
+        rows = min(N, args.birch_oracle_rows)
+        secs, n_rows = birch_oracle_time(out.cpu().numpy(), args.birch_threshold, args.birch_branching, rows)
+        rec["oracle"] = {"s": secs, "rows": n_rows, "cores": 1, "us_per_row": secs / n_rows * 1e6,
+                         "note": "oracle fit + predict on the first rows of the same embedding"}
+    return rec
+
+
 # ---------------------------------------------------------------- GPU arm
 def run_gpu(args, cfg):
     import torch
@@ -561,26 +588,11 @@ def run_gpu(args, cfg):
     # the downstream BIRCH (Alg. 1 l.7) on this step's embedding: reported beside the FFP, not
     # part of the step; the oracle's BIRCH on the same rows (one thread) is its reference
     if not args.no_birch:
-        torch.cuda.synchronize(dev)
-        b0 = time.perf_counter()
-        bt = igp.Birch(d, args.birch_threshold, args.birch_branching, device=dev).partial_fit(out, stream=stream)
-        fit_s = time.perf_counter() - b0
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        bt.predict(out, stream=stream)
-        p1.record(stream)
-        torch.cuda.synchronize(dev)
-        K, depth, nodes, pts = bt.info()
-        bt.close()
-        line["birch"] = {"fit_s": fit_s, "predict_ms": p0.elapsed_time(p1), "clusters": K, "depth": depth,
-                         "threshold": args.birch_threshold, "branching": args.birch_branching, "rows": pts,
-                         "what": "igp_birch_partial_fit (CF-tree build, one persistent CTA, fp64) + igp_birch_predict "
-                                 "on the step's embedding; not part of the timed step"}
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            rows = min(N, args.birch_oracle_rows)
-            secs, n_rows = birch_oracle_time(out.cpu().numpy(), args.birch_threshold, args.birch_branching, rows)
-            line["birch"]["oracle"] = {"s": secs, "rows": n_rows, "cores": 1,
-                                       "rows_per_s": n_rows / secs, "gpu_rows_per_s": pts / (fit_s + p0.elapsed_time(p1) / 1e3)}
+        try:  # a failure here must not cost the bench line: it is reported instead
+            line["birch"] = birch_leg(args, igp, out, stream, dev, N, d,
+                                      oracle_ref=rank == 0 and world == 1 and not args.no_cpu_baseline)
+        except Exception as exc:  # noqa: BLE001
+            line["birch"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = cpu_cores()

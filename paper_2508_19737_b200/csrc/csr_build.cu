@@ -690,35 +690,58 @@ igp_status stable_sort_pairs(int32_t n, int key_bits, const PairSortScratch& sc,
 }  // namespace
 
 // Streaming merge (Alg. 2 l.1): row r of the union = the sorted, duplicate-free
-// merge of the base graph's canonical row (sorted, unique) and the new edges' row (sorted and
-// deduplicated on their own first).  One thread per row, two-pointer merge; a counting pass
-// sizes the rows, a writing pass fills the final CSR directly.
-template <bool WRITE>
-__global__ void merge_rows_kernel(const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
-                                  const int32_t* __restrict__ noff, const int32_t* __restrict__ ndata,
-                                  const int32_t* __restrict__ ncnt, int32_t n, int32_t* __restrict__ ucnt,
-                                  const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx) {
+// merge of the base graph's canonical row B (sorted, unique) and the new edges' row U (sorted and
+// deduplicated on their own first).
+//  - merge_count_kernel (one thread per row): drops the entries of U already in B (binary search),
+//    compacting the rest U' in place; |row| = |B| + |U'|.
+//  - merge_write_kernel (one warp per row): B[i] goes to position i + #{U' < B[i]}, U'[j] to
+//    j + #{B < U'[j]}: both sides written straight into the final CSR, B read coalesced.
+__device__ __forceinline__ int32_t lower_bound_i32(const int32_t* __restrict__ a, int32_t n, int32_t x) {
+    int32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void merge_count_kernel(const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                                   const int32_t* __restrict__ noff, int32_t* __restrict__ ndata,
+                                   int32_t* __restrict__ ncnt, int32_t n, int32_t* __restrict__ ucnt) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += stride) {
-        int32_t i = brp[r];
-        const int32_t i1 = brp[r + 1];
-        int32_t j = noff[r];
-        const int32_t j1 = j + ncnt[r];
-        int32_t k = WRITE ? row_ptr[r] : 0;
-        const int32_t k0 = k;
-        while (i < i1 && j < j1) {
-            const int32_t x = bci[i], y = ndata[j];
-            const int32_t v = x < y ? x : y;
-            i += x <= y;
-            j += y <= x;
-            if (WRITE) col_idx[k] = v;
-            ++k;
+        const int32_t b0 = brp[r], nb = brp[r + 1] - b0;
+        const int32_t u0 = noff[r], nu = ncnt[r];
+        int32_t w = 0;
+        for (int32_t j = 0; j < nu; ++j) {
+            const int32_t u = ndata[u0 + j];
+            const int32_t pos = lower_bound_i32(bci + b0, nb, u);
+            if (pos == nb || bci[b0 + pos] != u) ndata[u0 + w++] = u;  // not in B: kept (in order)
         }
-        for (; i < i1; ++i, ++k)
-            if (WRITE) col_idx[k] = bci[i];
-        for (; j < j1; ++j, ++k)
-            if (WRITE) col_idx[k] = ndata[j];
-        if (!WRITE) ucnt[r] = k - k0;
+        ncnt[r] = w;
+        ucnt[r] = nb + w;
+    }
+}
+
+__global__ void merge_write_kernel(const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                                   const int32_t* __restrict__ noff, const int32_t* __restrict__ ndata,
+                                   const int32_t* __restrict__ ncnt, int32_t n, const int32_t* __restrict__ row_ptr,
+                                   int32_t* __restrict__ col_idx) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nwarps) {
+        const int32_t b0 = brp[r], nb = brp[r + 1] - b0;
+        const int32_t* U = ndata + noff[r];
+        const int32_t nu = ncnt[r];
+        int32_t* out = col_idx + row_ptr[r];
+        for (int32_t i = lane; i < nb; i += 32) {
+            const int32_t x = bci[b0 + i];
+            out[i + lower_bound_i32(U, nu, x)] = x;
+        }
+        for (int32_t j = lane; j < nu; j += 32) {
+            const int32_t u = U[j];
+            out[j + lower_bound_i32(bci + b0, nb, u)] = u;
+        }
     }
 }
 
@@ -894,15 +917,14 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     IGP_STEP(segmented_sort(off, tmp, base ? cnt : ucnt, n, 2 * E, n, sc, s, di));
     if (base) {
         // streaming merge: the base rows are already canonical; merge each with its sorted new
-        // run (no re-sort of the base), counting first, then writing the final rows
+        // run (no re-sort of the base): count (dropping new entries already present), then write
+        // both sides at their merged positions
         const int tg = grid_for(n, 256, di.num_sms, 8);
-        merge_rows_kernel<false><<<tg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, ucnt, nullptr,
-                                                    nullptr);
-        IGP_STEP(launch_status("merge_rows_kernel<count>"));
+        merge_count_kernel<<<tg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, ucnt);
+        IGP_STEP(launch_status("merge_count_kernel"));
         IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
-        merge_rows_kernel<true><<<tg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, nullptr,
-                                                   c.row_ptr, c.col_idx);
-        IGP_STEP(launch_status("merge_rows_kernel<write>"));
+        merge_write_kernel<<<rg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, c.row_ptr, c.col_idx);
+        IGP_STEP(launch_status("merge_write_kernel"));
     } else {
         // B5: row pointers, compaction
         IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
