@@ -179,7 +179,7 @@ def load_traffic(config_name):
 def l2_policy(cfg, nnz, l2_bytes):
     """How the timing rule on L2 is met for this config (stated in config.l2): inputs larger than
     L2, or an explicit L2 flush between timed steps."""
-    edges_b = 8 * (cfg.num_edges if cfg.name != "streaming" else cfg.num_edges)
+    edges_b = 8 * cfg.num_edges  # int32 (u, v) pairs (streaming: all 10 stages' batches stay resident)
     z_b = 4 * cfg.num_nodes * cfg.d
     csr_b = 4 * nnz + 4 * (cfg.num_nodes + 1)
     foot = edges_b + z_b + csr_b

@@ -239,7 +239,8 @@ IGP_API igp_status igp_philox_normal(uint64_t seed, uint64_t subsequence, int64_
  * row order; its leaf entries, in leaf-chain order, are the K-agnostic clusters, and a
  * row's label is the index of its nearest leaf centroid.  fp64 on the device, with the
  * exact operation order of oracle/birch_oracle.c (readings B1-B6), so trees,
- * clusters and labels are bitwise reproducible.
+ * clusters and labels are bitwise reproducible.  A tree is single-writer: calls on the same
+ * igp_birch_t must not run concurrently (predict is read-only once fitting stops).
  * ------------------------------------------------------------------------- */
 typedef struct igp_birch_s* igp_birch_t;
 
