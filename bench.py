@@ -381,6 +381,48 @@ def birch_leg(args, igp, out, stream, dev, N, d, oracle_ref):
     return rec
 
 
+def streaming_alg2_leg(args, igp, batches, N, d, L, tau, seed, stream, dev):
+    """Alg. 2 end to end on the streaming config, after the timed region: per
+    stage t, merge (l.1) and re-embed with a fresh draw (l.2-7), extract the rows of the nodes that
+    arrived at stage t (their first edge; l.8), partially fit BIRCH with them (l.9), append them to
+    the kept embeddings (l.10) and predict every arrived node (l.11).  Row extraction and appending
+    are bench-side tensor plumbing; every step of the method runs in the library."""
+    import torch
+    out = torch.empty((N, d), dtype=torch.float32, device=dev)
+    kept = torch.empty((N, d), dtype=torch.float32, device=dev)  # Z^hat: rows of arrived nodes
+    seen = torch.zeros(N, dtype=torch.bool, device=dev)
+    bt = igp.Birch(d, args.birch_threshold, args.birch_branching, device=dev)
+    g = igp.build_graph(batches[0], N, stream=stream)
+    rec = []
+    n_kept = 0
+    for t in range(10):
+        if t > 0:
+            g.add_edges(batches[t], stream=stream)
+        igp.embed(g, tau, d, L, seed, out=out, stream=stream, subsequence=t)
+        _, _, deg = g.csr(stream=stream, degrees=True)
+        new = torch.nonzero((deg > 0) & ~seen).flatten()
+        seen[new] = True
+        kept[n_kept:n_kept + new.numel()] = out[new]  # l.8 + l.10 (append)
+        torch.cuda.synchronize(dev)
+        f0 = time.perf_counter()
+        if new.numel():
+            bt.partial_fit(kept[n_kept:n_kept + new.numel()], stream=stream)  # l.9 (synchronous)
+        fit_ms = (time.perf_counter() - f0) * 1e3
+        n_kept += new.numel()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        bt.predict(kept[:n_kept], stream=stream)  # l.11
+        p1.record(stream)
+        torch.cuda.synchronize(dev)
+        K = bt.info()[0]
+        rec.append({"stage": t, "new_nodes": int(new.numel()), "partial_fit_ms": fit_ms,
+                    "predict_ms": p0.elapsed_time(p1), "clusters": K})
+    g.close()
+    bt.close()
+    return {"stages": rec, "threshold": args.birch_threshold, "branching": args.birch_branching,
+            "new_nodes": "nodes whose first edge arrives at stage t (edge-arrival stream)"}
+
+
 # ---------------------------------------------------------------- GPU arm
 def run_gpu(args, cfg):
     import torch
@@ -558,6 +600,11 @@ def run_gpu(args, cfg):
     if embed_ms is not None:
         extra.update({"embed_ms": embed_ms, "build_ms": t_max / args.steps - embed_ms})
     if stages is not None:
+        if not args.no_birch:
+            try:
+                extra["alg2_birch"] = streaming_alg2_leg(args, igp, batches, N, d, L, tau, seed, stream, dev)
+            except Exception as exc:  # noqa: BLE001
+                extra["alg2_birch"] = {"error": f"{type(exc).__name__}: {exc}"}
         extra["stages"] = stages
         extra["fresh_build_of_final_graph_ms"] = fresh_build_ms
         extra["merge_stage9_vs_fresh_build"] = stages[9]["build_or_merge_ms"] / fresh_build_ms
