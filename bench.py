@@ -354,6 +354,22 @@ def run_selftest_cpu(args, cfg):
     return 0
 
 
+def predict_times(bt, X, stream, dev, fp64=True):
+    """igp_birch_predict (auto path: tensor cores where d allows) timed with CUDA events on the
+    stream, the rows it left to fp64, and (fp64=True) the all-fp64 path's time beside it."""
+    import torch
+    rec = {}
+    for path in ("auto", "fp64") if fp64 else ("auto",):
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        bt.predict(X, stream=stream, path=path)
+        p1.record(stream)
+        torch.cuda.synchronize(dev)
+        rec["predict_ms" if path == "auto" else "predict_fp64_ms"] = p0.elapsed_time(p1)
+    _, rec["predict_rows_fp64"] = bt.predict(X, stream=stream, return_ambiguous=True)
+    return rec
+
+
 def birch_leg(args, igp, out, stream, dev, N, d, oracle_ref):
     """igp_birch_partial_fit + igp_birch_predict on the step's embedding (Alg. 1 l.7)."""
     import torch
@@ -361,14 +377,10 @@ def birch_leg(args, igp, out, stream, dev, N, d, oracle_ref):
     b0 = time.perf_counter()
     bt = igp.Birch(d, args.birch_threshold, args.birch_branching, device=dev).partial_fit(out, stream=stream)
     fit_s = time.perf_counter() - b0
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    bt.predict(out, stream=stream)
-    p1.record(stream)
-    torch.cuda.synchronize(dev)
+    times = predict_times(bt, out, stream, dev)
     K, depth, nodes, pts = bt.info()
     bt.close()
-    rec = {"fit_s": fit_s, "predict_ms": p0.elapsed_time(p1), "clusters": K, "depth": depth,
+    rec = {"fit_s": fit_s, **times, "clusters": K, "depth": depth,
            "threshold": args.birch_threshold, "branching": args.birch_branching, "rows": pts,
            "us_per_row": fit_s / max(pts, 1) * 1e6,
            "what": "igp_birch_partial_fit (CF-tree build, one persistent CTA, fp64) + igp_birch_predict on the "
@@ -409,14 +421,9 @@ def streaming_alg2_leg(args, igp, batches, N, d, L, tau, seed, stream, dev):
             bt.partial_fit(kept[n_kept:n_kept + new.numel()], stream=stream)  # l.9 (synchronous)
         fit_ms = (time.perf_counter() - f0) * 1e3
         n_kept += new.numel()
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        bt.predict(kept[:n_kept], stream=stream)  # l.11
-        p1.record(stream)
-        torch.cuda.synchronize(dev)
+        times = predict_times(bt, kept[:n_kept], stream, dev, fp64=(t == 9))  # l.11
         K = bt.info()[0]
-        rec.append({"stage": t, "new_nodes": int(new.numel()), "partial_fit_ms": fit_ms,
-                    "predict_ms": p0.elapsed_time(p1), "clusters": K})
+        rec.append({"stage": t, "new_nodes": int(new.numel()), "partial_fit_ms": fit_ms, **times, "clusters": K})
     g.close()
     bt.close()
     return {"stages": rec, "threshold": args.birch_threshold, "branching": args.birch_branching,

@@ -268,10 +268,28 @@ IGP_API igp_status igp_birch_clusters(igp_birch_t b, double* d_centroids, double
                                       double* d_ss, igp_stream_t stream);
 
 /* Labels (Alg. 2 l.11): d_labels[i] = argmin_j |c_j|^2 - 2 c_j . x_i over the K clusters
- * (first minimum; |x_i|^2 is common to all j, reading B5), device int32 [m].  Does not
- * modify the tree.  Empty tree -> IGP_ERR_INPUT.  Asynchronous on `stream`. */
+ * (first minimum; |x_i|^2 is common to all j, reading B5; fp64, bit-identical to the oracle),
+ * device int32 [m].  Does not modify the tree.  Empty tree -> IGP_ERR_INPUT.  Runs the
+ * tensor-core path where d allows (igp_birch_predict_ex, IGP_PREDICT_AUTO), which synchronises
+ * `stream` once to size its fp64 pass; the fp64 path is asynchronous on `stream`. */
 IGP_API igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m, int32_t* d_labels,
                                      igp_stream_t stream);
+
+/* igp_birch_predict with a choice of arithmetic (same labels either way):
+ *   IGP_PREDICT_FP64   every distance in fp64 on the CUDA cores, in the oracle's order;
+ *   IGP_PREDICT_TENSOR the scores c_j . x_i on the tensor cores (tcgen05, 3xTF32 split),
+ *                      each row's argmin certified by an error margin; rows whose best and
+ *                      second-best approximate distances lie within twice the margin (near or
+ *                      exact ties) are re-solved in fp64 as above.  Needs d a multiple of 8 in
+ *                      [8, 64] (else IGP_ERR_INPUT);
+ *   IGP_PREDICT_AUTO   TENSOR where eligible, else FP64 (what igp_birch_predict does).
+ * ambiguous (host, may be NULL) receives the number of rows solved in fp64: the uncertified
+ * rows on the tensor path (the call then synchronises `stream` to read it), m on the FP64 path. */
+#define IGP_PREDICT_AUTO 0
+#define IGP_PREDICT_FP64 1
+#define IGP_PREDICT_TENSOR 2
+IGP_API igp_status igp_birch_predict_ex(igp_birch_t b, const float* d_X, int64_t m, int32_t* d_labels, int32_t path,
+                                        int64_t* ambiguous, igp_stream_t stream);
 
 /* Release the tree (waits for the legacy default stream).  NULL is a no-op. */
 IGP_API igp_status igp_birch_destroy(igp_birch_t b);

@@ -71,6 +71,7 @@ SIGNATURES = {
                                       ctypes.POINTER(_i64)]),
     "igp_birch_clusters": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "igp_birch_predict": (ctypes.c_int, [_P, _P, _i64, _P, _P]),
+    "igp_birch_predict_ex": (ctypes.c_int, [_P, _P, _i64, _P, _i32, ctypes.POINTER(_i64), _P]),
     "igp_birch_destroy": (ctypes.c_int, [_P]),
     "igp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "igp_last_error_message": (ctypes.c_char_p, []),
@@ -342,15 +343,28 @@ class Birch:
             _check(_lib.igp_birch_clusters(self._h, ptr(cen), ptr(sqn), ptr(n), ptr(ls), ptr(ss), _stream_ptr(stream)))
         return cen, sqn, n, ls, ss
 
-    def predict(self, X: torch.Tensor, stream=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    PATHS = {"auto": 0, "fp64": 1, "tensor": 2}  # IGP_PREDICT_*
+
+    def predict(self, X: torch.Tensor, stream=None, out: torch.Tensor | None = None, path: str = "auto",
+                return_ambiguous: bool = False):
+        """Labels (int32 [m]).  path: "fp64" (CUDA cores, every distance in fp64), "tensor"
+        (tcgen05 3xTF32 scores, certified; uncertified rows re-solved in fp64), "auto" (tensor
+        where d allows).  The labels are the same on every path.  With return_ambiguous, also
+        the number of rows solved in fp64 (synchronises)."""
         X = self._rows(X)
+        if path not in self.PATHS:
+            raise ValueError(f"path must be one of {sorted(self.PATHS)}")
         if out is None:
             out = torch.empty(X.shape[0], dtype=torch.int32, device=self.device)
         _require_cuda(out, torch.int32, "out")
+        if out.dim() != 1 or out.shape[0] < X.shape[0]:
+            raise ValueError("out must be int32 [m]")
+        amb = _i64()
         with torch.cuda.device(self.device):
-            _check(_lib.igp_birch_predict(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[0],
-                                          ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
-        return out
+            _check(_lib.igp_birch_predict_ex(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[0],
+                                             ctypes.c_void_p(out.data_ptr()), self.PATHS[path],
+                                             ctypes.byref(amb) if return_ambiguous else None, _stream_ptr(stream)))
+        return (out, amb.value) if return_ambiguous else out
 
     def close(self):
         if getattr(self, "_h", None) is not None:

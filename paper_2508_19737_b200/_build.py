@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libigp.so")
-SOURCES = ["csr_build.cu", "philox.cu", "embed.cu", "igp_api.cu", "birch.cu"]
+SOURCES = ["csr_build.cu", "philox.cu", "embed.cu", "igp_api.cu", "birch.cu", "birch_tc.cu"]
 HEADERS = ["igp_internal.cuh", "philox.cuh"]
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -606,34 +606,42 @@ __global__ void birch_gather_kernel(TreeDev t, const int32_t* __restrict__ idx, 
 
 // label_i = argmin_j sqn_j - 2 dot(c_j, x_i) (first minimum; the oracle's dot order).  128 points per block (one per
 // thread), cluster tiles of kPT centroids staged in shared memory; the point's row lives in
-// shared memory too (stride d + 1).
-constexpr int kPredThreads = 128;  // points per block (fewer for wide rows, see igp_birch_predict)
+// shared memory too (stride d + 1).  Rows: 0 .. n-1, or list[0 .. n) (the rows the tensor-core
+// pass could not certify, birch_tc.cu).  Clusters: blockIdx.y's range [y kchunk, (y+1) kchunk);
+// with several ranges (few rows: the grid would not fill the GPU) each block writes its range's
+// (distance, index) to part_d / part_j [y][n] and birch_argmin_merge_kernel picks the minimum.
+constexpr int kPredThreads = 128;  // points per block (fewer for wide rows, see launch_predict_fp64)
 constexpr int kPT = 16;            // centroids per shared-memory tile
 // XS: the block's rows are staged in shared memory (stride d + 1); otherwise (very wide rows)
 // each thread reads its row from global memory (L1-cached)
 template <bool XS>
 __global__ void __launch_bounds__(kPredThreads) birch_predict_kernel(const double* __restrict__ cen,
                                                                     const double* __restrict__ sqn, int64_t K, int d,
-                                                                    const float* __restrict__ X, int64_t m,
-                                                                    int32_t* __restrict__ labels) {
+                                                                    const float* __restrict__ X, int64_t n,
+                                                                    const int32_t* __restrict__ list, int64_t kchunk,
+                                                                    int32_t* __restrict__ labels,
+                                                                    double* __restrict__ part_d,
+                                                                    int32_t* __restrict__ part_j) {
     extern __shared__ double pred_smem[];
     const int P = blockDim.x;
+    const int64_t i0 = (int64_t)blockIdx.x * P;
+    auto row_of = [&](int64_t i) -> int64_t { return list ? (int64_t)list[i] : i; };
     double* cs = pred_smem;                   // [kPT][d]
     double* xs = pred_smem + (size_t)kPT * d;  // [P][d + 1] (XS)
-    const int64_t i0 = (int64_t)blockIdx.x * P;
     if (XS) {
         for (int e = threadIdx.x; e < P * d; e += P) {
             const int p = e / d, k = e % d;
-            xs[p * (d + 1) + k] = (i0 + p < m) ? (double)X[(i0 + p) * d + k] : 0.0;
+            xs[p * (d + 1) + k] = (i0 + p < n) ? (double)X[row_of(i0 + p) * d + k] : 0.0;
         }
     }
-    const int64_t row = i0 + threadIdx.x < m ? i0 + threadIdx.x : m - 1;
+    const int64_t i = i0 + threadIdx.x < n ? i0 + threadIdx.x : n - 1;
     const double* x = XS ? xs + threadIdx.x * (d + 1) : nullptr;
-    const float* xg = X + row * d;
+    const float* xg = X + row_of(i) * d;
+    const int64_t jb = (int64_t)blockIdx.y * kchunk, je = jb + kchunk < K ? jb + kchunk : K;
     double best = INFINITY;
-    int64_t bj = 0;
-    for (int64_t j0 = 0; j0 < K; j0 += kPT) {
-        const int nt = (int)(K - j0 < kPT ? K - j0 : kPT);
+    int64_t bj = jb;
+    for (int64_t j0 = jb; j0 < je; j0 += kPT) {
+        const int nt = (int)(je - j0 < kPT ? je - j0 : kPT);
         __syncthreads();
         for (int e = threadIdx.x; e < nt * d; e += P) cs[e] = cen[j0 * d + e];
         __syncthreads();
@@ -655,7 +663,31 @@ __global__ void __launch_bounds__(kPredThreads) birch_predict_kernel(const doubl
             }
         }
     }
-    if (i0 + threadIdx.x < m) labels[i0 + threadIdx.x] = (int32_t)bj;
+    if (i0 + threadIdx.x < n) {
+        if (part_d) {
+            part_d[(int64_t)blockIdx.y * n + i] = best;
+            part_j[(int64_t)blockIdx.y * n + i] = (int32_t)bj;
+        } else {
+            labels[row_of(i)] = (int32_t)bj;
+        }
+    }
+}
+
+// the minimum over the cluster ranges, first range on ties (= the first minimum overall)
+__global__ void birch_argmin_merge_kernel(const double* __restrict__ part_d, const int32_t* __restrict__ part_j, int ks,
+                                          int64_t n, const int32_t* __restrict__ list, int32_t* __restrict__ labels) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double best = part_d[i];
+        int32_t bj = part_j[i];
+        for (int y = 1; y < ks; ++y) {
+            const double v = part_d[(int64_t)y * n + i];
+            if (v < best) {
+                best = v;
+                bj = part_j[(int64_t)y * n + i];
+            }
+        }
+        labels[list ? (int64_t)list[i] : i] = bj;
+    }
 }
 
 __global__ void nonfinite_kernel(const float* __restrict__ X, int64_t count, int32_t* bad) {
@@ -781,6 +813,50 @@ igp_status read_hdr(igp_birch_s* b, long long* h, cudaStream_t s) {
     IGP_CUDA(cudaMemcpyAsync(h, b->t.hdr, sizeof(long long) * H_WORDS, cudaMemcpyDeviceToHost, s), "birch header");
     IGP_CUDA(cudaStreamSynchronize(s), "birch sync");
     return IGP_OK;
+}
+
+// the fp64 kernel over n rows (all rows, or the listed ones): points per block as many (<= 128,
+// multiple of 32) as fit in shared memory with their rows; when the row blocks alone would not
+// fill the GPU, the clusters are split into ranges (grid y) and merged by a second kernel
+igp_status launch_predict_fp64(const double* cen, const double* sqn, int64_t K, int d, const float* X, int64_t n,
+                               const int32_t* list, int32_t* labels, cudaStream_t s) {
+    const size_t budget = 200 * 1024, tile = sizeof(double) * (size_t)kPT * d;
+    int P = kPredThreads;
+    while (P > 32 && tile + sizeof(double) * (size_t)P * (d + 1) > budget) P -= 32;
+    const bool xs = tile + sizeof(double) * (size_t)P * (d + 1) <= budget;
+    if (!xs) P = kPredThreads;
+    const size_t smem = tile + (xs ? sizeof(double) * (size_t)P * (d + 1) : 0);
+    auto kern = xs ? birch_predict_kernel<true> : birch_predict_kernel<false>;
+    IGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "predict smem attribute");
+    DeviceInfo di;
+    if (!device_info(&di)) return IGP_ERR_CUDA;
+    const int64_t rb = (n + P - 1) / P, want = (int64_t)di.num_sms * 4;
+    int64_t ks = rb >= want ? 1 : std::min<int64_t>((want + rb - 1) / rb, (K + 255) / 256);
+    if (ks < 1) ks = 1;
+    if (ks > 65535) ks = 65535;
+    int64_t kchunk = (K + ks - 1) / ks;
+    kchunk = (kchunk + kPT - 1) / kPT * kPT;
+    ks = (K + kchunk - 1) / kchunk;
+    double* pd = nullptr;
+    int32_t* pj = nullptr;
+    if (ks > 1) {
+        IGP_CUDA(alloc_async((void**)&pd, sizeof(double) * (size_t)ks * n, s), "alloc");
+        igp_status st = cuda_status(alloc_async((void**)&pj, sizeof(int32_t) * (size_t)ks * n, s), "alloc");
+        if (st != IGP_OK) {
+            free_async(pd, s);
+            return st;
+        }
+    }
+    kern<<<dim3((unsigned)rb, (unsigned)ks), P, smem, s>>>(cen, sqn, K, d, X, n, list, kchunk, labels, pd, pj);
+    igp_status st = launch_status("birch_predict_kernel");
+    if (st == IGP_OK && ks > 1) {
+        birch_argmin_merge_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(pd, pj, (int)ks, n,
+                                                                                                   list, labels);
+        st = launch_status("birch_argmin_merge_kernel");
+    }
+    if (pd) free_async(pd, s);
+    if (pj) free_async(pj, s);
+    return st;
 }
 
 }  // namespace
@@ -930,10 +1006,15 @@ igp_status igp_birch_clusters(igp_birch_t b, double* d_centroids, double* d_sqn,
     return st;
 }
 
-igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m, int32_t* d_labels, igp_stream_t stream) {
+igp_status igp_birch_predict_ex(igp_birch_t b, const float* d_X, int64_t m, int32_t* d_labels, int32_t path,
+                                int64_t* ambiguous, igp_stream_t stream) {
     set_error("");
     if (!b || m < 0 || (m > 0 && (!d_X || !d_labels))) {
         set_error("birch handle or buffers invalid");
+        return IGP_ERR_INPUT;
+    }
+    if (path != IGP_PREDICT_AUTO && path != IGP_PREDICT_FP64 && path != IGP_PREDICT_TENSOR) {
+        set_error("birch: unknown predict path");
         return IGP_ERR_INPUT;
     }
     int64_t K = 0;
@@ -942,34 +1023,43 @@ igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m, int32_t
         set_error("birch: predict on an empty tree");
         return IGP_ERR_INPUT;
     }
+    const int d = b->t.d;
+    const bool tc_ok = birch_tc_eligible(d, K);
+    if (path == IGP_PREDICT_TENSOR && !tc_ok) {
+        set_error("birch: the tensor-core predict needs d a multiple of 8 in [8, 64]");
+        return IGP_ERR_INPUT;
+    }
+    const bool tc = path != IGP_PREDICT_FP64 && tc_ok;
+    if (ambiguous) *ambiguous = tc ? 0 : m;
     if (m == 0) return IGP_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    const int d = b->t.d;
     double* cen = nullptr;
     double* sqn = nullptr;
-    IGP_CUDA(alloc_async((void**)&cen, 8 * (size_t)K * d, s), "alloc");
-    IGP_CUDA(alloc_async((void**)&sqn, 8 * (size_t)K, s), "alloc");
+    int32_t* amb_rows = nullptr;
+    unsigned long long* amb_count = nullptr;
+    IGP_CUDA(alloc_async((void**)&cen, 8 * ((size_t)K * d + (size_t)K), s), "alloc");  // centroids, then sqn
+    sqn = cen + (size_t)K * d;
     igp_status st = igp_birch_clusters(b, cen, sqn, nullptr, nullptr, nullptr, stream);
-    if (st == IGP_OK) {
-        // points per block: as many (<= 128, multiple of 32) as fit in shared memory with their rows
-        const size_t budget = 200 * 1024, tile = sizeof(double) * (size_t)kPT * d;
-        int P = kPredThreads;
-        while (P > 32 && tile + sizeof(double) * (size_t)P * (d + 1) > budget) P -= 32;
-        const bool xs = tile + sizeof(double) * (size_t)P * (d + 1) <= budget;
-        if (!xs) P = kPredThreads;
-        const size_t smem = tile + (xs ? sizeof(double) * (size_t)P * (d + 1) : 0);
-        auto kern = xs ? birch_predict_kernel<true> : birch_predict_kernel<false>;
-        st = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                         "predict smem attribute");
-        if (st == IGP_OK) {
-            const int64_t grid = (m + P - 1) / P;
-            kern<<<(unsigned)grid, P, smem, s>>>(cen, sqn, K, d, d_X, m, d_labels);
-            st = launch_status("birch_predict_kernel");
-        }
+    int64_t n = m;  // rows left for the fp64 kernel
+    if (st == IGP_OK && tc) {
+        st = cuda_status(alloc_async((void**)&amb_rows, 4 * (size_t)m, s), "alloc");
+        if (st == IGP_OK) st = cuda_status(alloc_async((void**)&amb_count, sizeof(unsigned long long), s), "alloc");
+        if (st == IGP_OK) st = launch_birch_tc(cen, sqn, K, d, d_X, m, d_labels, amb_rows, amb_count, s);
+        unsigned long long h = 0;  // the grid of the fp64 pass is sized by the uncertified count
+        if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(&h, amb_count, sizeof(h), cudaMemcpyDeviceToHost, s), "readback");
+        if (st == IGP_OK) st = cuda_status(cudaStreamSynchronize(s), "sync");
+        n = (int64_t)h;
+        if (ambiguous) *ambiguous = n;
     }
+    if (st == IGP_OK && n > 0) st = launch_predict_fp64(cen, sqn, K, d, d_X, n, tc ? amb_rows : nullptr, d_labels, s);
     free_async(cen, s);
-    free_async(sqn, s);
+    if (amb_rows) free_async(amb_rows, s);
+    if (amb_count) free_async(amb_count, s);
     return st;
+}
+
+igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m, int32_t* d_labels, igp_stream_t stream) {
+    return igp_birch_predict_ex(b, d_X, m, d_labels, IGP_PREDICT_AUTO, nullptr, stream);
 }
 
 igp_status igp_birch_destroy(igp_birch_t b) {

@@ -1,0 +1,397 @@
+// birch_tc.cu — BIRCH predict's nearest-centroid search on the 5th-generation tensor cores.
+//
+// Labels (Alg. 1 l.7; Alg. 2 l.11) are
+//     label_i = argmin_j  d_ij,   d_ij = |c_j|^2 - 2 c_j . x_i      (first minimum, reading B5)
+// with d_ij in fp64 in the oracle's operation order (oracle/birch_oracle.c).  Over all rows and
+// clusters the scores c_j . x_i form a dense (m x d) . (d x K) contraction, so they run as
+// tcgen05.mma (kind::tf32; operands in shared memory, accumulator in TMEM) instead of fp64 FMAs
+// on the CUDA cores.  TF32 keeps 11 significant bits, so each operand is split v = hi + lo
+// (hi = v rounded to TF32, lo = v - hi) and the three products lo.hi + hi.lo + hi.hi are
+// accumulated ("3xTF32"): the result is within a few fp32 ulps of the product sum.
+//
+// The labels must still be the fp64 labels bit for bit.  The tensor-core pass therefore only
+// certifies: a_ij = |c_j|^2 - 2 acc_ij is within a margin M of the fp64 d_ij (M bounds every
+// rounding of the split, the products, the fp32 accumulation and the epilogue; DESIGN.md
+// §"BIRCH predict on the tensor cores" derives it, with a factor-2 safety).  Per row the
+// epilogue keeps the best and second-best a_ij; if second - best > 2M no other cluster can
+// come within M of the best, so the approximate argmin IS the exact argmin.  Otherwise (near
+// ties, exact ties, duplicate centroids; every row when a magnitude leaves the safe fp32 range,
+// M = inf) the row is listed and the fp64 kernel (birch.cu) resolves it in the oracle's order.
+//
+// Kernel layout (one CTA = 128 rows, warp-specialised, 192 threads):
+//   warp 0      : producer — cp.async.bulk of the row tile (once) and of each 128-centroid tile
+//                 (hi, lo) into a 2-stage shared-memory ring, completion on mbarriers
+//   warp 1      : TMEM allocator + MMA issuer (one lane): 3 x d/8 tcgen05.mma per tile into one
+//                 of two 128-column TMEM accumulators, tcgen05.commit -> ring slot / epilogue
+//   warps 2..5  : epilogue — tcgen05.ld of the accumulator (warp w reads TMEM lanes
+//                 32(w%4)..+31 = its 32 rows), a = fma(-2, acc, |c|^2), running best / second
+// Operands are pre-arranged in global memory in the UMMA canonical K-major no-swizzle layout
+// (core matrices of 8 rows x 16 bytes; row groups SBO = 32 d bytes apart, K chunks LBO = 128
+// bytes apart), so every tile is ONE contiguous bulk copy.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "igp_internal.cuh"
+
+namespace igp {
+namespace {
+
+constexpr int kTcM = 128;      // rows per CTA: MMA M, TMEM lanes
+constexpr int kTcN = 128;      // centroids per tile: MMA N, TMEM columns per accumulator
+constexpr int kTcStages = 2;   // centroid-tile ring depth
+constexpr int kTcThreads = 192;
+constexpr int kTcTmemCols = 2 * kTcN;  // two accumulators (power of two >= 32)
+// idesc (kind::tf32): c_format F32 (bits 4-5 = 1), a/b_format TF32 (bits 7-9, 10-12 = 2),
+// both K-major (bits 15, 16 = 0), N >> 3 at bits 17-22, M >> 4 at bits 24-28
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
+                            ((uint32_t)(kTcM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n\t"
+        "DONE:\n\t}" ::"r"(sa(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(dst)),
+                 "l"(src), "r"(bytes), "r"(sa(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// shared-memory matrix descriptor: start >> 4 (bits 0-13), LBO >> 4 (16-29), SBO >> 4 (32-45),
+// version 1 (46-47), base offset 0, no swizzle (61-63 = 0)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(accumulate), "r"(kIdesc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(bar)) : "memory");
+}
+// 64 consecutive fp32 accumulator columns of this thread's TMEM lane: two loads and the wait in
+// ONE asm statement, so no use of the registers can be scheduled before the wait
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
+    uint32_t r[64];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%64];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%65];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr), "r"(taddr + 32u)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float to_tf32(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return __uint_as_float(r);
+}
+
+// stats word: max_j |c_j|^2 as an fp32 bit pattern (non-negative: unsigned max == float max)
+enum { S_SQMAX = 0, S_WORDS = 4 };
+
+// Split rows [rows][d] (fp32 or fp64) into TF32 hi / fp32 lo, both written in the tiled
+// canonical K-major layout: tile r >> 7, row group (r & 127) >> 3, K chunk k >> 2, row r & 7.
+// One thread per row: for a fixed chunk the 32 lanes write 4 row groups x 128 contiguous bytes.
+// Rows >= `rows` (padding up to a multiple of 128) are zero.  Rows (T = float): norm[r] = an
+// upper bound of |x_r| (NaN / inf propagate).  Centroids (sqn given): sq32[r] = (float)sqn[r]
+// (+inf for padding, so padded centroids never win) and stats[S_SQMAX] = max sqn.
+template <typename T>
+__global__ void tc_split_kernel(const T* __restrict__ src, int64_t rows, int64_t rows_pad, int d, float* __restrict__ hi,
+                                float* __restrict__ lo, float* __restrict__ norm, const double* __restrict__ sqn,
+                                float* __restrict__ sq32, unsigned* stats) {
+    float smax = 0.f;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows_pad; r += (int64_t)gridDim.x * blockDim.x) {
+        float* h = hi + (r >> 7) * (int64_t)kTcM * d + ((r & 127) >> 3) * (int64_t)8 * d + (r & 7) * 4;
+        float* l = lo + (h - hi);
+        float n2 = 0.f;
+        for (int c = 0; c < d / 4; ++c) {
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (r < rows) {
+                const T* p = src + r * d + 4 * c;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = (float)p[u];
+            }
+            float4 vh, vl;
+            vh.x = to_tf32(v[0]); vh.y = to_tf32(v[1]); vh.z = to_tf32(v[2]); vh.w = to_tf32(v[3]);
+            vl.x = v[0] - vh.x; vl.y = v[1] - vh.y; vl.z = v[2] - vh.z; vl.w = v[3] - vh.w;  // exact in fp32
+            *reinterpret_cast<float4*>(h + 32 * c) = vh;
+            *reinterpret_cast<float4*>(l + 32 * c) = vl;
+            n2 = fmaf(v[0], v[0], fmaf(v[1], v[1], fmaf(v[2], v[2], fmaf(v[3], v[3], n2))));
+        }
+        // fp32 sum of d squares: relative error below d 2^-24; inflate past it
+        if (norm && r < rows) norm[r] = sqrtf(n2 * (1.f + (float)(d + 2) * 0x1p-23f)) * (1.f + 0x1p-20f);
+        if (sqn) {
+            const float sv = r < rows ? (float)sqn[r] : INFINITY;
+            sq32[r] = sv;
+            if (r < rows) smax = (sv == sv) ? fmaxf(smax, sv) : INFINITY;
+        }
+    }
+    if (sqn) {
+        unsigned u = __float_as_uint(smax);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) u = max(u, __shfl_xor_sync(0xffffffffu, u, o));
+        if ((threadIdx.x & 31) == 0) atomicMax(stats + S_SQMAX, u);
+    }
+}
+
+struct TcArgs {
+    const float* xh;  // row tiles, canonical layout
+    const float* xl;
+    const float* ch;  // centroid tiles, canonical layout
+    const float* cl;
+    const float* sq;  // [n_tiles * 128] |c_j|^2 (fp32), +inf padding
+    const float* xnorm;  // [m] upper bounds of |x_i|
+    const unsigned* stats;
+    int64_t m;
+    int n_tiles;
+    int d;
+    int32_t* labels;
+    int32_t* amb_rows;
+    unsigned long long* amb_count;
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
+    extern __shared__ __align__(1024) unsigned char tc_smem[];
+    __shared__ __align__(8) uint64_t bar_full[kTcStages], bar_empty[kTcStages], bar_tfull[2], bar_tempty[2], bar_a;
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(16) float sq_stage[4 * 2 * kTcN];  // epilogue warps' |c_j|^2 tiles
+    const int d = a.d;
+    const uint32_t tile_floats = (uint32_t)kTcM * d, tile_bytes = 4u * tile_floats;
+    float* sA_hi = reinterpret_cast<float*>(tc_smem);
+    float* sA_lo = sA_hi + tile_floats;
+    float* sB = sA_lo + tile_floats;  // stage s: hi at sB + 2 s tile, lo right after
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t mt = blockIdx.x;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&bar_full[s], 1);
+            mbar_init(&bar_empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&bar_tfull[b], 1);
+            mbar_init(&bar_tempty[b], 4);  // one arrival per epilogue warp
+        }
+        mbar_init(&bar_a, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(&tmem_slot)),
+                     "n"(kTcTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(&bar_a, 2 * tile_bytes);
+            bulk_g2s(sA_hi, a.xh + mt * tile_floats, tile_bytes, &bar_a);
+            bulk_g2s(sA_lo, a.xl + mt * tile_floats, tile_bytes, &bar_a);
+            for (int t = 0; t < a.n_tiles; ++t) {
+                const int s = t % kTcStages;
+                if (t >= kTcStages) mbar_wait(&bar_empty[s], (uint32_t)((t / kTcStages - 1) & 1));
+                float* dst = sB + (size_t)2 * s * tile_floats;
+                mbar_expect_tx(&bar_full[s], 2 * tile_bytes);
+                bulk_g2s(dst, a.ch + (size_t)t * tile_floats, tile_bytes, &bar_full[s]);
+                bulk_g2s(dst + tile_floats, a.cl + (size_t)t * tile_floats, tile_bytes, &bar_full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            mbar_wait(&bar_a, 0);
+            tc_fence_after();
+            const uint32_t a_hi = sa(sA_hi), a_lo = sa(sA_lo), sbo = 32u * d;
+            for (int t = 0; t < a.n_tiles; ++t) {
+                const int s = t % kTcStages, b = t & 1;
+                mbar_wait(&bar_full[s], (uint32_t)((t / kTcStages) & 1));
+                if (t >= 2) mbar_wait(&bar_tempty[b], (uint32_t)(((t >> 1) - 1) & 1));
+                tc_fence_after();
+                const uint32_t b_hi = sa(sB + (size_t)2 * s * tile_floats), b_lo = b_hi + tile_bytes;
+                const uint32_t acc = tmem + (uint32_t)(b * kTcN);
+                for (int kk = 0; kk < d / 8; ++kk) {  // K = 8 tf32 = two 16-byte chunks per MMA
+                    const uint32_t o = 256u * kk;
+                    mma_tf32(acc, umma_desc(a_lo + o, 128, sbo), umma_desc(b_hi + o, 128, sbo), kk > 0);
+                    mma_tf32(acc, umma_desc(a_hi + o, 128, sbo), umma_desc(b_lo + o, 128, sbo), 1);
+                    mma_tf32(acc, umma_desc(a_hi + o, 128, sbo), umma_desc(b_hi + o, 128, sbo), 1);
+                }
+                mma_commit(&bar_empty[s]);  // ring slot free once these MMAs have read it
+                mma_commit(&bar_tfull[b]);  // accumulator b complete
+            }
+        }
+    } else {
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = q * 32 + lane;
+        const int64_t gi = mt * kTcM + row;
+        // the certified margin M_i: S_i = |x_i| max_j |c_j| bounds sum_k |x_ik c_jk|
+        const float sqmax = __uint_as_float(a.stats[S_SQMAX]);
+        const float cn = sqrtf(sqmax) * (1.f + 0x1p-20f);
+        const float xn = gi < a.m ? a.xnorm[gi] : 0.f;
+        float M = INFINITY;
+        if (xn < 1e15f && cn < 1e15f && sqmax < 1e30f) {  // every fp32 partial sum stays far from overflow
+            const float S = xn * cn;
+            // + flushed subnormal operands / products (each below 2^-126 times a magnitude)
+            M = (float)(6 * d + 24) * 0x1p-22f * S + 0x1p-22f * sqmax + (float)(8 * d) * 0x1p-118f * (xn + cn + 1.f);
+        }
+        // four independent (best, second, index) trackers, one per column residue mod 4: the
+        // compare-select chains interleave instead of serialising 128 columns per tile
+        float bb[4], ss[4];
+        int jj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            bb[u] = ss[u] = INFINITY;
+            jj[u] = 0;
+        }
+        // |c_j|^2 of the tile, staged per warp in shared memory (broadcast reads), the next tile's
+        // values loaded into registers while this tile is processed
+        float* sqw = sq_stage + q * 2 * kTcN;
+        float4 nxt = __ldg(reinterpret_cast<const float4*>(a.sq) + lane);
+        for (int t = 0; t < a.n_tiles; ++t) {
+            const int b = t & 1;
+            reinterpret_cast<float4*>(sqw + b * kTcN)[lane] = nxt;
+            __syncwarp();
+            if (t + 1 < a.n_tiles) nxt = __ldg(reinterpret_cast<const float4*>(a.sq + (size_t)(t + 1) * kTcN) + lane);
+            mbar_wait(&bar_tfull[b], (uint32_t)((t >> 1) & 1));
+            tc_fence_after();
+            const float* sqt = sqw + b * kTcN;
+#pragma unroll 1
+            for (int c0 = 0; c0 < kTcN; c0 += 64) {
+                float v[64];
+                tmem_ld64(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * kTcN + c0), v);
+#pragma unroll
+                for (int j = 0; j < 64; j += 4) {
+                    const float4 s4 = *reinterpret_cast<const float4*>(sqt + c0 + j);
+                    const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float av = fmaf(-2.f, v[j + u], sv[u]);
+                        const bool nb = av < bb[u];
+                        ss[u] = nb ? bb[u] : fminf(ss[u], av);
+                        jj[u] = nb ? t * kTcN + c0 + j + u : jj[u];
+                        bb[u] = nb ? av : bb[u];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_tempty[b]);
+        }
+        // merge: best = min over trackers (ties: any — a tie leaves gap 0 and goes to fp64),
+        // second = smallest of the other trackers' bests and every tracker's second
+        int w = 0;
+#pragma unroll
+        for (int u = 1; u < 4; ++u) w = bb[u] < bb[w] ? u : w;
+        const float best = bb[w];
+        const int bj = jj[w];
+        float second = INFINITY;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) second = fminf(second, u == w ? ss[u] : fminf(bb[u], ss[u]));
+        if (gi < a.m) {
+            if (second - best > 2.f * M) {
+                a.labels[gi] = bj;
+            } else {  // not certified: the fp64 kernel decides
+                a.labels[gi] = -1;
+                const unsigned long long k = atomicAdd(a.amb_count, 1ull);
+                a.amb_rows[k] = (int32_t)gi;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcTmemCols) : "memory");
+}
+
+size_t tc_smem_bytes(int d) {
+    const size_t need = sizeof(float) * (size_t)kTcM * d * (2 + 2 * kTcStages);
+    // at least ~100 KB: at most two CTAs share an SM, so their 2 x 256 TMEM columns always fit
+    return need > 100 * 1024 ? need : 100 * 1024;
+}
+
+}  // namespace
+
+bool birch_tc_eligible(int d, int64_t K) {
+    DeviceInfo di;
+    if (!device_info(&di)) return false;
+    return d >= 8 && d <= kBirchTcMaxD && d % 8 == 0 && K >= 1 && K < (int64_t)INT32_MAX - kTcN &&
+           tc_smem_bytes(d) <= (size_t)di.max_smem_optin;
+}
+
+igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int d, const float* X, int64_t m,
+                           int32_t* labels, int32_t* amb_rows, unsigned long long* amb_count, cudaStream_t s) {
+    const int64_t mt = (m + kTcM - 1) / kTcM, nt = (K + kTcN - 1) / kTcN;
+    const size_t xf = (size_t)mt * kTcM * d, cf = (size_t)nt * kTcN * d;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t o_xl = al(4 * xf), o_ch = o_xl + al(4 * xf), o_cl = o_ch + al(4 * cf), o_sq = o_cl + al(4 * cf),
+                 o_xn = o_sq + al(4 * (size_t)nt * kTcN), o_st = o_xn + al(4 * (size_t)m), total = o_st + al(4 * S_WORDS);
+    char* ws = nullptr;
+    IGP_CUDA(alloc_async((void**)&ws, total, s), "birch tc workspace");
+    float* xh = (float*)ws;
+    float* xl = (float*)(ws + o_xl);
+    float* ch = (float*)(ws + o_ch);
+    float* cl = (float*)(ws + o_cl);
+    float* sq = (float*)(ws + o_sq);
+    float* xn = (float*)(ws + o_xn);
+    unsigned* st = (unsigned*)(ws + o_st);
+    igp_status r = cuda_status(cudaMemsetAsync(st, 0, 4 * S_WORDS, s), "memset");
+    if (r == IGP_OK) r = cuda_status(cudaMemsetAsync(amb_count, 0, sizeof(unsigned long long), s), "memset");
+    if (r == IGP_OK) {
+        tc_split_kernel<float><<<(unsigned)((mt * kTcM + 255) / 256), 256, 0, s>>>(X, m, mt * kTcM, d, xh, xl, xn, nullptr,
+                                                                              nullptr, nullptr);
+        r = launch_status("tc_split_kernel<float>");
+    }
+    if (r == IGP_OK) {
+        tc_split_kernel<double><<<(unsigned)((nt * kTcN + 255) / 256), 256, 0, s>>>(cen, K, nt * kTcN, d, ch, cl, nullptr,
+                                                                                sqn, sq, st);
+        r = launch_status("tc_split_kernel<double>");
+    }
+    if (r == IGP_OK) {
+        const size_t smem = tc_smem_bytes(d);
+        r = cuda_status(cudaFuncSetAttribute(birch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "birch tc smem attribute");
+        if (r == IGP_OK) {
+            TcArgs ar{xh, xl, ch, cl, sq, xn, st, m, (int)nt, d, labels, amb_rows, amb_count};
+            birch_tc_kernel<<<(unsigned)mt, kTcThreads, smem, s>>>(ar);
+            r = launch_status("birch_tc_kernel");
+        }
+    }
+    free_async(ws, s);
+    return r;
+}
+
+}  // namespace igp

@@ -142,6 +142,16 @@ struct HostCopy {
 igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cudaStream_t s,
                      HostCopy* hc = nullptr);
 
+// ---------------------------------------------------------------------------
+// birch_tc.cu: BIRCH predict's nearest-centroid search on the tensor cores (3xTF32 tcgen05.mma,
+// certified by a margin; rows it cannot certify get label -1 and are listed in amb_rows /
+// amb_count for the fp64 kernel in birch.cu)
+// ---------------------------------------------------------------------------
+constexpr int kBirchTcMaxD = 64;
+bool birch_tc_eligible(int d, int64_t K);
+igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int d, const float* X, int64_t m,
+                           int32_t* labels, int32_t* amb_rows, unsigned long long* amb_count, cudaStream_t s);
+
 }  // namespace igp
 
 struct igp_graph_s {

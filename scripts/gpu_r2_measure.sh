@@ -1,5 +1,5 @@
 # Round-2 measurements behind profiles/r02/ (run under gpurun; each section is independent):
-#   bash scripts/gpu_r2_measure.sh [sweep|dsmem|birch|stream|configs|ncu] ...
+#   bash scripts/gpu_r2_measure.sh [sweep|dsmem|birch|stream|configs|ncu|large|tcpredict] ...
 mkdir -p gpurun_out
 python paper_2508_19737_b200/_build.py > gpurun_out/r2_build.log 2>&1
 for what in "$@"; do
@@ -36,5 +36,15 @@ large)    # the Large config as a bench line + one --set full capture of its fil
   $CMD > gpurun_out/r2_plain_large.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:layer_kernel -s 2 -c 1 -o gpurun_out/r2_prof_large -f \
       $CMD > gpurun_out/r2_ncu_large.log 2>&1 ;;
+tcpredict)  # BIRCH predict: tensor-core path vs fp64 path at the streaming leg's scale, + ncu of the tc kernel
+  python tools/birch_predict_bench.py 150000 200000 64 0.05 > gpurun_out/r2_tc_predict.txt 2>&1
+  python tools/birch_predict_bench.py 20000 1000000 64 1.0 >> gpurun_out/r2_tc_predict.txt 2>&1
+  python tools/birch_predict_bench.py 40000 200000 32 0.03 >> gpurun_out/r2_tc_predict.txt 2>&1
+  CMD="python tools/birch_predict_bench.py 150000 200000 64 0.05 --profile"
+  $CMD > gpurun_out/r2_tc_plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_tc_launches.csv $CMD \
+      > gpurun_out/r2_tc_ncu_launch.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:birch_tc_kernel -c 1 -o gpurun_out/r2_prof_tc -f \
+      $CMD > gpurun_out/r2_ncu_tc.log 2>&1 ;;
 esac
 done

@@ -102,6 +102,7 @@ def test_more_host_validated_errors(igp):
     assert lib.igp_birch_create(4, -1.0, 50, ctypes.byref(h)) == 2
     assert lib.igp_birch_create(4, 0.5, 64, ctypes.byref(h)) == 2
     assert lib.igp_birch_partial_fit(None, None, 3, None) == 2
+    assert lib.igp_birch_predict_ex(None, None, 3, None, 0, None, None) == 2
     assert lib.igp_birch_destroy(None) == 0
     for bad_d in (40, 8, 2048):                                                          # multiple of 16 in [16, 1024]
         o2 = igp.make_opts(-1.0, bad_d, 3)

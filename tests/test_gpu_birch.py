@@ -55,11 +55,19 @@ def check_same_tree(igp, X, T, B, pieces=1):
     cen, sqn, cnt, ls, ss = (t.cpu().numpy() for t in g.clusters())
     for name, a, b in (("n", cnt, on), ("LS", ls, ols), ("SS", ss, oss), ("centroid", cen, ocen), ("sqn", sqn, osqn)):
         assert np.array_equal(a, b), f"{name} differs (max |diff| {np.abs(a - b).max():.3e})"
-    lab = g.predict(Xg).cpu().numpy()
     olab = oracle.birch_predict(ocen, osqn, X.astype(np.float64))
+    lab = g.predict(Xg, path="fp64").cpu().numpy()
     assert np.array_equal(lab, olab)
+    if tensor_eligible(d):  # the tensor-core search, certified: the same labels
+        lab, amb = g.predict(Xg, path="tensor", return_ambiguous=True)
+        assert np.array_equal(lab.cpu().numpy(), olab)
+        record(f"birch_tc_ambiguous_{n}x{d}_K{K}", amb)
     g.close()
     return K, dep
+
+
+def tensor_eligible(d):
+    return d % 8 == 0 and 8 <= d <= 64
 
 
 def datasets():
@@ -109,6 +117,93 @@ def test_birch_on_embeddings_medium(igp):
     record("birch_medium8k_T05_K", K2)
 
 
+def fit_clusters(igp, X, T, B):
+    """fit on both sides (bit-exact trees are checked elsewhere); returns (gpu tree, centroids, sqn)"""
+    g = igp.Birch(X.shape[1], T, B).partial_fit(torch.from_numpy(f32(X)).cuda())
+    o = oracle.Birch(X.shape[1], T, B).fit(f32(X).astype(np.float64))
+    ocen, osqn = o.clusters()[:2]
+    return g, ocen, osqn
+
+
+def test_birch_tensor_predict_ties_fall_back_to_fp64(igp):
+    """Rows exactly between two clusters (and duplicate centroids) cannot be certified by the
+    tensor-core pass (gap 0 < 2M): they are listed and solved in fp64; the labels are the
+    oracle's first minimum."""
+    rng = np.random.default_rng(3)
+    C = np.round(rng.random((40, 16)) * 8) / 8  # dyadic values: midpoints and distances are exact
+    X = np.concatenate([C, C[:5]])  # duplicates collapse into the same leaf entries
+    g, ocen, osqn = fit_clusters(igp, X, 1e-3, 50)
+    assert ocen.shape[0] == 40
+    Q = np.concatenate([(C[:-1] + C[1:]) / 2, C, rng.random((300, 16))])
+    Qg = torch.from_numpy(f32(Q)).cuda()
+    lab, amb = g.predict(Qg, path="tensor", return_ambiguous=True)
+    olab = oracle.birch_predict(ocen, osqn, f32(Q).astype(np.float64))
+    assert np.array_equal(lab.cpu().numpy(), olab)
+    assert amb >= 1  # at least the exact ties among the midpoints went to fp64
+    record("birch_tc_ties_ambiguous", amb)
+    g.close()
+
+
+def test_birch_tensor_predict_huge_values_all_fp64(igp):
+    """Magnitudes outside the certified fp32 range (M = inf): every row is solved in fp64."""
+    rng = np.random.default_rng(4)
+    X = rng.normal(0, 1, (500, 8)) * 1e16
+    g, ocen, osqn = fit_clusters(igp, X, 1e15, 50)
+    Xg = torch.from_numpy(f32(X)).cuda()
+    lab, amb = g.predict(Xg, path="tensor", return_ambiguous=True)
+    assert amb == X.shape[0]
+    assert np.array_equal(lab.cpu().numpy(), oracle.birch_predict(ocen, osqn, f32(X).astype(np.float64)))
+    g.close()
+
+
+@pytest.mark.parametrize("d", [8, 24, 32, 64])
+def test_birch_tensor_predict_many_clusters(igp, d):
+    """Thousands of clusters (several 128-centroid tiles, a ragged last tile) and a ragged last
+    row tile: tensor path == fp64 path == oracle; almost every row certified."""
+    rng = np.random.default_rng(10 + d)
+    X = 1 / (1 + np.exp(-rng.normal(0, 1, (6000, d))))
+    g, ocen, osqn = fit_clusters(igp, X, 0.35 * np.sqrt(d / 64), 50)
+    K = ocen.shape[0]
+    assert K > 300
+    Q = f32(1 / (1 + np.exp(-rng.normal(0, 1, (3001, d)))))
+    Qg = torch.from_numpy(Q).cuda()
+    olab = oracle.birch_predict(ocen, osqn, Q.astype(np.float64))
+    lab, amb = g.predict(Qg, path="tensor", return_ambiguous=True)
+    assert np.array_equal(lab.cpu().numpy(), olab)
+    assert np.array_equal(g.predict(Qg, path="fp64").cpu().numpy(), olab)
+    assert amb < Q.shape[0] // 10
+    record(f"birch_tc_many_d{d}", {"K": K, "rows": Q.shape[0], "ambiguous": amb})
+    g.close()
+
+
+def test_birch_tensor_predict_streaming_scale(igp):
+    """The streaming leg's regime (tens of thousands of clusters): tensor path == fp64 path
+    (the fp64 path is pinned to the oracle above) on 100K rows x 40K clusters; times recorded."""
+    rng = np.random.default_rng(21)
+    X = torch.from_numpy(f32(1 / (1 + np.exp(-rng.normal(0, 1.5, (40000, 64)))))).cuda()
+    g = igp.Birch(64, 0.05, 50).partial_fit(X)
+    K = g.info()[0]
+    assert K > 30000
+    Q = torch.cat([X, torch.from_numpy(f32(1 / (1 + np.exp(-rng.normal(0, 1.5, (60000, 64)))))).cuda()])
+    times = {}
+    for path in ("fp64", "tensor"):
+        g.predict(Q, path=path)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        lab = g.predict(Q, path=path)
+        b.record()
+        torch.cuda.synchronize()
+        times[path] = a.elapsed_time(b)
+        if path == "fp64":
+            ref = lab.clone()
+    lab, amb = g.predict(Q, path="tensor", return_ambiguous=True)
+    assert torch.equal(lab, ref)
+    record("birch_tc_streaming_scale", {"K": K, "rows": Q.shape[0], "ambiguous": amb,
+                                        "fp64_ms": times["fp64"], "tensor_ms": times["tensor"]})
+    g.close()
+
+
 def test_birch_errors(igp):
     with pytest.raises(igp.IGPError):
         igp.Birch(8, 0.0, 50)
@@ -125,6 +220,10 @@ def test_birch_errors(igp):
     b.partial_fit(torch.zeros((0, 4), device="cuda"))
     b.partial_fit(torch.ones((2, 4), device="cuda"))
     assert b.info()[:1] == (1,)
+    with pytest.raises(igp.IGPError):
+        b.predict(torch.ones((2, 4), device="cuda"), path="tensor")  # d = 4: not a multiple of 8
+    with pytest.raises(ValueError):
+        b.predict(torch.ones((2, 4), device="cuda"), path="bf16")
     b.close()
 
 

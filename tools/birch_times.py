@@ -1,7 +1,8 @@
 """BIRCH (igp_birch_*) device times on a config's GPU embedding (tooling).
 
     python tools/birch_times.py headline [T1,T2,...] [--oracle-rows R]
-For each threshold: fit (igp_birch_partial_fit, host-timed: synchronous call), predict (CUDA events),
+For each threshold: fit (igp_birch_partial_fit, host-timed: synchronous call), predict on both paths
+(tensor cores, certified, and all-fp64; CUDA events; labels must agree),
 K / depth / nodes, us per inserted row; the oracle's fit + predict on the first R rows (one thread).
 """
 import os
@@ -33,14 +34,21 @@ for T in thresholds:
     t0 = time.perf_counter()
     b.partial_fit(Z)
     fit = time.perf_counter() - t0
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record()
-    lab = b.predict(Z)
-    p1.record()
-    torch.cuda.synchronize()
+    pt = {}
+    for path in ("tensor", "fp64"):
+        b.predict(Z, path=path)  # warm
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record()
+        lab = b.predict(Z, path=path)
+        p1.record()
+        torch.cuda.synchronize()
+        pt[path] = (p0.elapsed_time(p1), lab)
+    _, amb = b.predict(Z, path="tensor", return_ambiguous=True)
+    assert torch.equal(pt["tensor"][1], pt["fp64"][1])
     K, dep, nodes, pts = b.info()
     line = (f"{cfg.name} T={T}: K={K} depth={dep} nodes={nodes}  fit {fit * 1e3:9.1f} ms "
-            f"({fit / pts * 1e6:.2f} us/row)  predict {p0.elapsed_time(p1):8.2f} ms")
+            f"({fit / pts * 1e6:.2f} us/row)  predict tensor {pt['tensor'][0]:8.2f} ms ({amb} rows to fp64) "
+            f"fp64 {pt['fp64'][0]:8.2f} ms")
     if orows:
         import oracle
         X = Z[:orows].cpu().numpy().astype(np.float64)
