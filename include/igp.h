@@ -278,13 +278,14 @@ IGP_API igp_status igp_birch_predict(igp_birch_t b, const float* d_X, int64_t m,
 /* igp_birch_predict with a choice of arithmetic (same labels either way):
  *   IGP_PREDICT_FP64   every distance in fp64 on the CUDA cores, in the oracle's order;
  *   IGP_PREDICT_TENSOR the scores c_j . x_i on the tensor cores (tcgen05, 3xTF32 split),
- *                      each row's argmin certified by an error margin; rows whose best and
- *                      second-best approximate distances lie within twice the margin (near or
- *                      exact ties) are re-solved in fp64 as above.  Needs d a multiple of 8 in
- *                      [8, 64] (else IGP_ERR_INPUT);
+ *                      each row's argmin certified by an error margin; where other clusters
+ *                      come within twice the margin of the best (near or exact ties) the
+ *                      candidates' distances are evaluated in fp64 as above (all clusters when
+ *                      the candidates cannot be isolated).  Needs d a multiple of 8 in [8, 64]
+ *                      (else IGP_ERR_INPUT);
  *   IGP_PREDICT_AUTO   TENSOR where eligible, else FP64 (what igp_birch_predict does).
- * ambiguous (host, may be NULL) receives the number of rows solved in fp64: the uncertified
- * rows on the tensor path (the call then synchronises `stream` to read it), m on the FP64 path. */
+ * ambiguous (host, may be NULL) receives the number of rows whose label was decided by fp64
+ * distances: the rows the tensor scores alone did not settle, m on the FP64 path. */
 #define IGP_PREDICT_AUTO 0
 #define IGP_PREDICT_FP64 1
 #define IGP_PREDICT_TENSOR 2

@@ -573,17 +573,54 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
     }
 }
 
-// leaf entries in leaf-chain order -> idx[K] (one thread; K = hdr-derived count)
-__global__ void birch_list_kernel(TreeDev t, int32_t* idx, long long* count) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// leaf entries in leaf-chain order -> idx[K], K -> *count.  The chain walk is a pointer chase
+// (one dependent load per leaf); with the tree's next / nsub arrays staged in shared memory
+// (nodes <= smem_nodes) a hop costs a shared-memory latency instead of an L2 one, thread 0
+// records each leaf's rank and output offset, and the block then writes the entries in parallel.
+// Larger trees walk global memory (one thread).
+__global__ void __launch_bounds__(1024) birch_list_kernel(TreeDev t, int32_t* idx, long long* count, int smem_nodes) {
+    extern __shared__ int32_t list_smem[];
     const int B1 = t.B + 1;
-    long long k = 0;
-    for (int v = (int)t.hdr[H_FIRST_LEAF]; v >= 0; v = t.next[v])
-        for (int j = 0; j < t.nsub[v]; ++j) {
-            if (idx) idx[k] = t.sub[(int64_t)v * B1 + j];
-            ++k;
+    const int nn = (int)t.hdr[H_NN];
+    if (nn > smem_nodes) {
+        if (threadIdx.x != 0) return;
+        long long k = 0;
+        for (int v = (int)t.hdr[H_FIRST_LEAF]; v >= 0; v = t.next[v])
+            for (int j = 0; j < t.nsub[v]; ++j) {
+                if (idx) idx[k] = t.sub[(int64_t)v * B1 + j];
+                ++k;
+            }
+        *count = k;
+        return;
+    }
+    int32_t* nxt = list_smem;       // [nn]
+    int32_t* nsb = nxt + nn;        // [nn]
+    int32_t* ord = nsb + nn;        // [nn] leaves in chain order
+    int32_t* off = ord + nn;        // [nn] their first output position
+    __shared__ int nleaves;
+    for (int v = threadIdx.x; v < nn; v += blockDim.x) {
+        nxt[v] = t.next[v];
+        nsb[v] = t.nsub[v];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int r = 0, k = 0;
+        for (int v = (int)t.hdr[H_FIRST_LEAF]; v >= 0; v = nxt[v]) {
+            ord[r] = v;
+            off[r++] = k;
+            k += nsb[v];
         }
-    *count = k;
+        nleaves = r;
+        *count = k;
+    }
+    __syncthreads();
+    if (!idx) return;
+    const int L = nleaves;
+    for (int e = threadIdx.x; e < L * B1; e += blockDim.x) {  // (leaf rank, slot) pairs
+        const int r = e / B1, j = e - r * B1;
+        const int v = ord[r];
+        if (j < nsb[v]) idx[off[r] + j] = t.sub[(int64_t)v * B1 + j];
+    }
 }
 
 // gather the listed entries: centroids, sqn, n, LS, SS (any output may be null)
@@ -713,6 +750,11 @@ struct igp_birch_s {
     int device = 0;
     void* pool = nullptr;
     int64_t points = 0;
+    // the clusters' entry indices in label order, valid until the next partial fit
+    int32_t* list = nullptr;
+    int64_t list_cap = 0;
+    int64_t list_k = 0;
+    bool list_valid = false;
 };
 
 namespace {
@@ -812,6 +854,36 @@ igp_status grow(igp_birch_s* b, int64_t cs, int64_t cn, cudaStream_t s) {
 igp_status read_hdr(igp_birch_s* b, long long* h, cudaStream_t s) {
     IGP_CUDA(cudaMemcpyAsync(h, b->t.hdr, sizeof(long long) * H_WORDS, cudaMemcpyDeviceToHost, s), "birch header");
     IGP_CUDA(cudaStreamSynchronize(s), "birch sync");
+    return IGP_OK;
+}
+
+// (re)build the cached cluster list (entry indices in leaf-chain order) after a fit; synchronous
+igp_status refresh_list(igp_birch_s* b, const long long* h, cudaStream_t s) {
+    if (b->list_valid) return IGP_OK;
+    const int64_t ns = h[H_NS];  // entries of every node: an upper bound of the leaf entries
+    if (b->list_cap < ns || !b->list) {
+        if (b->list) free_async(b->list, s);
+        b->list = nullptr;
+        b->list_cap = 0;
+        const int64_t cap = (std::max<int64_t>(ns, 1024) + 1) & ~(int64_t)1;  // even: the count below is 8-B aligned
+        IGP_CUDA(alloc_async((void**)&b->list, sizeof(int32_t) * (size_t)(cap + 2), s), "alloc");
+        b->list_cap = cap;
+    }
+    long long* cnt = reinterpret_cast<long long*>(b->list + b->list_cap);  // past the entries
+    DeviceInfo di;
+    if (!device_info(&di)) return IGP_ERR_CUDA;
+    const int smem_nodes = (int)std::min<int64_t>((di.max_smem_optin - 1024) / 16, INT32_MAX);
+    const int nn = (int)h[H_NN];
+    const size_t smem = nn <= smem_nodes ? (size_t)16 * nn : 0;
+    IGP_CUDA(cudaFuncSetAttribute(birch_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+             "birch list smem attribute");
+    birch_list_kernel<<<1, 1024, smem, s>>>(b->t, b->list, cnt, smem_nodes);
+    IGP_TRY(launch_status("birch_list_kernel"));
+    long long k = 0;
+    IGP_CUDA(cudaMemcpyAsync(&k, cnt, sizeof(k), cudaMemcpyDeviceToHost, s), "readback");
+    IGP_CUDA(cudaStreamSynchronize(s), "birch sync");
+    b->list_k = k;
+    b->list_valid = true;
     return IGP_OK;
 }
 
@@ -953,6 +1025,7 @@ igp_status igp_birch_partial_fit(igp_birch_t b, const float* d_X, int64_t m, igp
         }
     }
     b->points += m;
+    b->list_valid = false;
     return IGP_OK;
 }
 
@@ -963,16 +1036,10 @@ igp_status igp_birch_info(igp_birch_t b, int64_t* num_clusters, int32_t* depth, 
         return IGP_ERR_INPUT;
     }
     cudaStream_t s = 0;
-    long long* cnt = nullptr;
-    IGP_CUDA(alloc_async((void**)&cnt, sizeof(long long), s), "alloc");
-    birch_list_kernel<<<1, 32, 0, s>>>(b->t, nullptr, cnt);
-    igp_status st = launch_status("birch_list_kernel");
-    long long k = 0, h[H_WORDS] = {0};
-    if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(&k, cnt, sizeof(k), cudaMemcpyDeviceToHost, s), "readback");
-    if (st == IGP_OK) st = read_hdr(b, h, s);
-    free_async(cnt, s);
-    if (st != IGP_OK) return st;
-    if (num_clusters) *num_clusters = k;
+    long long h[H_WORDS] = {0};
+    IGP_TRY(read_hdr(b, h, s));
+    IGP_TRY(refresh_list(b, h, s));
+    if (num_clusters) *num_clusters = b->list_k;
     if (depth) *depth = (int32_t)h[H_DEPTH];
     if (nodes) *nodes = h[H_NN];
     if (points) *points = h[H_NPOINTS];
@@ -987,23 +1054,12 @@ igp_status igp_birch_clusters(igp_birch_t b, double* d_centroids, double* d_sqn,
         return IGP_ERR_INPUT;
     }
     int64_t K = 0;
-    IGP_TRY(igp_birch_info(b, &K, nullptr, nullptr, nullptr));
+    IGP_TRY(igp_birch_info(b, &K, nullptr, nullptr, nullptr));  // the list is current after this
     if (K == 0) return IGP_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    int32_t* idx = nullptr;
-    long long* cnt = nullptr;
-    IGP_CUDA(alloc_async((void**)&idx, 4 * (size_t)K, s), "alloc");
-    IGP_CUDA(alloc_async((void**)&cnt, sizeof(long long), s), "alloc");
-    birch_list_kernel<<<1, 32, 0, s>>>(b->t, idx, cnt);
-    igp_status st = launch_status("birch_list_kernel");
-    if (st == IGP_OK) {
-        const int grid = (int)std::min<int64_t>((K * b->t.d + 255) / 256, 4096);
-        birch_gather_kernel<<<grid, 256, 0, s>>>(b->t, idx, K, d_centroids, d_sqn, d_n, d_ls, d_ss);
-        st = launch_status("birch_gather_kernel");
-    }
-    free_async(idx, s);
-    free_async(cnt, s);
-    return st;
+    const int grid = (int)std::min<int64_t>((K * b->t.d + 255) / 256, 4096);
+    birch_gather_kernel<<<grid, 256, 0, s>>>(b->t, b->list, K, d_centroids, d_sqn, d_n, d_ls, d_ss);
+    return launch_status("birch_gather_kernel");
 }
 
 igp_status igp_birch_predict_ex(igp_birch_t b, const float* d_X, int64_t m, int32_t* d_labels, int32_t path,
@@ -1043,13 +1099,13 @@ igp_status igp_birch_predict_ex(igp_birch_t b, const float* d_X, int64_t m, int3
     int64_t n = m;  // rows left for the fp64 kernel
     if (st == IGP_OK && tc) {
         st = cuda_status(alloc_async((void**)&amb_rows, 4 * (size_t)m, s), "alloc");
-        if (st == IGP_OK) st = cuda_status(alloc_async((void**)&amb_count, sizeof(unsigned long long), s), "alloc");
+        if (st == IGP_OK) st = cuda_status(alloc_async((void**)&amb_count, 2 * sizeof(unsigned long long), s), "alloc");
         if (st == IGP_OK) st = launch_birch_tc(cen, sqn, K, d, d_X, m, d_labels, amb_rows, amb_count, s);
-        unsigned long long h = 0;  // the grid of the fp64 pass is sized by the uncertified count
-        if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(&h, amb_count, sizeof(h), cudaMemcpyDeviceToHost, s), "readback");
+        unsigned long long h[2] = {0, 0};  // the grid of the fp64 pass is sized by the uncertified count
+        if (st == IGP_OK) st = cuda_status(cudaMemcpyAsync(h, amb_count, sizeof(h), cudaMemcpyDeviceToHost, s), "readback");
         if (st == IGP_OK) st = cuda_status(cudaStreamSynchronize(s), "sync");
-        n = (int64_t)h;
-        if (ambiguous) *ambiguous = n;
+        n = (int64_t)h[0];
+        if (ambiguous) *ambiguous = (int64_t)(h[0] + h[1]);
     }
     if (st == IGP_OK && n > 0) st = launch_predict_fp64(cen, sqn, K, d, d_X, n, tc ? amb_rows : nullptr, d_labels, s);
     free_async(cen, s);
@@ -1069,6 +1125,7 @@ igp_status igp_birch_destroy(igp_birch_t b) {
     if (prev != b->device) cudaSetDevice(b->device);
     cudaStreamSynchronize(0);  // the tree's calls are synchronous or ordered on the caller's stream
     if (b->pool) free_async(b->pool, 0);
+    if (b->list) free_async(b->list, 0);
     if (prev >= 0 && prev != b->device) cudaSetDevice(prev);
     delete b;
     return IGP_OK;

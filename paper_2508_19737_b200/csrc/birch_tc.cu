@@ -173,13 +173,29 @@ struct TcArgs {
     const float* sq;  // [n_tiles * 128] |c_j|^2 (fp32), +inf padding
     const float* xnorm;  // [m] upper bounds of |x_i|
     const unsigned* stats;
+    const float* X;      // the rows [m][d] and the clusters (fp64), for the exact re-check
+    const double* cen;
+    const double* sqn;
     int64_t m;
     int n_tiles;
     int d;
     int32_t* labels;
     int32_t* amb_rows;
-    unsigned long long* amb_count;
+    unsigned long long* amb_count;  // [0] rows left to the fp64 pass, [1] rows re-checked here in fp64
 };
+
+// d_ij in fp64 exactly as the oracle (and birch.cu's fp64 kernel) evaluates it: eight partial
+// sums p[k mod 8] by fma, combined pairwise, then sqn_j + (-2 dot)
+__device__ __forceinline__ double exact_dist(const float* __restrict__ x, const double* __restrict__ c, double sq, int d) {
+    double p[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < d; k += 8) {  // d is a multiple of 8 on this path
+#pragma unroll
+        for (int q = 0; q < 8; ++q) p[q] = __fma_rn(c[k + q], (double)x[k + q], p[q]);
+    }
+    const double dt = __dadd_rn(__dadd_rn(__dadd_rn(p[0], p[1]), __dadd_rn(p[2], p[3])),
+                                __dadd_rn(__dadd_rn(p[4], p[5]), __dadd_rn(p[6], p[7])));
+    return __dadd_rn(sq, -2.0 * dt);
+}
 
 __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
@@ -267,12 +283,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
             // + flushed subnormal operands / products (each below 2^-126 times a magnitude)
             M = (float)(6 * d + 24) * 0x1p-22f * S + 0x1p-22f * sqmax + (float)(8 * d) * 0x1p-118f * (xn + cn + 1.f);
         }
-        // four independent (best, second, index) trackers, one per column residue mod 4: the
-        // compare-select chains interleave instead of serialising 128 columns per tile
-        float bb[4], ss[4];
-        int jj[4];
+        // kTr independent (best, index, second) trackers, tracker u taking the columns j = u mod kTr:
+        // the compare-select chains interleave instead of serialising 128 columns per tile
+        constexpr int kTr = 8;
+        float bb[kTr], ss[kTr];
+        int jj[kTr];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kTr; ++u) {
             bb[u] = ss[u] = INFINITY;
             jj[u] = 0;
         }
@@ -293,11 +310,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
                 float v[64];
                 tmem_ld64(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * kTcN + c0), v);
 #pragma unroll
-                for (int j = 0; j < 64; j += 4) {
-                    const float4 s4 = *reinterpret_cast<const float4*>(sqt + c0 + j);
-                    const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+                for (int j = 0; j < 64; j += kTr) {
+                    const float4 s0 = *reinterpret_cast<const float4*>(sqt + c0 + j);
+                    const float4 s1 = *reinterpret_cast<const float4*>(sqt + c0 + j + 4);
+                    const float sv[kTr] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kTr; ++u) {
                         const float av = fmaf(-2.f, v[j + u], sv[u]);
                         const bool nb = av < bb[u];
                         ss[u] = nb ? bb[u] : fminf(ss[u], av);
@@ -310,20 +328,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_tempty[b]);
         }
-        // merge: best = min over trackers (ties: any — a tie leaves gap 0 and goes to fp64),
-        // second = smallest of the other trackers' bests and every tracker's second
-        int w = 0;
-#pragma unroll
-        for (int u = 1; u < 4; ++u) w = bb[u] < bb[w] ? u : w;
-        const float best = bb[w];
-        const int bj = jj[w];
-        float second = INFINITY;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) second = fminf(second, u == w ? ss[u] : fminf(bb[u], ss[u]));
         if (gi < a.m) {
-            if (second - best > 2.f * M) {
-                a.labels[gi] = bj;
-            } else {  // not certified: the fp64 kernel decides
+            // Certification: every a_ij is within M of d_ij.  Let best = min a and
+            // thr = best + 2M.  A column outside the trackers' bests has a >= its tracker's second;
+            // if every second exceeds thr, such columns have d > best + M >= d_min: the exact
+            // first minimum is among the trackers' bests with a <= thr.  One such candidate: it is
+            // the label.  Several: their d_ij are evaluated here in fp64 (the oracle's order) and
+            // the smallest (lowest index on ties) is the label.  Otherwise the fp64 pass decides.
+            float best = bb[0];
+#pragma unroll
+            for (int u = 1; u < kTr; ++u) best = fminf(best, bb[u]);
+            const float thr = best + 2.f * M;
+            bool cert = true;
+            int ncand = 0, cand = 0;
+#pragma unroll
+            for (int u = 0; u < kTr; ++u) {
+                cert = cert && (ss[u] > thr);
+                if (bb[u] <= thr) {
+                    ++ncand;
+                    cand = jj[u];
+                }
+            }
+            cert = cert && ncand >= 1;  // NaN scores (M = inf rows excepted) never certify
+            if (cert && ncand == 1) {
+                a.labels[gi] = cand;
+            } else if (cert) {
+                const float* x = a.X + gi * d;
+                double dbest = INFINITY;
+                int lbest = INT32_MAX;
+#pragma unroll
+                for (int u = 0; u < kTr; ++u) {  // unrolled: the trackers stay in registers
+                    if (!(bb[u] <= thr)) continue;
+                    const int j = jj[u];
+                    const double dj = exact_dist(x, a.cen + (int64_t)j * d, a.sqn[j], d);
+                    if (dj < dbest || (dj == dbest && j < lbest)) {
+                        dbest = dj;
+                        lbest = j;
+                    }
+                }
+                a.labels[gi] = lbest;
+                atomicAdd(a.amb_count + 1, 1ull);
+            } else {  // not certified: the fp64 pass decides
                 a.labels[gi] = -1;
                 const unsigned long long k = atomicAdd(a.amb_count, 1ull);
                 a.amb_rows[k] = (int32_t)gi;
@@ -369,7 +414,7 @@ igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int 
     float* xn = (float*)(ws + o_xn);
     unsigned* st = (unsigned*)(ws + o_st);
     igp_status r = cuda_status(cudaMemsetAsync(st, 0, 4 * S_WORDS, s), "memset");
-    if (r == IGP_OK) r = cuda_status(cudaMemsetAsync(amb_count, 0, sizeof(unsigned long long), s), "memset");
+    if (r == IGP_OK) r = cuda_status(cudaMemsetAsync(amb_count, 0, 2 * sizeof(unsigned long long), s), "memset");
     if (r == IGP_OK) {
         tc_split_kernel<float><<<(unsigned)((mt * kTcM + 255) / 256), 256, 0, s>>>(X, m, mt * kTcM, d, xh, xl, xn, nullptr,
                                                                               nullptr, nullptr);
@@ -385,7 +430,7 @@ igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int 
         r = cuda_status(cudaFuncSetAttribute(birch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "birch tc smem attribute");
         if (r == IGP_OK) {
-            TcArgs ar{xh, xl, ch, cl, sq, xn, st, m, (int)nt, d, labels, amb_rows, amb_count};
+            TcArgs ar{xh, xl, ch, cl, sq, xn, st, X, cen, sqn, m, (int)nt, d, labels, amb_rows, amb_count};
             birch_tc_kernel<<<(unsigned)mt, kTcThreads, smem, s>>>(ar);
             r = launch_status("birch_tc_kernel");
         }

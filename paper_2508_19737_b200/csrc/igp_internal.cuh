@@ -144,8 +144,9 @@ igp_status run_embed(const CsrDevice& g, const igp_embed_opts& o, float* out, cu
 
 // ---------------------------------------------------------------------------
 // birch_tc.cu: BIRCH predict's nearest-centroid search on the tensor cores (3xTF32 tcgen05.mma,
-// certified by a margin; rows it cannot certify get label -1 and are listed in amb_rows /
-// amb_count for the fp64 kernel in birch.cu)
+// certified by a margin; near-ties among a few candidates are re-checked in fp64 in the kernel
+// (counted in amb_count[1]); rows it cannot settle get label -1 and are listed in amb_rows /
+// amb_count[0] for the fp64 kernel in birch.cu)
 // ---------------------------------------------------------------------------
 constexpr int kBirchTcMaxD = 64;
 bool birch_tc_eligible(int d, int64_t K);

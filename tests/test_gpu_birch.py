@@ -47,6 +47,9 @@ def check_same_tree(igp, X, T, B, pieces=1):
     for a, b in zip(cuts[:-1], cuts[1:]):
         g.partial_fit(Xg[a:b])
         o.partial_fit(X[a:b].astype(np.float64))
+        if pieces > 1:  # the cached cluster list is rebuilt after every fit
+            assert g.info()[0] == o.clusters()[0].shape[0]
+            assert np.array_equal(g.clusters()[0].cpu().numpy(), o.clusters()[0])
     K, dep, nodes, pts = g.info()
     ocen, osqn, on, ols, oss = o.clusters()
     assert K == ocen.shape[0] and pts == n
