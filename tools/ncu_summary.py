@@ -21,7 +21,12 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
         "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct",
         "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        # tensor-core kernels (birch_tc_kernel)
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]
 
 
 def launches(path):
@@ -53,8 +58,9 @@ def full(path):
         name = r[h.index("Kernel Name")] if "Kernel Name" in h else "?"
         d = {"kernel": name[:80]}
         for k in KEYS:
-            if k in h:
-                i = h.index(k)
+            hit = [c for c in h if c == k or c.endswith("." + k)]  # some counters carry a section prefix
+            if hit:
+                i = h.index(hit[0])
                 d[k] = f"{r[i]} {units[i]}".strip()
         res.append(d)
     return json.dumps(res, indent=1)
