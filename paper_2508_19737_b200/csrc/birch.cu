@@ -346,49 +346,16 @@ __device__ void copy_tree(const TreeDev& dst, const TreeDev& src, long long ns, 
     for (int w = threadIdx.x; w < H_WORDS; w += kFitThreads) dst.hdr[w] = src.hdr[w];
 }
 
-// Insert rows [start, m) of X in order.  One CTA.  When the whole tree (plus the growth one
-// launch may need) fits in the cap_s_sm / cap_n_sm pool carved from shared memory, the tree is
-// moved there for the launch and written back at its end (every dependent lookup of the descent
-// then costs a shared-memory access instead of an L2 round trip); otherwise it is used in place.
-__global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, const float* __restrict__ X, int64_t m,
-                                                                    int64_t start, int64_t cap_s_sm, int64_t cap_n_sm) {
-    extern __shared__ double fit_smem[];
-    __shared__ FitShared sh;
-    __shared__ int use_sm;
-    const int d = t.d, B1 = t.B + 1;
-    double* xs = fit_smem;              // [d] the point
-    double* tmp = fit_smem + d;         // [2d] merge candidate LS', c'
-    double* D = fit_smem + 3 * d;       // [(B+1)^2] split distances
-    float* xring = reinterpret_cast<float*>(D + (((size_t)B1 * B1 + 1) & ~(size_t)1));  // [2][CH][d] staged rows
+// The insertion loop over rows [start, m).  Instantiated twice: SM = true with every tree pointer
+// derived from the kernel's shared-memory pool inside the same inlined body (the compiler then
+// emits shared-memory loads / stores instead of generic ones on the descent's dependent chain),
+// SM = false for trees left in global memory.
+template <bool SM>
+__device__ __forceinline__ void fit_rows(TreeDev T, const float* __restrict__ X, int64_t m, int64_t start, double* xs,
+                                         double* tmp, double* D, float* xring, FitShared& sh) {
+    const int d = T.d, B1 = T.B + 1;
     const int CH = ring_rows(d);
     const int g = threadIdx.x >> 1, r = threadIdx.x & 1;
-    // shared-memory pool (if it holds the tree with room for at least a few hundred inserts)
-    TreeDev T = t;
-    if (threadIdx.x == 0) {
-        const long long ns0 = t.hdr[H_NS], nn0 = t.hdr[H_NN], dep0 = t.hdr[H_DEPTH];
-        use_sm = cap_s_sm > 0 && ns0 + 64 + 2 * (dep0 + 2) <= cap_s_sm && nn0 + 2 * (dep0 + 2) + 8 <= cap_n_sm;
-    }
-    __syncthreads();
-    if (use_sm) {
-        char* p = reinterpret_cast<char*>(xring + (size_t)2 * CH * d);
-        T.n = reinterpret_cast<double*>(p);
-        T.ss = T.n + cap_s_sm;
-        T.sqn = T.ss + cap_s_sm;
-        T.ls = T.sqn + cap_s_sm;
-        T.cen = T.ls + cap_s_sm * d;
-        T.ldc = (d & 1) ? d : d + 2;
-        T.hdr = reinterpret_cast<long long*>(T.cen + cap_s_sm * T.ldc);
-        T.child = reinterpret_cast<int32_t*>(T.hdr + H_WORDS);
-        T.is_leaf = T.child + cap_s_sm;
-        T.nsub = T.is_leaf + cap_n_sm;
-        T.prev = T.nsub + cap_n_sm;
-        T.next = T.prev + cap_n_sm;
-        T.sub = T.next + cap_n_sm;
-        T.cap_s = cap_s_sm;
-        T.cap_n = cap_n_sm;
-        copy_tree(T, t, t.hdr[H_NS], t.hdr[H_NN]);
-        __syncthreads();
-    }
     if (threadIdx.x == 0) T.hdr[H_STOP] = m;
     auto issue_chunk = [&](int64_t c) {  // rows [start + c CH, ...) into ring slot c & 1
         const int64_t r0 = start + c * CH;
@@ -567,9 +534,54 @@ __global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, co
         if (threadIdx.x == 0) T.hdr[H_NPOINTS]++;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// Insert rows [start, m) of X in order.  One CTA.  When the whole tree (plus the growth one
+// launch may need) fits in the cap_s_sm / cap_n_sm pool carved from shared memory, the tree is
+// moved there for the launch and written back at its end (every dependent lookup of the descent
+// then costs a shared-memory access instead of an L2 round trip); otherwise it is used in place.
+__global__ void __launch_bounds__(kFitThreads, 1) birch_fit_kernel(TreeDev t, const float* __restrict__ X, int64_t m,
+                                                                    int64_t start, int64_t cap_s_sm, int64_t cap_n_sm) {
+    extern __shared__ double fit_smem[];
+    __shared__ FitShared sh;
+    __shared__ int use_sm;
+    const int d = t.d, B1 = t.B + 1;
+    double* xs = fit_smem;              // [d] the point
+    double* tmp = fit_smem + d;         // [2d] merge candidate LS', c'
+    double* D = fit_smem + 3 * d;       // [(B+1)^2] split distances
+    float* xring = reinterpret_cast<float*>(D + (((size_t)B1 * B1 + 1) & ~(size_t)1));  // [2][CH][d] staged rows
+    const int CH = ring_rows(d);
+    // shared-memory pool (if it holds the tree with room for at least a few hundred inserts)
+    if (threadIdx.x == 0) {
+        const long long ns0 = t.hdr[H_NS], nn0 = t.hdr[H_NN], dep0 = t.hdr[H_DEPTH];
+        use_sm = cap_s_sm > 0 && ns0 + 64 + 2 * (dep0 + 2) <= cap_s_sm && nn0 + 2 * (dep0 + 2) + 8 <= cap_n_sm;
+    }
+    __syncthreads();
     if (use_sm) {
+        TreeDev T = t;  // every pointer derived from fit_smem in this branch only
+        char* p = reinterpret_cast<char*>(xring + (size_t)2 * CH * d);
+        T.n = reinterpret_cast<double*>(p);
+        T.ss = T.n + cap_s_sm;
+        T.sqn = T.ss + cap_s_sm;
+        T.ls = T.sqn + cap_s_sm;
+        T.cen = T.ls + cap_s_sm * d;
+        T.ldc = (d & 1) ? d : d + 2;
+        T.hdr = reinterpret_cast<long long*>(T.cen + cap_s_sm * T.ldc);
+        T.child = reinterpret_cast<int32_t*>(T.hdr + H_WORDS);
+        T.is_leaf = T.child + cap_s_sm;
+        T.nsub = T.is_leaf + cap_n_sm;
+        T.prev = T.nsub + cap_n_sm;
+        T.next = T.prev + cap_n_sm;
+        T.sub = T.next + cap_n_sm;
+        T.cap_s = cap_s_sm;
+        T.cap_n = cap_n_sm;
+        copy_tree(T, t, t.hdr[H_NS], t.hdr[H_NN]);
+        __syncthreads();
+        fit_rows<true>(T, X, m, start, xs, tmp, D, xring, sh);
         __syncthreads();
         copy_tree(t, T, T.hdr[H_NS], T.hdr[H_NN]);
+    } else {
+        fit_rows<false>(t, X, m, start, xs, tmp, D, xring, sh);
     }
 }
 
