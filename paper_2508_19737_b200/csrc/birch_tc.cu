@@ -176,7 +176,8 @@ struct TcArgs {
     const float* X;      // the rows [m][d] and the clusters (fp64), for the exact re-check
     const double* cen;
     const double* sqn;
-    int64_t m;
+    int64_t m;     // rows of this launch (a chunk of the call's rows)
+    int64_t row0;  // the chunk's first row in the call (amb_rows holds call-level indices)
     int n_tiles;
     int d;
     int32_t* labels;
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
             } else {  // not certified: the fp64 pass decides
                 a.labels[gi] = -1;
                 const unsigned long long k = atomicAdd(a.amb_count, 1ull);
-                a.amb_rows[k] = (int32_t)gi;
+                a.amb_rows[k] = (int32_t)(a.row0 + gi);
             }
         }
     }
@@ -399,11 +400,14 @@ bool birch_tc_eligible(int d, int64_t K) {
 
 igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int d, const float* X, int64_t m,
                            int32_t* labels, int32_t* amb_rows, unsigned long long* amb_count, cudaStream_t s) {
-    const int64_t mt = (m + kTcM - 1) / kTcM, nt = (K + kTcN - 1) / kTcN;
+    // rows in chunks of at most kChunk (bounded workspace), the centroids split once
+    constexpr int64_t kChunk = (int64_t)1 << 22;
+    const int64_t mc = m < kChunk ? m : kChunk;
+    const int64_t mt = (mc + kTcM - 1) / kTcM, nt = (K + kTcN - 1) / kTcN;
     const size_t xf = (size_t)mt * kTcM * d, cf = (size_t)nt * kTcN * d;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t o_xl = al(4 * xf), o_ch = o_xl + al(4 * xf), o_cl = o_ch + al(4 * cf), o_sq = o_cl + al(4 * cf),
-                 o_xn = o_sq + al(4 * (size_t)nt * kTcN), o_st = o_xn + al(4 * (size_t)m), total = o_st + al(4 * S_WORDS);
+                 o_xn = o_sq + al(4 * (size_t)nt * kTcN), o_st = o_xn + al(4 * (size_t)mc), total = o_st + al(4 * S_WORDS);
     char* ws = nullptr;
     IGP_CUDA(alloc_async((void**)&ws, total, s), "birch tc workspace");
     float* xh = (float*)ws;
@@ -416,22 +420,24 @@ igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int 
     igp_status r = cuda_status(cudaMemsetAsync(st, 0, 4 * S_WORDS, s), "memset");
     if (r == IGP_OK) r = cuda_status(cudaMemsetAsync(amb_count, 0, 2 * sizeof(unsigned long long), s), "memset");
     if (r == IGP_OK) {
-        tc_split_kernel<float><<<(unsigned)((mt * kTcM + 255) / 256), 256, 0, s>>>(X, m, mt * kTcM, d, xh, xl, xn, nullptr,
-                                                                              nullptr, nullptr);
-        r = launch_status("tc_split_kernel<float>");
-    }
-    if (r == IGP_OK) {
         tc_split_kernel<double><<<(unsigned)((nt * kTcN + 255) / 256), 256, 0, s>>>(cen, K, nt * kTcN, d, ch, cl, nullptr,
                                                                                 sqn, sq, st);
         r = launch_status("tc_split_kernel<double>");
     }
-    if (r == IGP_OK) {
-        const size_t smem = tc_smem_bytes(d);
+    const size_t smem = tc_smem_bytes(d);
+    if (r == IGP_OK)
         r = cuda_status(cudaFuncSetAttribute(birch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "birch tc smem attribute");
+    for (int64_t row0 = 0; row0 < m && r == IGP_OK; row0 += kChunk) {
+        const int64_t rows = m - row0 < kChunk ? m - row0 : kChunk;
+        const int64_t rt = (rows + kTcM - 1) / kTcM;
+        const float* Xc = X + row0 * d;
+        tc_split_kernel<float><<<(unsigned)((rt * kTcM + 255) / 256), 256, 0, s>>>(Xc, rows, rt * kTcM, d, xh, xl, xn,
+                                                                              nullptr, nullptr, nullptr);
+        r = launch_status("tc_split_kernel<float>");
         if (r == IGP_OK) {
-            TcArgs ar{xh, xl, ch, cl, sq, xn, st, X, cen, sqn, m, (int)nt, d, labels, amb_rows, amb_count};
-            birch_tc_kernel<<<(unsigned)mt, kTcThreads, smem, s>>>(ar);
+            TcArgs ar{xh, xl, ch, cl, sq, xn, st, Xc, cen, sqn, rows, row0, (int)nt, d, labels + row0, amb_rows, amb_count};
+            birch_tc_kernel<<<(unsigned)rt, kTcThreads, smem, s>>>(ar);
             r = launch_status("birch_tc_kernel");
         }
     }

@@ -207,6 +207,20 @@ def test_birch_tensor_predict_streaming_scale(igp):
     g.close()
 
 
+def test_birch_tensor_predict_row_chunks(igp):
+    """More rows than one tensor-core pass takes (2^22 per chunk; the chunks share the centroid
+    split and the uncertified-row list): tensor path == fp64 path on 2^22 + 1000 rows."""
+    g = torch.Generator().manual_seed(8)
+    fit = torch.rand((3000, 8), generator=g).cuda()
+    b = igp.Birch(8, 0.15, 50).partial_fit(fit)
+    Q = torch.rand(((1 << 22) + 1000, 8), generator=g).cuda()
+    lab, amb = b.predict(Q, path="tensor", return_ambiguous=True)
+    ref = b.predict(Q, path="fp64")
+    assert torch.equal(lab, ref)
+    record("birch_tc_chunks", {"K": b.info()[0], "rows": Q.shape[0], "ambiguous": amb})
+    b.close()
+
+
 def test_birch_errors(igp):
     with pytest.raises(igp.IGPError):
         igp.Birch(8, 0.0, 50)
