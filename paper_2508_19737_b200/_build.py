@@ -22,6 +22,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "-I" + os.path.join(ROOT, "include")]
 if os.environ.get("IGP_DEBUG") == "1":  # device asserts on every dereferenced index (igp_internal.cuh)
     FLAGS += ["-DIGP_DEBUG"]
+if os.environ.get("IGP_FIT_PROFILE") == "1":  # BIRCH fit phase cycle counts printed per launch (tooling)
+    FLAGS += ["-DIGP_FIT_PROFILE"]
 
 
 def _stale(target: str, deps) -> bool:

@@ -350,12 +350,27 @@ __device__ void copy_tree(const TreeDev& dst, const TreeDev& src, long long ns, 
 // derived from the kernel's shared-memory pool inside the same inlined body (the compiler then
 // emits shared-memory loads / stores instead of generic ones on the descent's dependent chain),
 // SM = false for trees left in global memory.
+#ifdef IGP_FIT_PROFILE  // phase cycle counts of thread 0, printed at the end of a launch (tooling builds only)
+#define FIT_MARK(k)                                  \
+    do {                                             \
+        const long long _t = clock64();              \
+        prof[k] += _t - prof_t;                      \
+        prof_t = _t;                                 \
+    } while (0)
+#else
+#define FIT_MARK(k) ((void)0)
+#endif
+
 template <bool SM>
 __device__ __forceinline__ void fit_rows(TreeDev T, const float* __restrict__ X, int64_t m, int64_t start, double* xs,
                                          double* tmp, double* D, float* xring, FitShared& sh) {
     const int d = T.d, B1 = T.B + 1;
     const int CH = ring_rows(d);
     const int g = threadIdx.x >> 1, r = threadIdx.x & 1;
+#ifdef IGP_FIT_PROFILE
+    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long prof_t = clock64();
+#endif
     if (threadIdx.x == 0) T.hdr[H_STOP] = m;
     auto issue_chunk = [&](int64_t c) {  // rows [start + c CH, ...) into ring slot c & 1
         const int64_t r0 = start + c * CH;
@@ -391,6 +406,7 @@ __device__ __forceinline__ void fit_rows(TreeDev T, const float* __restrict__ X,
             for (int k = threadIdx.x; k < d; k += kFitThreads) xs[k] = (double)xr[k];
         }
         __syncthreads();
+        FIT_MARK(0);
         double xx = 0.0;  // |x|^2: computed beside the leaf's merge test (not on the descent's path)
         const int root = (int)T.hdr[H_ROOT];
         if (T.nsub[root] == 0) {  // the empty root leaf takes the first point
@@ -434,6 +450,7 @@ __device__ __forceinline__ void fit_rows(TreeDev T, const float* __restrict__ X,
             v = T.child[T.sub[(int64_t)v * B1 + j]];
         }
         __syncthreads();
+        FIT_MARK(1);
         // leaf: merge into the closest entry if the merged radius^2 <= T^2, else append
         const int leaf = v;
         const int sj = T.sub[(int64_t)leaf * B1 + sh.path_j[depth - 1]];
@@ -459,6 +476,7 @@ __device__ __forceinline__ void fit_rows(TreeDev T, const float* __restrict__ X,
         }
         __syncthreads();
         xx = sh.scal[0];
+        FIT_MARK(2);
         int split = 0;
         if (sh.flag) {
             for (int k = threadIdx.x; k < d; k += kFitThreads) {
@@ -482,6 +500,7 @@ __device__ __forceinline__ void fit_rows(TreeDev T, const float* __restrict__ X,
             __syncthreads();
             split = T.nsub[leaf] > T.B;
         }
+        FIT_MARK(3);
         // back up the path: splits bottom-up while they propagate, then one batched CF update of
         // every remaining ancestor entry (distinct entries: their order does not matter)
         int l = depth - 2;
@@ -497,6 +516,7 @@ __device__ __forceinline__ void fit_rows(TreeDev T, const float* __restrict__ X,
             __syncthreads();
             split = T.nsub[pv] > T.B;
         }
+        FIT_MARK(5);
         if (l >= 0) {  // levels 0..l: CF_e += x, c = LS / n, sqn = |c|^2
             const int nl = l + 1;
             for (int idx = threadIdx.x; idx < nl * d; idx += kFitThreads) {
@@ -532,8 +552,15 @@ __device__ __forceinline__ void fit_rows(TreeDev T, const float* __restrict__ X,
             }
         }
         if (threadIdx.x == 0) T.hdr[H_NPOINTS]++;
+        FIT_MARK(4);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+#ifdef IGP_FIT_PROFILE
+    if (threadIdx.x == 0)
+        printf("fit profile (cycles, thread 0; rows %lld..%lld, smem tree %d): top+stage %lld descent %lld merge-test %lld "
+               "write %lld ancestors+root %lld split %lld\n",
+               (long long)start, (long long)T.hdr[H_STOP], (int)SM, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5]);
+#endif
 }
 
 // Insert rows [start, m) of X in order.  One CTA.  When the whole tree (plus the growth one
