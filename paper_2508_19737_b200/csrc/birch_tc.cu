@@ -40,14 +40,18 @@ namespace igp {
 namespace {
 
 constexpr int kTcM = 128;      // rows per CTA: MMA M, TMEM lanes
-constexpr int kTcN = 128;      // centroids per tile: MMA N, TMEM columns per accumulator
-constexpr int kTcStages = 2;   // centroid-tile ring depth
+// centroids per tile (MMA N, TMEM columns per accumulator): a template parameter N -- 256 for
+// d >= 48 (half the row-tile re-reads per flop: the operand reads share the shared-memory pipe with
+// the ring fills), 128 below (there the 256-column epilogue would outlast the tile's MMAs)
+constexpr int kTcKC = 32;      // K columns per ring stage (a centroid tile is ceil(d / 32) stages)
+constexpr int kTcStages = 2;   // ring depth
 constexpr int kTcThreads = 192;
-constexpr int kTcTmemCols = 2 * kTcN;  // two accumulators (power of two >= 32)
 // idesc (kind::tf32): c_format F32 (bits 4-5 = 1), a/b_format TF32 (bits 7-9, 10-12 = 2),
 // both K-major (bits 15, 16 = 0), N >> 3 at bits 17-22, M >> 4 at bits 24-28
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
-                            ((uint32_t)(kTcM >> 4) << 24);
+template <int N>
+__host__ __device__ constexpr uint32_t idesc_tf32() {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+}
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -85,12 +89,13 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
+template <int N>
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %3, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(accumulate), "r"(kIdesc)
+        "l"(a), "l"(b), "r"(accumulate), "r"(idesc_tf32<N>())
         : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -126,16 +131,22 @@ enum { S_SQMAX = 0, S_WORDS = 4 };
 // Rows >= `rows` (padding up to a multiple of 128) are zero.  Rows (T = float): norm[r] = an
 // upper bound of |x_r| (NaN / inf propagate).  Centroids (sqn given): sq32[r] = (float)sqn[r]
 // (+inf for padding, so padded centroids never win) and stats[S_SQMAX] = max sqn.
+// Tiles of TR rows; inside a tile, K chunks of KC columns (the last one d - KC floor(..) wide), each
+// chunk a canonical block (row groups 32 w bytes apart for chunk width w) -- rows: TR = 128, KC = d
+// (one block per tile); centroids: TR = 256, KC = 32 (one block per ring stage).
 template <typename T>
-__global__ void tc_split_kernel(const T* __restrict__ src, int64_t rows, int64_t rows_pad, int d, float* __restrict__ hi,
-                                float* __restrict__ lo, float* __restrict__ norm, const double* __restrict__ sqn,
-                                float* __restrict__ sq32, unsigned* stats) {
+__global__ void tc_split_kernel(const T* __restrict__ src, int64_t rows, int64_t rows_pad, int d, int TR, int KC,
+                                float* __restrict__ hi, float* __restrict__ lo, float* __restrict__ norm,
+                                const double* __restrict__ sqn, float* __restrict__ sq32, unsigned* stats) {
     float smax = 0.f;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows_pad; r += (int64_t)gridDim.x * blockDim.x) {
-        float* h = hi + (r >> 7) * (int64_t)kTcM * d + ((r & 127) >> 3) * (int64_t)8 * d + (r & 7) * 4;
-        float* l = lo + (h - hi);
+        const int64_t tile = r / TR;
+        const int rr = (int)(r - tile * TR);
         float n2 = 0.f;
         for (int c = 0; c < d / 4; ++c) {
+            const int k0 = 4 * c, ck = k0 / KC, w = d - ck * KC < KC ? d - ck * KC : KC;
+            const int64_t off = tile * (int64_t)TR * d + (int64_t)ck * TR * KC + (rr >> 3) * (int64_t)8 * w +
+                                ((k0 - ck * KC) >> 2) * 32 + (rr & 7) * 4;
             float v[4] = {0.f, 0.f, 0.f, 0.f};
             if (r < rows) {
                 const T* p = src + r * d + 4 * c;
@@ -145,8 +156,8 @@ __global__ void tc_split_kernel(const T* __restrict__ src, int64_t rows, int64_t
             float4 vh, vl;
             vh.x = to_tf32(v[0]); vh.y = to_tf32(v[1]); vh.z = to_tf32(v[2]); vh.w = to_tf32(v[3]);
             vl.x = v[0] - vh.x; vl.y = v[1] - vh.y; vl.z = v[2] - vh.z; vl.w = v[3] - vh.w;  // exact in fp32
-            *reinterpret_cast<float4*>(h + 32 * c) = vh;
-            *reinterpret_cast<float4*>(l + 32 * c) = vl;
+            *reinterpret_cast<float4*>(hi + off) = vh;
+            *reinterpret_cast<float4*>(lo + off) = vl;
             n2 = fmaf(v[0], v[0], fmaf(v[1], v[1], fmaf(v[2], v[2], fmaf(v[3], v[3], n2))));
         }
         // fp32 sum of d squares: relative error below d 2^-24; inflate past it
@@ -198,16 +209,20 @@ __device__ __forceinline__ double exact_dist(const float* __restrict__ x, const 
     return __dadd_rn(sq, -2.0 * dt);
 }
 
+template <int kTcN>
 __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
+    constexpr int kTcTmemCols = 2 * kTcN;  // two accumulators
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     __shared__ __align__(8) uint64_t bar_full[kTcStages], bar_empty[kTcStages], bar_tfull[2], bar_tempty[2], bar_a;
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(16) float sq_stage[4 * 2 * kTcN];  // epilogue warps' |c_j|^2 tiles
     const int d = a.d;
-    const uint32_t tile_floats = (uint32_t)kTcM * d, tile_bytes = 4u * tile_floats;
+    const int nc = (d + kTcKC - 1) / kTcKC;  // ring stages per centroid tile
+    const uint32_t a_floats = (uint32_t)kTcM * d, a_bytes = 4u * a_floats;
+    const uint32_t st_floats = (uint32_t)kTcN * (d < kTcKC ? d : kTcKC);  // one stage's hi (or lo) capacity
     float* sA_hi = reinterpret_cast<float*>(tc_smem);
-    float* sA_lo = sA_hi + tile_floats;
-    float* sB = sA_lo + tile_floats;  // stage s: hi at sB + 2 s tile, lo right after
+    float* sA_lo = sA_hi + a_floats;
+    float* sB = sA_lo + a_floats;  // stage q: hi at sB + 2 q st_floats, lo right after
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t mt = blockIdx.x;
 
@@ -236,37 +251,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(&bar_a, 2 * tile_bytes);
-            bulk_g2s(sA_hi, a.xh + mt * tile_floats, tile_bytes, &bar_a);
-            bulk_g2s(sA_lo, a.xl + mt * tile_floats, tile_bytes, &bar_a);
+            mbar_expect_tx(&bar_a, 2 * a_bytes);
+            bulk_g2s(sA_hi, a.xh + mt * a_floats, a_bytes, &bar_a);
+            bulk_g2s(sA_lo, a.xl + mt * a_floats, a_bytes, &bar_a);
             for (int t = 0; t < a.n_tiles; ++t) {
-                const int s = t % kTcStages;
-                if (t >= kTcStages) mbar_wait(&bar_empty[s], (uint32_t)((t / kTcStages - 1) & 1));
-                float* dst = sB + (size_t)2 * s * tile_floats;
-                mbar_expect_tx(&bar_full[s], 2 * tile_bytes);
-                bulk_g2s(dst, a.ch + (size_t)t * tile_floats, tile_bytes, &bar_full[s]);
-                bulk_g2s(dst + tile_floats, a.cl + (size_t)t * tile_floats, tile_bytes, &bar_full[s]);
+                for (int c = 0; c < nc; ++c) {
+                    const int u = t * nc + c, q = u % kTcStages;  // stage use u
+                    const int w = d - c * kTcKC < kTcKC ? d - c * kTcKC : kTcKC;
+                    const uint32_t bytes = 4u * kTcN * w;
+                    if (u >= kTcStages) mbar_wait(&bar_empty[q], (uint32_t)((u / kTcStages - 1) & 1));
+                    float* dst = sB + (size_t)2 * q * st_floats;
+                    const size_t src = (size_t)t * kTcN * d + (size_t)c * kTcN * kTcKC;
+                    mbar_expect_tx(&bar_full[q], 2 * bytes);
+                    bulk_g2s(dst, a.ch + src, bytes, &bar_full[q]);
+                    bulk_g2s(dst + st_floats, a.cl + src, bytes, &bar_full[q]);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             mbar_wait(&bar_a, 0);
             tc_fence_after();
-            const uint32_t a_hi = sa(sA_hi), a_lo = sa(sA_lo), sbo = 32u * d;
+            const uint32_t a_hi = sa(sA_hi), a_lo = sa(sA_lo), sbo_a = 32u * d;
             for (int t = 0; t < a.n_tiles; ++t) {
-                const int s = t % kTcStages, b = t & 1;
-                mbar_wait(&bar_full[s], (uint32_t)((t / kTcStages) & 1));
+                const int b = t & 1;
                 if (t >= 2) mbar_wait(&bar_tempty[b], (uint32_t)(((t >> 1) - 1) & 1));
-                tc_fence_after();
-                const uint32_t b_hi = sa(sB + (size_t)2 * s * tile_floats), b_lo = b_hi + tile_bytes;
                 const uint32_t acc = tmem + (uint32_t)(b * kTcN);
-                for (int kk = 0; kk < d / 8; ++kk) {  // K = 8 tf32 = two 16-byte chunks per MMA
-                    const uint32_t o = 256u * kk;
-                    mma_tf32(acc, umma_desc(a_lo + o, 128, sbo), umma_desc(b_hi + o, 128, sbo), kk > 0);
-                    mma_tf32(acc, umma_desc(a_hi + o, 128, sbo), umma_desc(b_lo + o, 128, sbo), 1);
-                    mma_tf32(acc, umma_desc(a_hi + o, 128, sbo), umma_desc(b_hi + o, 128, sbo), 1);
+                for (int c = 0; c < nc; ++c) {
+                    const int u = t * nc + c, q = u % kTcStages;
+                    const int w = d - c * kTcKC < kTcKC ? d - c * kTcKC : kTcKC;
+                    mbar_wait(&bar_full[q], (uint32_t)((u / kTcStages) & 1));
+                    tc_fence_after();
+                    const uint32_t b_hi = sa(sB + (size_t)2 * q * st_floats), b_lo = sa(sB + (size_t)(2 * q + 1) * st_floats);
+                    const uint32_t sbo_b = 32u * w;
+                    for (int kk = 0; kk < w / 8; ++kk) {  // K = 8 tf32 = two 16-byte chunks per MMA
+                        const uint32_t oa = 128u * (uint32_t)(c * kTcKC / 4 + 2 * kk), ob = 256u * kk;
+                        mma_tf32<kTcN>(acc, umma_desc(a_lo + oa, 128, sbo_a), umma_desc(b_hi + ob, 128, sbo_b), c > 0 || kk > 0);
+                        mma_tf32<kTcN>(acc, umma_desc(a_hi + oa, 128, sbo_a), umma_desc(b_lo + ob, 128, sbo_b), 1);
+                        mma_tf32<kTcN>(acc, umma_desc(a_hi + oa, 128, sbo_a), umma_desc(b_hi + ob, 128, sbo_b), 1);
+                    }
+                    mma_commit(&bar_empty[q]);  // ring stage free once these MMAs have read it
                 }
-                mma_commit(&bar_empty[s]);  // ring slot free once these MMAs have read it
                 mma_commit(&bar_tfull[b]);  // accumulator b complete
             }
         }
@@ -297,12 +322,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
         // |c_j|^2 of the tile, staged per warp in shared memory (broadcast reads), the next tile's
         // values loaded into registers while this tile is processed
         float* sqw = sq_stage + q * 2 * kTcN;
-        float4 nxt = __ldg(reinterpret_cast<const float4*>(a.sq) + lane);
+        constexpr int kV = kTcN / 128;  // float4s per lane per tile
+        float4 nxt[kV];
+#pragma unroll
+        for (int v = 0; v < kV; ++v) nxt[v] = __ldg(reinterpret_cast<const float4*>(a.sq) + 32 * v + lane);
         for (int t = 0; t < a.n_tiles; ++t) {
             const int b = t & 1;
-            reinterpret_cast<float4*>(sqw + b * kTcN)[lane] = nxt;
+#pragma unroll
+            for (int v = 0; v < kV; ++v) reinterpret_cast<float4*>(sqw + b * kTcN)[32 * v + lane] = nxt[v];
             __syncwarp();
-            if (t + 1 < a.n_tiles) nxt = __ldg(reinterpret_cast<const float4*>(a.sq + (size_t)(t + 1) * kTcN) + lane);
+            if (t + 1 < a.n_tiles) {
+#pragma unroll
+                for (int v = 0; v < kV; ++v)
+                    nxt[v] = __ldg(reinterpret_cast<const float4*>(a.sq + (size_t)(t + 1) * kTcN) + 32 * v + lane);
+            }
             mbar_wait(&bar_tfull[b], (uint32_t)((t >> 1) & 1));
             tc_fence_after();
             const float* sqt = sqw + b * kTcN;
@@ -383,10 +416,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcTmemCols) : "memory");
 }
 
+int tc_tile_n(int d) { return d >= 48 ? 256 : 128; }
+
 size_t tc_smem_bytes(int d) {
-    const size_t need = sizeof(float) * (size_t)kTcM * d * (2 + 2 * kTcStages);
-    // at least ~100 KB: at most two CTAs share an SM, so their 2 x 256 TMEM columns always fit
-    return need > 100 * 1024 ? need : 100 * 1024;
+    const size_t kc = d < kTcKC ? d : kTcKC, n = tc_tile_n(d);
+    const size_t need = sizeof(float) * ((size_t)2 * kTcM * d + (size_t)2 * kTcStages * n * kc);
+    // at most 512 / (2 n) CTAs per SM, so their TMEM columns always fit: N = 256 needs the whole
+    // TMEM (more than half an SM's shared memory), N = 128 half of it (over a third)
+    const size_t floor_bytes = n == 256 ? 120 * 1024 : 80 * 1024;
+    return need > floor_bytes ? need : floor_bytes;
 }
 
 }  // namespace
@@ -394,7 +432,7 @@ size_t tc_smem_bytes(int d) {
 bool birch_tc_eligible(int d, int64_t K) {
     DeviceInfo di;
     if (!device_info(&di)) return false;
-    return d >= 8 && d <= kBirchTcMaxD && d % 8 == 0 && K >= 1 && K < (int64_t)INT32_MAX - kTcN &&
+    return d >= 8 && d <= kBirchTcMaxD && d % 8 == 0 && K >= 1 && K < (int64_t)INT32_MAX - 256 &&
            tc_smem_bytes(d) <= (size_t)di.max_smem_optin;
 }
 
@@ -403,6 +441,7 @@ igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int 
     // rows in chunks of at most kChunk (bounded workspace), the centroids split once
     constexpr int64_t kChunk = (int64_t)1 << 22;
     const int64_t mc = m < kChunk ? m : kChunk;
+    const int kTcN = tc_tile_n(d);
     const int64_t mt = (mc + kTcM - 1) / kTcM, nt = (K + kTcN - 1) / kTcN;
     const size_t xf = (size_t)mt * kTcM * d, cf = (size_t)nt * kTcN * d;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -420,24 +459,25 @@ igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int 
     igp_status r = cuda_status(cudaMemsetAsync(st, 0, 4 * S_WORDS, s), "memset");
     if (r == IGP_OK) r = cuda_status(cudaMemsetAsync(amb_count, 0, 2 * sizeof(unsigned long long), s), "memset");
     if (r == IGP_OK) {
-        tc_split_kernel<double><<<(unsigned)((nt * kTcN + 255) / 256), 256, 0, s>>>(cen, K, nt * kTcN, d, ch, cl, nullptr,
-                                                                                sqn, sq, st);
+        tc_split_kernel<double><<<(unsigned)((nt * kTcN + 255) / 256), 256, 0, s>>>(cen, K, nt * kTcN, d, kTcN, kTcKC, ch,
+                                                                                cl, nullptr, sqn, sq, st);
         r = launch_status("tc_split_kernel<double>");
     }
     const size_t smem = tc_smem_bytes(d);
+    auto kern = kTcN == 256 ? birch_tc_kernel<256> : birch_tc_kernel<128>;
     if (r == IGP_OK)
-        r = cuda_status(cudaFuncSetAttribute(birch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+        r = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "birch tc smem attribute");
     for (int64_t row0 = 0; row0 < m && r == IGP_OK; row0 += kChunk) {
         const int64_t rows = m - row0 < kChunk ? m - row0 : kChunk;
         const int64_t rt = (rows + kTcM - 1) / kTcM;
         const float* Xc = X + row0 * d;
-        tc_split_kernel<float><<<(unsigned)((rt * kTcM + 255) / 256), 256, 0, s>>>(Xc, rows, rt * kTcM, d, xh, xl, xn,
-                                                                              nullptr, nullptr, nullptr);
+        tc_split_kernel<float><<<(unsigned)((rt * kTcM + 255) / 256), 256, 0, s>>>(Xc, rows, rt * kTcM, d, kTcM, d, xh,
+                                                                              xl, xn, nullptr, nullptr, nullptr);
         r = launch_status("tc_split_kernel<float>");
         if (r == IGP_OK) {
             TcArgs ar{xh, xl, ch, cl, sq, xn, st, Xc, cen, sqn, rows, row0, (int)nt, d, labels + row0, amb_rows, amb_count};
-            birch_tc_kernel<<<(unsigned)rt, kTcThreads, smem, s>>>(ar);
+            kern<<<(unsigned)rt, kTcThreads, smem, s>>>(ar);
             r = launch_status("birch_tc_kernel");
         }
     }

@@ -159,10 +159,11 @@ def test_birch_tensor_predict_huge_values_all_fp64(igp):
     g.close()
 
 
-@pytest.mark.parametrize("d", [8, 24, 32, 64])
+@pytest.mark.parametrize("d", [8, 24, 32, 40, 48, 56, 64])
 def test_birch_tensor_predict_many_clusters(igp, d):
-    """Thousands of clusters (several 128-centroid tiles, a ragged last tile) and a ragged last
-    row tile: tensor path == fp64 path == oracle; almost every row certified."""
+    """Thousands of clusters (many centroid tiles, a ragged last tile) and a ragged last row tile,
+    every tile shape: N = 128 (d < 48) and 256 (d >= 48), one K stage (d <= 32) or two, full or
+    partial (d = 40, 48, 56): tensor path == fp64 path == oracle; almost every row certified."""
     rng = np.random.default_rng(10 + d)
     X = 1 / (1 + np.exp(-rng.normal(0, 1, (6000, d))))
     g, ocen, osqn = fit_clusters(igp, X, 0.35 * np.sqrt(d / 64), 50)
