@@ -24,6 +24,8 @@ if os.environ.get("IGP_DEBUG") == "1":  # device asserts on every dereferenced i
     FLAGS += ["-DIGP_DEBUG"]
 if os.environ.get("IGP_FIT_PROFILE") == "1":  # BIRCH fit phase cycle counts printed per launch (tooling)
     FLAGS += ["-DIGP_FIT_PROFILE"]
+if os.environ.get("IGP_TC_STATS") == "1":  # tensor-core predict: rows re-checked / sent to fp64 (tooling)
+    FLAGS += ["-DIGP_TC_STATS"]
 
 
 def _stale(target: str, deps) -> bool:

@@ -25,6 +25,7 @@
 // leaf centroids (first minimum), one thread per point, cluster tiles staged in shared memory.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -1145,6 +1146,10 @@ igp_status igp_birch_predict_ex(igp_birch_t b, const float* d_X, int64_t m, int3
         if (st == IGP_OK) st = cuda_status(cudaStreamSynchronize(s), "sync");
         n = (int64_t)h[0];
         if (ambiguous) *ambiguous = (int64_t)(h[0] + h[1]);
+#ifdef IGP_TC_STATS  // diagnostics builds: how the tensor-core pass settled the rows
+        fprintf(stderr, "birch tc predict: %lld rows, K %lld: %llu re-checked in the kernel, %llu to the fp64 pass\n",
+                (long long)m, (long long)K, h[1], h[0]);
+#endif
     }
     if (st == IGP_OK && n > 0) st = launch_predict_fp64(cen, sqn, K, d, d_X, n, tc ? amb_rows : nullptr, d_labels, s);
     free_async(cen, s);

@@ -208,6 +208,25 @@ def test_birch_tensor_predict_streaming_scale(igp):
     g.close()
 
 
+def test_birch_tensor_predict_degenerate_sizes(igp):
+    """One cluster (K = 1: every row's second-best is the +inf padding), one row, and K just
+    past a tile boundary (257 clusters: a 1-centroid ragged tile), on the tensor path."""
+    b = igp.Birch(16, 0.5, 50).partial_fit(torch.full((10, 16), 0.25, device="cuda"))
+    assert b.info()[0] == 1
+    lab, amb = b.predict(torch.rand((300, 16), device="cuda"), path="tensor", return_ambiguous=True)
+    assert torch.all(lab == 0) and amb == 0
+    assert b.predict(torch.rand((1, 16), device="cuda"), path="tensor").tolist() == [0]
+    b.close()
+    rng = np.random.default_rng(12)
+    X = rng.random((257, 64)) * 4  # well separated: every row its own cluster
+    g, ocen, osqn = fit_clusters(igp, X, 1e-3, 50)
+    assert ocen.shape[0] == 257
+    Q = f32(np.concatenate([X, rng.random((100, 64)) * 4]))
+    lab = g.predict(torch.from_numpy(Q).cuda(), path="tensor").cpu().numpy()
+    assert np.array_equal(lab, oracle.birch_predict(ocen, osqn, Q.astype(np.float64)))
+    g.close()
+
+
 def test_birch_tensor_predict_row_chunks(igp):
     """More rows than one tensor-core pass takes (2^22 per chunk; the chunks share the centroid
     split and the uncertified-row list): tensor path == fp64 path on 2^22 + 1000 rows."""
