@@ -135,9 +135,10 @@ enum { S_SQMAX = 0, S_WORDS = 4 };
 // chunk a canonical block (row groups 32 w bytes apart for chunk width w) -- rows: TR = 128, KC = d
 // (one block per tile); centroids: TR = 256, KC = 32 (one block per ring stage).
 template <typename T>
-__global__ void tc_split_kernel(const T* __restrict__ src, int64_t rows, int64_t rows_pad, int d, int TR, int KC,
-                                float* __restrict__ hi, float* __restrict__ lo, float* __restrict__ norm,
-                                const double* __restrict__ sqn, float* __restrict__ sq32, unsigned* stats) {
+__global__ void tc_split_kernel(const T* __restrict__ src, const int32_t* __restrict__ list, int64_t rows,
+                                int64_t rows_pad, int d, int TR, int KC, float* __restrict__ hi, float* __restrict__ lo,
+                                float* __restrict__ norm, const double* __restrict__ sqn, float* __restrict__ sq32,
+                                unsigned* stats) {
     float smax = 0.f;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows_pad; r += (int64_t)gridDim.x * blockDim.x) {
         const int64_t tile = r / TR;
@@ -149,7 +150,7 @@ __global__ void tc_split_kernel(const T* __restrict__ src, int64_t rows, int64_t
                                 ((k0 - ck * KC) >> 2) * 32 + (rr & 7) * 4;
             float v[4] = {0.f, 0.f, 0.f, 0.f};
             if (r < rows) {
-                const T* p = src + r * d + 4 * c;
+                const T* p = src + (list ? (int64_t)list[r] : r) * d + 4 * c;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) v[u] = (float)p[u];
             }
@@ -190,11 +191,20 @@ struct TcArgs {
     int64_t m;     // rows of this launch (a chunk of the call's rows)
     int64_t row0;  // the chunk's first row in the call (amb_rows holds call-level indices)
     int n_tiles;
+    int tiles_per_split;  // centroid tiles per CTA column: blockIdx.y takes [y tps, (y+1) tps)
     int d;
     int32_t* labels;
     int32_t* amb_rows;
     unsigned long long* amb_count;  // [0] rows left to the fp64 pass, [1] rows re-checked here in fp64
+    float* amb_thr;                 // pass 1: each listed row's threshold best + 2M (beside amb_rows)
+    // pass 2 (collect mode): the rows are the listed ones; each row's pass-1 threshold in, every
+    // column with a <= threshold out (at most kCandCap; ccnt = -1 past that)
+    const float* row_thr;
+    int32_t* cand;
+    int32_t* ccnt;
 };
+
+constexpr int kCandCap = 32;
 
 // d_ij in fp64 exactly as the oracle (and birch.cu's fp64 kernel) evaluates it: eight partial
 // sums p[k mod 8] by fma, combined pairwise, then sqn_j + (-2 dot)
@@ -209,7 +219,7 @@ __device__ __forceinline__ double exact_dist(const float* __restrict__ x, const 
     return __dadd_rn(sq, -2.0 * dt);
 }
 
-template <int kTcN>
+template <int kTcN, bool kCollect>
 __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
     constexpr int kTcTmemCols = 2 * kTcN;  // two accumulators
     extern __shared__ __align__(1024) unsigned char tc_smem[];
@@ -225,6 +235,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
     float* sB = sA_lo + a_floats;  // stage q: hi at sB + 2 q st_floats, lo right after
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t mt = blockIdx.x;
+    const int t0 = blockIdx.y * a.tiles_per_split;  // this CTA's centroid tiles: [t0, t0 + nT)
+    const int nT = a.n_tiles - t0 < a.tiles_per_split ? a.n_tiles - t0 : a.tiles_per_split;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTcStages; ++s) {
@@ -254,14 +266,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
             mbar_expect_tx(&bar_a, 2 * a_bytes);
             bulk_g2s(sA_hi, a.xh + mt * a_floats, a_bytes, &bar_a);
             bulk_g2s(sA_lo, a.xl + mt * a_floats, a_bytes, &bar_a);
-            for (int t = 0; t < a.n_tiles; ++t) {
+            for (int t = 0; t < nT; ++t) {
                 for (int c = 0; c < nc; ++c) {
                     const int u = t * nc + c, q = u % kTcStages;  // stage use u
                     const int w = d - c * kTcKC < kTcKC ? d - c * kTcKC : kTcKC;
                     const uint32_t bytes = 4u * kTcN * w;
                     if (u >= kTcStages) mbar_wait(&bar_empty[q], (uint32_t)((u / kTcStages - 1) & 1));
                     float* dst = sB + (size_t)2 * q * st_floats;
-                    const size_t src = (size_t)t * kTcN * d + (size_t)c * kTcN * kTcKC;
+                    const size_t src = (size_t)(t0 + t) * kTcN * d + (size_t)c * kTcN * kTcKC;
                     mbar_expect_tx(&bar_full[q], 2 * bytes);
                     bulk_g2s(dst, a.ch + src, bytes, &bar_full[q]);
                     bulk_g2s(dst + st_floats, a.cl + src, bytes, &bar_full[q]);
@@ -273,7 +285,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
             mbar_wait(&bar_a, 0);
             tc_fence_after();
             const uint32_t a_hi = sa(sA_hi), a_lo = sa(sA_lo), sbo_a = 32u * d;
-            for (int t = 0; t < a.n_tiles; ++t) {
+            for (int t = 0; t < nT; ++t) {
                 const int b = t & 1;
                 if (t >= 2) mbar_wait(&bar_tempty[b], (uint32_t)(((t >> 1) - 1) & 1));
                 const uint32_t acc = tmem + (uint32_t)(b * kTcN);
@@ -299,6 +311,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int row = q * 32 + lane;
         const int64_t gi = mt * kTcM + row;
+        if constexpr (kCollect) {  // pass 2: every column within the row's pass-1 threshold
+            const float thr = gi < a.m ? a.row_thr[gi] : -INFINITY;
+            for (int t = 0; t < nT; ++t) {
+                const int b = t & 1;
+                mbar_wait(&bar_tfull[b], (uint32_t)((t >> 1) & 1));
+                tc_fence_after();
+                const float* sqt = a.sq + (size_t)(t0 + t) * kTcN;
+#pragma unroll 1
+                for (int c0 = 0; c0 < kTcN; c0 += 64) {
+                    float v[64];
+                    tmem_ld64(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * kTcN + c0), v);
+#pragma unroll
+                    for (int j = 0; j < 64; j += 4) {
+                        const float4 s4 = __ldg(reinterpret_cast<const float4*>(sqt + c0 + j));
+                        const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (fmaf(-2.f, v[j + u], sv[u]) <= thr) {  // rare: near ties only
+                                const int slot = atomicAdd(a.ccnt + gi, 1);  // CTA columns append
+                                if (slot < kCandCap) a.cand[gi * kCandCap + slot] = (t0 + t) * kTcN + c0 + j + u;
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_tempty[b]);
+            }
+        } else {
         // the certified margin M_i: S_i = |x_i| max_j |c_j| bounds sum_k |x_ik c_jk|
         const float sqmax = __uint_as_float(a.stats[S_SQMAX]);
         const float cn = sqrtf(sqmax) * (1.f + 0x1p-20f);
@@ -325,16 +366,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
         constexpr int kV = kTcN / 128;  // float4s per lane per tile
         float4 nxt[kV];
 #pragma unroll
-        for (int v = 0; v < kV; ++v) nxt[v] = __ldg(reinterpret_cast<const float4*>(a.sq) + 32 * v + lane);
-        for (int t = 0; t < a.n_tiles; ++t) {
+        for (int v = 0; v < kV; ++v)
+            nxt[v] = __ldg(reinterpret_cast<const float4*>(a.sq + (size_t)t0 * kTcN) + 32 * v + lane);
+        for (int t = 0; t < nT; ++t) {  // pass 1 runs with one CTA column: t0 = 0, nT = n_tiles
             const int b = t & 1;
 #pragma unroll
             for (int v = 0; v < kV; ++v) reinterpret_cast<float4*>(sqw + b * kTcN)[32 * v + lane] = nxt[v];
             __syncwarp();
-            if (t + 1 < a.n_tiles) {
+            if (t + 1 < nT) {
 #pragma unroll
                 for (int v = 0; v < kV; ++v)
-                    nxt[v] = __ldg(reinterpret_cast<const float4*>(a.sq + (size_t)(t + 1) * kTcN) + 32 * v + lane);
+                    nxt[v] = __ldg(reinterpret_cast<const float4*>(a.sq + (size_t)(t0 + t + 1) * kTcN) + 32 * v + lane);
             }
             mbar_wait(&bar_tfull[b], (uint32_t)((t >> 1) & 1));
             tc_fence_after();
@@ -353,7 +395,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
                         const float av = fmaf(-2.f, v[j + u], sv[u]);
                         const bool nb = av < bb[u];
                         ss[u] = nb ? bb[u] : fminf(ss[u], av);
-                        jj[u] = nb ? t * kTcN + c0 + j + u : jj[u];
+                        jj[u] = nb ? (t0 + t) * kTcN + c0 + j + u : jj[u];
                         bb[u] = nb ? av : bb[u];
                     }
                 }
@@ -402,18 +444,51 @@ __global__ void __launch_bounds__(kTcThreads, 1) birch_tc_kernel(TcArgs a) {
                 }
                 a.labels[gi] = lbest;
                 atomicAdd(a.amb_count + 1, 1ull);
-            } else {  // not certified: the fp64 pass decides
+            } else {  // not certified alone: pass 2 collects the row's candidates
                 a.labels[gi] = -1;
                 const unsigned long long k = atomicAdd(a.amb_count, 1ull);
                 a.amb_rows[k] = (int32_t)(a.row0 + gi);
+                a.amb_thr[k] = thr;
             }
         }
+        }  // pass 1
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcTmemCols) : "memory");
+}
+
+// pass 3: the listed rows' labels from their candidates in fp64 (the oracle's order; smallest
+// distance, lowest index on ties); rows without a usable list (none, or more than kCandCap) go to
+// `out` for the fp64 pass over every cluster
+__global__ void tc_recheck_kernel(const int32_t* __restrict__ rows, int64_t n, const int32_t* __restrict__ cand,
+                                  const int32_t* __restrict__ ccnt, const float* __restrict__ X,
+                                  const double* __restrict__ cen, const double* __restrict__ sqn, int d,
+                                  int32_t* __restrict__ labels, int32_t* __restrict__ out,
+                                  unsigned long long* __restrict__ counts) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t row = rows[k];
+        const int c = ccnt[k];
+        if (c <= 0 || c > kCandCap) {
+            out[atomicAdd(counts, 1ull)] = row;
+            continue;
+        }
+        const float* x = X + (int64_t)row * d;
+        double dbest = INFINITY;
+        int lbest = INT32_MAX;
+        for (int i = 0; i < c; ++i) {
+            const int j = cand[k * kCandCap + i];
+            const double dj = exact_dist(x, cen + (int64_t)j * d, sqn[j], d);
+            if (dj < dbest || (dj == dbest && j < lbest)) {
+                dbest = dj;
+                lbest = j;
+            }
+        }
+        labels[row] = lbest;
+        atomicAdd(counts + 1, 1ull);
+    }
 }
 
 int tc_tile_n(int d) { return d >= 48 ? 256 : 128; }
@@ -440,13 +515,14 @@ igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int 
                            int32_t* labels, int32_t* amb_rows, unsigned long long* amb_count, cudaStream_t s) {
     // rows in chunks of at most kChunk (bounded workspace), the centroids split once
     constexpr int64_t kChunk = (int64_t)1 << 22;
-    const int64_t mc = m < kChunk ? m : kChunk;
     const int kTcN = tc_tile_n(d);
+    const int64_t mc = m < kChunk ? m : kChunk;
     const int64_t mt = (mc + kTcM - 1) / kTcM, nt = (K + kTcN - 1) / kTcN;
     const size_t xf = (size_t)mt * kTcM * d, cf = (size_t)nt * kTcN * d;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t o_xl = al(4 * xf), o_ch = o_xl + al(4 * xf), o_cl = o_ch + al(4 * cf), o_sq = o_cl + al(4 * cf),
-                 o_xn = o_sq + al(4 * (size_t)nt * kTcN), o_st = o_xn + al(4 * (size_t)mc), total = o_st + al(4 * S_WORDS);
+                 o_xn = o_sq + al(4 * (size_t)nt * kTcN), o_st = o_xn + al(4 * (size_t)mc),
+                 o_thr = o_st + al(4 * S_WORDS), total = o_thr + al(4 * (size_t)m);
     char* ws = nullptr;
     IGP_CUDA(alloc_async((void**)&ws, total, s), "birch tc workspace");
     float* xh = (float*)ws;
@@ -456,29 +532,94 @@ igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int 
     float* sq = (float*)(ws + o_sq);
     float* xn = (float*)(ws + o_xn);
     unsigned* st = (unsigned*)(ws + o_st);
+    float* thr = (float*)(ws + o_thr);
     igp_status r = cuda_status(cudaMemsetAsync(st, 0, 4 * S_WORDS, s), "memset");
     if (r == IGP_OK) r = cuda_status(cudaMemsetAsync(amb_count, 0, 2 * sizeof(unsigned long long), s), "memset");
     if (r == IGP_OK) {
-        tc_split_kernel<double><<<(unsigned)((nt * kTcN + 255) / 256), 256, 0, s>>>(cen, K, nt * kTcN, d, kTcN, kTcKC, ch,
-                                                                                cl, nullptr, sqn, sq, st);
+        tc_split_kernel<double><<<(unsigned)((nt * kTcN + 255) / 256), 256, 0, s>>>(cen, nullptr, K, nt * kTcN, d, kTcN,
+                                                                                kTcKC, ch, cl, nullptr, sqn, sq, st);
         r = launch_status("tc_split_kernel<double>");
     }
     const size_t smem = tc_smem_bytes(d);
-    auto kern = kTcN == 256 ? birch_tc_kernel<256> : birch_tc_kernel<128>;
+    auto kern = kTcN == 256 ? birch_tc_kernel<256, false> : birch_tc_kernel<128, false>;
+    auto kcol = kTcN == 256 ? birch_tc_kernel<256, true> : birch_tc_kernel<128, true>;
     if (r == IGP_OK)
         r = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "birch tc smem attribute");
+    if (r == IGP_OK)
+        r = cuda_status(cudaFuncSetAttribute(kcol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "birch tc smem attribute");
+    // pass 1: every row; certified rows are labelled, the rest listed with their thresholds
     for (int64_t row0 = 0; row0 < m && r == IGP_OK; row0 += kChunk) {
         const int64_t rows = m - row0 < kChunk ? m - row0 : kChunk;
         const int64_t rt = (rows + kTcM - 1) / kTcM;
         const float* Xc = X + row0 * d;
-        tc_split_kernel<float><<<(unsigned)((rt * kTcM + 255) / 256), 256, 0, s>>>(Xc, rows, rt * kTcM, d, kTcM, d, xh,
-                                                                              xl, xn, nullptr, nullptr, nullptr);
+        tc_split_kernel<float><<<(unsigned)((rt * kTcM + 255) / 256), 256, 0, s>>>(Xc, nullptr, rows, rt * kTcM, d, kTcM,
+                                                                              d, xh, xl, xn, nullptr, nullptr, nullptr);
         r = launch_status("tc_split_kernel<float>");
         if (r == IGP_OK) {
-            TcArgs ar{xh, xl, ch, cl, sq, xn, st, Xc, cen, sqn, rows, row0, (int)nt, d, labels + row0, amb_rows, amb_count};
+            TcArgs ar{xh,  xl,   ch,      cl,      sq, xn,           st,       Xc,        cen, sqn,     rows,
+                      row0, (int)nt, (int)nt, d, labels + row0, amb_rows, amb_count, thr, nullptr, nullptr, nullptr};
             kern<<<(unsigned)rt, kTcThreads, smem, s>>>(ar);
             r = launch_status("birch_tc_kernel");
+        }
+    }
+    unsigned long long h[2] = {0, 0};
+    if (r == IGP_OK) r = cuda_status(cudaMemcpyAsync(h, amb_count, sizeof(h), cudaMemcpyDeviceToHost, s), "readback");
+    if (r == IGP_OK) r = cuda_status(cudaStreamSynchronize(s), "sync");
+    const int64_t n1 = (int64_t)h[0];
+    if (r == IGP_OK && n1 > 0) {
+        // pass 2 (the listed rows, as tiles of their own): every column within the row's threshold;
+        // pass 3: fp64 over those candidates.  Rows without a usable list stay listed (in place:
+        // the list is rebuilt from the front) for the fp64 pass over every cluster.
+        constexpr int64_t kChunk2 = (int64_t)1 << 20;
+        const int64_t c2 = n1 < kChunk2 ? n1 : kChunk2;
+        int32_t* cand = nullptr;
+        r = cuda_status(alloc_async((void**)&cand, sizeof(int32_t) * ((size_t)c2 * (kCandCap + 1) + 2 * (size_t)n1 + 8), s),
+                        "alloc");
+        if (r == IGP_OK) {
+            int32_t* ccnt = cand + (size_t)c2 * kCandCap;
+            int32_t* rows1 = ccnt + c2;        // the pass-1 list (a copy: amb_rows is rebuilt)
+            const size_t o_cnt = ((size_t)c2 * (kCandCap + 1) + (size_t)n1 + 1) & ~(size_t)1;  // 8-byte aligned
+            unsigned long long* cnt2 = reinterpret_cast<unsigned long long*>(cand + o_cnt);
+            r = cuda_status(cudaMemcpyAsync(rows1, amb_rows, sizeof(int32_t) * (size_t)n1, cudaMemcpyDeviceToDevice, s),
+                            "list copy");
+            if (r == IGP_OK) r = cuda_status(cudaMemsetAsync(cnt2, 0, 2 * sizeof(unsigned long long), s), "memset");
+            for (int64_t k0 = 0; k0 < n1 && r == IGP_OK; k0 += kChunk2) {
+                const int64_t rows = n1 - k0 < kChunk2 ? n1 - k0 : kChunk2;
+                const int64_t rt = (rows + kTcM - 1) / kTcM;
+                tc_split_kernel<float><<<(unsigned)((rt * kTcM + 255) / 256), 256, 0, s>>>(
+                    X, rows1 + k0, rows, rt * kTcM, d, kTcM, d, xh, xl, nullptr, nullptr, nullptr, nullptr);
+                r = launch_status("tc_split_kernel<float>");
+                // few rows: the centroid tiles are split over CTA columns to fill the GPU
+                DeviceInfo di;
+                const int sms = device_info(&di) ? di.num_sms : 148;
+                const int64_t ys = std::max<int64_t>(1, std::min<int64_t>(nt, (2 * sms + rt - 1) / rt));
+                const int tps = (int)((nt + ys - 1) / ys);
+                const unsigned gy = (unsigned)((nt + tps - 1) / tps);
+                if (r == IGP_OK) r = cuda_status(cudaMemsetAsync(ccnt, 0, sizeof(int32_t) * (size_t)rows, s), "memset");
+                if (r == IGP_OK) {
+                    TcArgs ar{xh,  xl,      ch,  cl, sq,      nullptr, st,      X,       cen,      sqn,  rows,
+                              k0,  (int)nt, tps, d,  nullptr, nullptr, nullptr, nullptr, thr + k0, cand, ccnt};
+                    kcol<<<dim3((unsigned)rt, gy), kTcThreads, smem, s>>>(ar);
+                    r = launch_status("birch_tc_kernel<collect>");
+                }
+                if (r == IGP_OK) {
+                    tc_recheck_kernel<<<(unsigned)std::min<int64_t>((rows + 127) / 128, 8192), 128, 0, s>>>(
+                        rows1 + k0, rows, cand, ccnt, X, cen, sqn, d, labels, amb_rows, cnt2);
+                    r = launch_status("tc_recheck_kernel");
+                }
+            }
+            // amb_count: [0] = rows still listed, [1] += rows settled by the candidate re-check
+            unsigned long long h2[2] = {0, 0};
+            if (r == IGP_OK) r = cuda_status(cudaMemcpyAsync(h2, cnt2, sizeof(h2), cudaMemcpyDeviceToHost, s), "readback");
+            if (r == IGP_OK) r = cuda_status(cudaStreamSynchronize(s), "sync");
+            if (r == IGP_OK) {
+                const unsigned long long hn[2] = {h2[0], h[1] + h2[1]};
+                r = cuda_status(cudaMemcpyAsync(amb_count, hn, sizeof(hn), cudaMemcpyHostToDevice, s), "count");
+                if (r == IGP_OK) r = cuda_status(cudaStreamSynchronize(s), "sync");  // hn is on this stack frame
+            }
+            free_async(cand, s);
         }
     }
     free_async(ws, s);
