@@ -147,6 +147,24 @@ def test_birch_tensor_predict_ties_fall_back_to_fp64(igp):
     g.close()
 
 
+def test_birch_tensor_predict_lattice_ties(igp):
+    """Rows on an integer lattice against lattice clusters, queried at half-integer offsets: exact
+    ties by the dozen (up to 2^8 equidistant clusters), so the tensor path takes all three routes —
+    in-kernel re-check, the candidate pass, and rows with more than 32 candidates through the
+    all-cluster fp64 pass — and must still return the oracle's first minimum."""
+    rng = np.random.default_rng(9)
+    X = np.unique(rng.integers(0, 3, (3000, 8)), axis=0).astype(np.float64)
+    g, ocen, osqn = fit_clusters(igp, X, 0.1, 50)
+    assert ocen.shape[0] == X.shape[0]
+    Q = f32(np.concatenate([X, X[:400] + 0.5, X[:400] + rng.integers(0, 2, (400, 8)) * 0.5, rng.random((400, 8)) * 2]))
+    Qg = torch.from_numpy(Q).cuda()
+    lab, amb = g.predict(Qg, path="tensor", return_ambiguous=True)
+    assert np.array_equal(lab.cpu().numpy(), oracle.birch_predict(ocen, osqn, Q.astype(np.float64)))
+    assert amb > 400
+    record("birch_tc_lattice_ambiguous", amb)
+    g.close()
+
+
 def test_birch_tensor_predict_huge_values_all_fp64(igp):
     """Magnitudes outside the certified fp32 range (M = inf): every row is solved in fp64."""
     rng = np.random.default_rng(4)
