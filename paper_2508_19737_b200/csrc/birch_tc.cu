@@ -12,22 +12,31 @@
 // The labels must still be the fp64 labels bit for bit.  The tensor-core pass therefore only
 // certifies: a_ij = |c_j|^2 - 2 acc_ij is within a margin M of the fp64 d_ij (M bounds every
 // rounding of the split, the products, the fp32 accumulation and the epilogue; DESIGN.md
-// §"BIRCH predict on the tensor cores" derives it, with a factor-2 safety).  Per row the
-// epilogue keeps the best and second-best a_ij; if second - best > 2M no other cluster can
-// come within M of the best, so the approximate argmin IS the exact argmin.  Otherwise (near
-// ties, exact ties, duplicate centroids; every row when a magnitude leaves the safe fp32 range,
-// M = inf) the row is listed and the fp64 kernel (birch.cu) resolves it in the oracle's order.
+// §5 "Predict" derives it, with a factor-2 safety).  Three passes:
+//   1. every row: 8 (best, index, second) trackers per row; with thr = best + 2M, if every
+//      tracker's second exceeds thr the fp64 minimum is among the trackers' bests within thr --
+//      one: the label; several (near ties): their d_ij in fp64, in the oracle's order, in the
+//      kernel.  Otherwise (M = inf when a magnitude leaves the safe fp32 range) the row is listed
+//      with its thr;
+//   2. the listed rows as their own row tiles (centroid tiles split over CTA columns when few):
+//      every column with a <= thr (a superset of the fp64 minimisers) into a per-row list;
+//   3. tc_recheck_kernel: fp64 over each list.  Rows without a usable list (none or > 32
+//      candidates) are left listed for birch.cu's fp64 kernel over all clusters.
 //
-// Kernel layout (one CTA = 128 rows, warp-specialised, 192 threads):
-//   warp 0      : producer — cp.async.bulk of the row tile (once) and of each 128-centroid tile
-//                 (hi, lo) into a 2-stage shared-memory ring, completion on mbarriers
-//   warp 1      : TMEM allocator + MMA issuer (one lane): 3 x d/8 tcgen05.mma per tile into one
-//                 of two 128-column TMEM accumulators, tcgen05.commit -> ring slot / epilogue
-//   warps 2..5  : epilogue — tcgen05.ld of the accumulator (warp w reads TMEM lanes
-//                 32(w%4)..+31 = its 32 rows), a = fma(-2, acc, |c|^2), running best / second
+// Kernel layout (birch_tc_kernel<N, collect>: one CTA = 128 rows, warp-specialised, 192 threads):
+//   warp 0      : producer -- cp.async.bulk of the row tile (once) and of each N-centroid tile
+//                 (hi, lo) in stages of 32 K columns through a 2-stage shared-memory ring,
+//                 completion on mbarriers
+//   warp 1      : TMEM allocator + MMA issuer (one lane): 3 x d/8 tcgen05.mma (M = 128, N, K = 8)
+//                 per tile into one of two N-column TMEM accumulators, tcgen05.commit -> ring
+//                 stage / epilogue.  N = 256 for d >= 48 (half the row-tile operand re-reads per
+//                 flop), 128 below (where a 256-column epilogue would outlast the MMAs)
+//   warps 2..5  : epilogue -- tcgen05.ld of the accumulator (warp w reads TMEM lanes
+//                 32(w%4)..+31 = its 32 rows), a = fma(-2, acc, |c|^2), the trackers (pass 1) or
+//                 the threshold test (pass 2)
 // Operands are pre-arranged in global memory in the UMMA canonical K-major no-swizzle layout
-// (core matrices of 8 rows x 16 bytes; row groups SBO = 32 d bytes apart, K chunks LBO = 128
-// bytes apart), so every tile is ONE contiguous bulk copy.
+// (core matrices of 8 rows x 16 bytes; row groups SBO = 32 w bytes apart for a block w columns
+// wide, K chunks LBO = 128 bytes apart), so every tile stage is ONE contiguous bulk copy.
 #include <cuda_runtime.h>
 
 #include <algorithm>
