@@ -24,6 +24,7 @@
 // Predict (Alg. 2 l.11) is data-parallel: label_i = argmin_j sqn_j - 2 c_j . x_i over the K
 // leaf centroids (first minimum), one thread per point, cluster tiles staged in shared memory.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1113,8 +1114,18 @@ igp_status igp_birch_predict_ex(igp_birch_t b, const float* d_X, int64_t m, int3
         set_error("birch: unknown predict path");
         return IGP_ERR_INPUT;
     }
+#ifdef IGP_TC_STATS
+    auto now = [] { cudaDeviceSynchronize(); return std::chrono::steady_clock::now(); };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto t0 = now();
+#endif
     int64_t K = 0;
     IGP_TRY(igp_birch_info(b, &K, nullptr, nullptr, nullptr));
+#ifdef IGP_TC_STATS
+    const auto t1 = now();
+#endif
     if (K == 0) {
         set_error("birch: predict on an empty tree");
         return IGP_ERR_INPUT;
@@ -1133,12 +1144,15 @@ igp_status igp_birch_predict_ex(igp_birch_t b, const float* d_X, int64_t m, int3
     double* sqn = nullptr;
     int32_t* amb_rows = nullptr;
     unsigned long long* amb_count = nullptr;
-    IGP_CUDA(alloc_async((void**)&cen, 8 * ((size_t)K * d + (size_t)K), s), "alloc");  // centroids, then sqn
+    IGP_CUDA(alloc_async_class((void**)&cen, 8 * ((size_t)K * d + (size_t)K), s), "alloc");  // centroids, then sqn
     sqn = cen + (size_t)K * d;
     igp_status st = igp_birch_clusters(b, cen, sqn, nullptr, nullptr, nullptr, stream);
+#ifdef IGP_TC_STATS
+    const auto t2 = now();
+#endif
     int64_t n = m;  // rows left for the fp64 kernel
     if (st == IGP_OK && tc) {
-        st = cuda_status(alloc_async((void**)&amb_rows, 4 * (size_t)m, s), "alloc");
+        st = cuda_status(alloc_async_class((void**)&amb_rows, 4 * (size_t)m, s), "alloc");
         if (st == IGP_OK) st = cuda_status(alloc_async((void**)&amb_count, 2 * sizeof(unsigned long long), s), "alloc");
         if (st == IGP_OK) st = launch_birch_tc(cen, sqn, K, d, d_X, m, d_labels, amb_rows, amb_count, s);
         unsigned long long h[2] = {0, 0};  // the grid of the fp64 pass is sized by the uncertified count
@@ -1147,8 +1161,10 @@ igp_status igp_birch_predict_ex(igp_birch_t b, const float* d_X, int64_t m, int3
         n = (int64_t)h[0];
         if (ambiguous) *ambiguous = (int64_t)(h[0] + h[1]);
 #ifdef IGP_TC_STATS  // diagnostics builds: how the tensor-core pass settled the rows
-        fprintf(stderr, "birch tc predict: %lld rows, K %lld: %llu re-checked in the kernel, %llu to the fp64 pass\n",
-                (long long)m, (long long)K, h[1], h[0]);
+        const auto t3 = now();
+        fprintf(stderr, "birch tc predict: %lld rows, K %lld: %llu re-checked in the kernel, %llu to the fp64 pass; "
+                "host ms: info %.2f clusters %.2f tensor passes %.2f\n",
+                (long long)m, (long long)K, h[1], h[0], ms(t0, t1), ms(t1, t2), ms(t2, t3));
 #endif
     }
     if (st == IGP_OK && n > 0) st = launch_predict_fp64(cen, sqn, K, d, d_X, n, tc ? amb_rows : nullptr, d_labels, s);

@@ -533,7 +533,7 @@ igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int 
                  o_xn = o_sq + al(4 * (size_t)nt * kTcN), o_st = o_xn + al(4 * (size_t)mc),
                  o_thr = o_st + al(4 * S_WORDS), total = o_thr + al(4 * (size_t)m);
     char* ws = nullptr;
-    IGP_CUDA(alloc_async((void**)&ws, total, s), "birch tc workspace");
+    IGP_CUDA(alloc_async_class((void**)&ws, total, s), "birch tc workspace");
     float* xh = (float*)ws;
     float* xl = (float*)(ws + o_xl);
     float* ch = (float*)(ws + o_ch);
@@ -584,8 +584,9 @@ igp_status launch_birch_tc(const double* cen, const double* sqn, int64_t K, int 
         constexpr int64_t kChunk2 = (int64_t)1 << 20;
         const int64_t c2 = n1 < kChunk2 ? n1 : kChunk2;
         int32_t* cand = nullptr;
-        r = cuda_status(alloc_async((void**)&cand, sizeof(int32_t) * ((size_t)c2 * (kCandCap + 1) + 2 * (size_t)n1 + 8), s),
-                        "alloc");
+        r = cuda_status(
+            alloc_async_class((void**)&cand, sizeof(int32_t) * ((size_t)c2 * (kCandCap + 1) + 2 * (size_t)n1 + 8), s),
+            "alloc");
         if (r == IGP_OK) {
             int32_t* ccnt = cand + (size_t)c2 * kCandCap;
             int32_t* rows1 = ccnt + c2;        // the pass-1 list (a copy: amb_rows is rebuilt)

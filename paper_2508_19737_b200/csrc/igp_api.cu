@@ -84,6 +84,21 @@ cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s) {
     return cudaMallocFromPoolAsync(p, bytes > 0 ? bytes : 16, pool, s);
 }
 
+// a size class above `bytes` (>= 1 MiB: 2^k x {1, 1.25, 1.5, 1.75}, at most 25% over): workspaces
+// whose size creeps up call by call (BIRCH predict as clusters accrue) then reuse the pool's block
+// instead of growing the pool on every call
+cudaError_t alloc_async_class(void** p, size_t bytes, cudaStream_t s) {
+    if (bytes >= ((size_t)1 << 20)) {
+        size_t k = (size_t)1 << 20;
+        while (k * 2 <= bytes) k *= 2;
+        const size_t q = k / 4;
+        size_t c = k;
+        while (c < bytes) c += q;
+        bytes = c;
+    }
+    return alloc_async(p, bytes, s);
+}
+
 cudaError_t trim_pool() {
     int dev = -1;
     cudaError_t e = cudaGetDevice(&dev);

@@ -48,6 +48,7 @@ cudaStream_t side_stream(int dev);
 // stream-ordered allocation helpers: a memory pool private to the library per device (freed
 // blocks are kept for reuse; igp_trim_memory releases them), never the device's default pool
 cudaError_t alloc_async(void** p, size_t bytes, cudaStream_t s);
+cudaError_t alloc_async_class(void** p, size_t bytes, cudaStream_t s);  // rounded up to a size class
 void free_async(void* p, cudaStream_t s);
 cudaError_t trim_pool();  // synchronises the device, then trims the current device's pool
 
