@@ -906,7 +906,8 @@ igp_status refresh_list(igp_birch_s* b, const long long* h, cudaStream_t s) {
         if (b->list) free_async(b->list, s);
         b->list = nullptr;
         b->list_cap = 0;
-        const int64_t cap = (std::max<int64_t>(ns, 1024) + 1) & ~(int64_t)1;  // even: the count below is 8-B aligned
+        // capacity: 1.5x the entries (fewer reallocations as the tree grows), even (the count below is 8-B aligned)
+        const int64_t cap = (std::max<int64_t>(ns + ns / 2, 1024) + 1) & ~(int64_t)1;
         IGP_CUDA(alloc_async((void**)&b->list, sizeof(int32_t) * (size_t)(cap + 2), s), "alloc");
         b->list_cap = cap;
     }
