@@ -105,6 +105,8 @@ __device__ __forceinline__ double dot2(const double* a, const double* b, int d, 
     return __dadd_rn(half, __shfl_xor_sync(mask, half, 1));  // left + right on both lanes (commutative)
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 struct FitShared {
     double best_d[kFitThreads / 32];
     int best_j[kFitThreads / 32 > 8 ? kFitThreads / 32 : 8];  // per-warp argmax (splits); split results
@@ -112,6 +114,7 @@ struct FitShared {
     int am_j[2][kFitThreads / 32];
     int path_node[kMaxDepth];
     int path_j[kMaxDepth];
+    int ch[2][64];  // global trees: each entry's child, published by the argmin's barrier (alternating)
     int depth;
     int cur;      // broadcast slot
     int flag;
@@ -434,22 +437,46 @@ __device__ __forceinline__ void fit_rows(TreeDev T, const float* __restrict__ X,
         int depth = 0, v = root;
         while (true) {
             const int cnt = T.nsub[v];
+            const int leafv = T.is_leaf[v];
             // one 2-lane group per entry; groups past the node's entries stay idle
             double dist = INFINITY;
             const unsigned act = __ballot_sync(kFullMask, g < cnt);
             if (g < cnt) {
                 const int s = T.sub[(int64_t)v * B1 + g];
+                // a tree in global memory: every entry's next hop is fetched beside its distance
+                // (the child and, into L1, that node's count / leaf flag / entry list; at a leaf,
+                // the entry's LS row and counts for the merge test), so the winner's path costs L1
+                // hits instead of dependent L2 round trips after the argmin
+                const int ch = (!SM && !leafv) ? T.child[s] : -1;
                 const double dt = dot2(T.cen + (int64_t)s * T.ldc, xs, d, r, act);
                 dist = __dadd_rn(T.sqn[s], -2.0 * dt);
+                if (!SM) {
+                    if (!leafv) {
+                        if (r == 0) {
+                            sh.ch[am_slot][g] = ch;
+                            prefetch_l1(T.nsub + ch);
+                            prefetch_l1(T.is_leaf + ch);
+                            prefetch_l1(T.sub + (int64_t)ch * B1);
+                            prefetch_l1(T.sub + (int64_t)ch * B1 + B1 - 1);
+                        }
+                    } else {
+                        for (int k = 16 * r; k < d; k += 32) prefetch_l1(T.ls + (int64_t)s * d + k);
+                        if (r == 0) {
+                            prefetch_l1(T.n + s);
+                            prefetch_l1(T.ss + s);
+                        }
+                    }
+                }
             }
+            const int slot = am_slot;  // the ch slot this level wrote (block_argmin toggles am_slot)
             const int j = block_argmin(dist, g, cnt, sh, am_slot);
             if (threadIdx.x == 0) {
                 sh.path_node[depth] = v;
                 sh.path_j[depth] = j;
             }
             ++depth;
-            if (T.is_leaf[v]) break;
-            v = T.child[T.sub[(int64_t)v * B1 + j]];
+            if (leafv) break;
+            v = SM ? T.child[T.sub[(int64_t)v * B1 + j]] : sh.ch[slot][j];
         }
         __syncthreads();
         FIT_MARK(1);
