@@ -723,10 +723,16 @@ __global__ void merge_count_kernel(const int32_t* __restrict__ brp, const int32_
     }
 }
 
+// PERM: the relabelled CSR is written in the same pass (row order computed from the merged
+// degrees before this kernel): row r's entries also go, mapped through inv, to relabelled row
+// inv[r] at the same positions (a relabelled row keeps the canonical neighbour order), so no
+// separate relabelling pass re-reads the merged CSR
+template <bool PERM>
 __global__ void merge_write_kernel(const int32_t* __restrict__ brp, const int32_t* __restrict__ bci,
                                    const int32_t* __restrict__ noff, const int32_t* __restrict__ ndata,
                                    const int32_t* __restrict__ ncnt, int32_t n, const int32_t* __restrict__ row_ptr,
-                                   int32_t* __restrict__ col_idx) {
+                                   int32_t* __restrict__ col_idx, const int32_t* __restrict__ inv,
+                                   const int32_t* __restrict__ rpp, int32_t* __restrict__ cip) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nwarps) {
@@ -734,13 +740,18 @@ __global__ void merge_write_kernel(const int32_t* __restrict__ brp, const int32_
         const int32_t* U = ndata + noff[r];
         const int32_t nu = ncnt[r];
         int32_t* out = col_idx + row_ptr[r];
+        int32_t* outp = PERM ? cip + rpp[inv[r]] : nullptr;
         for (int32_t i = lane; i < nb; i += 32) {
             const int32_t x = bci[b0 + i];
-            out[i + lower_bound_i32(U, nu, x)] = x;
+            const int32_t pos = i + lower_bound_i32(U, nu, x);
+            out[pos] = x;
+            if (PERM) outp[pos] = inv[x];
         }
         for (int32_t j = lane; j < nu; j += 32) {
             const int32_t u = U[j];
-            out[j + lower_bound_i32(bci + b0, nb, u)] = u;
+            const int32_t pos = j + lower_bound_i32(bci + b0, nb, u);
+            out[pos] = u;
+            if (PERM) outp[pos] = inv[u];
         }
     }
 }
@@ -908,6 +919,8 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
     IGP_STEP(scan_exclusive(cnt, off, n, s));
     IGP_STEP(cuda_status(cudaMemsetAsync(c.row_ptr + n + 1, 0, kRpPad * sizeof(int32_t), s), "pad memset"));
     const int rg = grid_for((int64_t)n * 32, 256, di.num_sms, 8);
+    // a streaming merge in degree order writes the relabelled CSR in the merge pass itself
+    const bool fused = base != nullptr && reorder && !community;
     if (E > 0) {
         IGP_STEP(cuda_status(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)n, s), "memset"));
         scatter_kernel<<<eg, 256, 0, s>>>(d_edges, E, n, off, cnt, tmp);
@@ -923,7 +936,25 @@ igp_status build_csr(const int32_t* d_edges, int64_t E, int32_t n, RowOrder row_
         merge_count_kernel<<<tg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, ucnt);
         IGP_STEP(launch_status("merge_count_kernel"));
         IGP_STEP(scan_exclusive(ucnt, c.row_ptr, n, s));
-        merge_write_kernel<<<rg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, c.row_ptr, c.col_idx);
+        if (fused) {
+            // degree order from the merged row lengths, then one pass writes both CSRs
+            const int ng = grid_for(n, 256, di.num_sms, 8);
+            degree_keys_kernel<<<ng, 256, 0, s>>>(c.row_ptr, n, psc.keys[0], psc.vals[0]);
+            IGP_STEP(launch_status("degree_keys_kernel"));
+            IGP_STEP(stable_sort_pairs(n, 10, psc, c.order, s, di));
+            inverse_perm_kernel<<<ng, 256, 0, s>>>(c.order, n, inv, c.row_ptr, degp);
+            IGP_STEP(launch_status("inverse_perm_kernel"));
+            IGP_STEP(scan_exclusive(degp, c.rp_perm, n, s));
+            IGP_STEP(cuda_status(cudaMemsetAsync(c.rp_perm + n + 1, 0, kRpPad * sizeof(int32_t), s), "pad memset"));
+            merge_write_kernel<true><<<rg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, c.row_ptr,
+                                                        c.col_idx, inv, c.rp_perm, c.col_perm);
+            IGP_STEP(launch_status("merge_write_kernel<perm>"));
+            free_async(ws, s);
+            *out = c;
+            return IGP_OK;
+        }
+        merge_write_kernel<false><<<rg, 256, 0, s>>>(base->row_ptr, base->col_idx, off, tmp, cnt, n, c.row_ptr,
+                                                     c.col_idx, nullptr, nullptr, nullptr);
         IGP_STEP(launch_status("merge_write_kernel"));
     } else {
         // B5: row pointers, compaction
