@@ -172,6 +172,52 @@ __global__ void scan_apply_kernel(const int32_t* __restrict__ in, int32_t n, con
     }
 }
 
+// scan_apply_kernel with the block's offset reduced from the raw block sums by the block itself
+// (nb <= 4 kScanThreads), so the single-block scan of the block sums is not a launch of its own;
+// the last block writes the total to out[n]
+__global__ void scan_apply_prefix_kernel(const int32_t* __restrict__ in, int32_t n, const int32_t* __restrict__ bsum,
+                                         int32_t nb, int32_t* __restrict__ out) {
+    __shared__ int32_t tile[kScanTile];
+    __shared__ int32_t wt[32];
+    __shared__ int32_t tot;
+    __shared__ int32_t pre;
+    int32_t v = 0;
+    for (int32_t i = threadIdx.x; i < (int32_t)blockIdx.x; i += kScanThreads) v += bsum[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = v;
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int64_t i = base + k * kScanThreads + threadIdx.x;
+        tile[k * kScanThreads + threadIdx.x] = i < n ? in[i] : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t t = 0;
+        for (int w = 0; w < kScanThreads / 32; ++w) t += wt[w];
+        pre = t;
+        if ((int32_t)blockIdx.x == nb - 1) out[n] = t + bsum[nb - 1];
+    }
+    __syncthreads();
+    int32_t loc[kScanItems];
+    int32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        loc[k] = s;
+        s += tile[threadIdx.x * kScanItems + k];
+    }
+    int32_t ex = block_exclusive_scan(s, wt, &tot) + pre;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) tile[threadIdx.x * kScanItems + k] = ex + loc[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int64_t i = base + k * kScanThreads + threadIdx.x;
+        if (i < n) out[i] = tile[k * kScanThreads + threadIdx.x];
+    }
+}
+
 // ---------------------------------------------------------------- B4 row sort + dedup
 __device__ __forceinline__ int next_pow2(int x) {
     int p = 1;
@@ -581,6 +627,12 @@ igp_status scan_exclusive(const int32_t* in, int32_t* out, int32_t n, cudaStream
     if (nb > 0) {
         scan_reduce_kernel<<<nb, kScanThreads, 0, s>>>(in, n, bsum);
         IGP_TRY(launch_status("scan_reduce_kernel"));
+    }
+    if (nb > 0 && nb <= 4 * kScanThreads) {  // up to ~2M elements: two launches
+        scan_apply_prefix_kernel<<<nb, kScanThreads, 0, s>>>(in, n, bsum, nb, out);
+        IGP_TRY(launch_status("scan_apply_prefix_kernel"));
+        free_async(bsum, s);
+        return IGP_OK;
     }
     scan_blocksums_kernel<<<1, 1024, 0, s>>>(bsum, nb, out + n);
     IGP_TRY(launch_status("scan_blocksums_kernel"));
