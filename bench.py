@@ -75,6 +75,17 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def tf32_peak():
+    """TF32 dense tensor peak for the tensor-core BIRCH predict: the measured bf16 peak x the guide's
+    nominal TF32/bf16 ratio (1.1 / 2.25 PFLOP/s), and the nominal 1.1 PFLOP/s beside it."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["bf16_tflops"]) * 1.1 / 2.25, "measured bf16 x 1.1/2.25 (MEASURED_PEAKS.json)"
+    except Exception:
+        return 1100.0, "nominal (B200_PROFILING.md)"
+
+
 def step_bytes(n, nnz, d):
     """compulsory bytes of one filter step (fp32, int32)."""
     return 4 * (n + 1) + 4 * nnz + 4 * n + 8 * n * d
@@ -426,7 +437,18 @@ def streaming_alg2_leg(args, igp, batches, N, d, L, tau, seed, stream, dev):
         rec.append({"stage": t, "new_nodes": int(new.numel()), "partial_fit_ms": fit_ms, **times, "clusters": K})
     g.close()
     bt.close()
+    # the final stage's predict against the TF32 tensor peak: 3 TF32 products per (row, cluster,
+    # column) over the padded tiles (whole call: split, both tensor passes, re-checks)
+    last = rec[-1]
+    tile_n = 256 if d >= 48 else 128
+    flops = 6.0 * (-(-n_kept // 128) * 128) * (-(-last["clusters"] // tile_n) * tile_n) * d
+    peak, src = tf32_peak()
+    ach = flops / (last["predict_ms"] * 1e-3) / 1e12
+    roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "peak_source": src, "nominal_peak": 1100.0, "frac_of_nominal": ach / 1100.0,
+            "what": "igp_birch_predict (tensor-core path) on the final stage, whole call, 6 m Kpad d flops"}
     return {"stages": rec, "threshold": args.birch_threshold, "branching": args.birch_branching,
+            "predict_roofline": roof,
             "new_nodes": "nodes whose first edge arrives at stage t (edge-arrival stream)"}
 
 
