@@ -191,7 +191,7 @@ struct TcArgs {
     const float* xl;
     const float* ch;  // centroid tiles, canonical layout
     const float* cl;
-    const float* sq;  // [n_tiles * 128] |c_j|^2 (fp32), +inf padding
+    const float* sq;  // [n_tiles * N] |c_j|^2 (fp32), +inf padding
     const float* xnorm;  // [m] upper bounds of |x_i|
     const unsigned* stats;
     const float* X;      // the rows [m][d] and the clusters (fp64), for the exact re-check
@@ -207,7 +207,7 @@ struct TcArgs {
     unsigned long long* amb_count;  // [0] rows left to the fp64 pass, [1] rows re-checked here in fp64
     float* amb_thr;                 // pass 1: each listed row's threshold best + 2M (beside amb_rows)
     // pass 2 (collect mode): the rows are the listed ones; each row's pass-1 threshold in, every
-    // column with a <= threshold out (at most kCandCap; ccnt = -1 past that)
+    // column with a <= threshold out (ccnt counts the appends; past kCandCap only the count grows)
     const float* row_thr;
     int32_t* cand;
     int32_t* ccnt;
