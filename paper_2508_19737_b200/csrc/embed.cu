@@ -50,6 +50,10 @@ constexpr int kFoldChunks = 8;   // fp32 partial sums span at most 128 neighbour
 constexpr int kBatch = 8;       // gathers issued back to back per lane (full chunks)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kDefaultOcc = 2;
+// index chunks start at each row's first entry (scalar index loads) instead of the 16-byte aligned
+// entry below it: fewer masked gather slots per row batch (round-trip fill 0.87 -> 0.92 on the
+// headline graph); measured headline -1.5%, Large -5% per filter step (profiles/r02/idx_any.txt)
+constexpr int kIdxAnyStart = 1;
 constexpr float kIdxEvictFirst = 1.0f;  // the index stream is read once per launch
 constexpr float kStoreEvictFirst = 1.0f;  // measured +2% (profiles/r01)
 
@@ -142,6 +146,7 @@ struct LayerArgs {
     double grid_c;  // 1.5 * 2^(52-g): (x + grid_c) - grid_c rounds x to the 2^-g grid
     float idx_ef;   // fraction of index-stream loads marked L2 evict_first
     float st_ef;    // fraction of output stores marked L2 evict_first
+    int idx_any;    // 1: index chunks start at the row's first entry (scalar index loads), 0: 16-byte aligned
 };
 
 // (mu, 1/sigma) of column c from exact sums; std with ddof (0 = population, reading A2; the
@@ -212,15 +217,20 @@ __device__ __forceinline__ int2 ld_idx2h(const int32_t* p, uint64_t pol) {
                  : "l"(p), "l"(pol));
     return v;
 }
-// indices [e0 + q*IPL, e0 + (q+1)*IPL) of an aligned chunk (e0 % 4 == 0); the col arrays are
+// indices [e0 + q*IPL, e0 + (q+1)*IPL) of a chunk (vector loads when e0 % 4 == 0 and !any); the col arrays are
 // padded, so a chunk may run past the row (those slots are masked by the caller)
 template <int IPL>
 __device__ __forceinline__ void load_idx(const int32_t* ci, int32_t e0, int32_t end, int q, uint64_t pol,
-                                         int (&jr)[IPL]) {
+                                         int (&jr)[IPL], int any) {
     const int32_t e = e0 + q * IPL;
     if (e >= end) {
 #pragma unroll
         for (int k = 0; k < IPL; ++k) jr[k] = 0;
+        return;
+    }
+    if (any) {
+#pragma unroll
+        for (int k = 0; k < IPL; ++k) jr[k] = ld_idx1(ci + e + k, pol);
         return;
     }
     if constexpr (IPL >= 4) {
@@ -275,6 +285,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
     float* tile = stage[warp];
     const uint64_t pol_idx = evict_first_policy(p.idx_ef);
     const uint64_t pol_st = evict_first_policy(p.st_ef);
+    const int32_t amask = p.idx_any ? ~0 : ~3;
     const int oc0 = W >= 32 ? lane * OC : lane / 2;  // owned statistics columns / rows
     const int or0 = W >= 32 ? 0 : (lane & 1) * OR;
     double s1[OC], s2[OC];
@@ -292,7 +303,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
         nbeg = __ldg(p.rp + base + g);
         nend = __ldg(p.rp + base + g + 1);
     }
-    load_idx<IPL>(p.ci, nbeg & ~3, nend, q, pol_idx, jfirst);
+    load_idx<IPL>(p.ci, nbeg & amask, nend, q, pol_idx, jfirst, p.idx_any);
     // the previous step's output (yin) and column sums (sums_in) are read only after this point
     asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int c = threadIdx.x; c < W; c += kThreads) {
@@ -328,17 +339,17 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
         bool folded = false;
         double* af = acc_f[grp] + 8 * q;
         // chunks start 16-byte aligned (vector index loads); slots outside [beg, end) are masked
-        const int32_t start = beg & ~3;
+        const int32_t start = beg & amask;
         const int nch = end > beg ? (end - start + kChunk - 1) / kChunk : 0;
         const int max_nch = __reduce_max_sync(kFull, nch);
         int jr[IPL];
 #pragma unroll
         for (int k = 0; k < IPL; ++k) jr[k] = jfirst[k];
-        if (max_nch == 0) load_idx<IPL>(p.ci, nbeg & ~3, nend, q, pol_idx, jfirst);
+        if (max_nch == 0) load_idx<IPL>(p.ci, nbeg & amask, nend, q, pol_idx, jfirst, p.idx_any);
         for (int c = 0; c < max_nch; ++c) {
             const int32_t e0 = start + c * kChunk, e1 = e0 + kChunk;
             int jn[IPL];
-            load_idx<IPL>(p.ci, e1, end, q, pol_idx, jn);  // prefetch the next chunk's indices
+            load_idx<IPL>(p.ci, e1, end, q, pol_idx, jn, p.idx_any);  // prefetch the next chunk's indices
             const int lo = beg > e0 ? beg - e0 : 0;        // valid slots of this chunk: [lo, hi)
             int hi = end - e0;
             hi = hi < 0 ? 0 : (hi > kChunk ? kChunk : hi);
@@ -380,7 +391,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
                 }
             }
             if (c == 0) {
-                load_idx<IPL>(p.ci, nbeg & ~3, nend, q, pol_idx, jfirst);  // next batch's first chunk
+                load_idx<IPL>(p.ci, nbeg & amask, nend, q, pol_idx, jfirst, p.idx_any);  // next batch's first chunk
                 // the next batch's whole index range (its G rows are consecutive) into L2 with one
                 // bulk prefetch (measured +0.5%)
                 const int32_t lo_e = __shfl_sync(kFull, nbeg, 0);
@@ -662,6 +673,8 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     float idx_ef = kIdxEvictFirst, st_ef = kStoreEvictFirst;  // L2 policies (development knobs)
     if (const char* e = getenv("IGP_IDX_EF")) idx_ef = (float)atof(e);
     if (const char* e = getenv("IGP_ST_EF")) st_ef = (float)atof(e);
+    int idx_any = kIdxAnyStart;  // development knob IGP_IDX_ANY=0: 16-byte aligned index chunks
+    if (const char* e = getenv("IGP_IDX_ANY")) idx_any = atoi(e) != 0;
 
     igp_status rc = IGP_OK;
     const bool timed = (o.flags & IGP_FLAG_TIME_LAYERS) != 0;
@@ -728,6 +741,7 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 a.grid_c = grid_c;
                 a.idx_ef = idx_ef;
                 a.st_ef = st_ef;
+                a.idx_any = idx_any;
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(grid);
                 cfg.blockDim = dim3(small ? 64 : 256);
