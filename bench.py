@@ -156,6 +156,17 @@ TRAFFIC_JSON = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 KERNEL_SRC = os.path.join(ROOT, "paper_2508_19737_b200", "csrc", "embed.cu")
 
 
+def layer_kernel_name(n, width):
+    """The filter-step kernel embed.cu launches for this slice (run_embed_w's rule): the
+    warp-specialised layer_ws_kernel where a W >= 64 slice exceeds 4x the L2, else layer_kernel."""
+    import torch
+
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size if torch.cuda.is_available() else 0
+    env = os.environ.get("IGP_LAYER_WS")
+    ws = env != "0" if env is not None else (width >= 64 and n * width * 4 > 4 * l2)
+    return "layer_ws_kernel" if ws and width >= 32 else "layer_kernel"
+
+
 def kernel_source_sha():
     """sha256 of the filter-step kernel's source (the ncu traffic numbers are tied to it)."""
     with open(KERNEL_SRC, "rb") as f:
@@ -608,7 +619,7 @@ def run_gpu(args, cfg):
     # time (identical to B_step / step time); traffic is the ncu DRAM bytes of one launch
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": traffic_src, "kernel_source_sha": kernel_source_sha()[:16],
-            "kernel": f"layer_kernel<{width}> ({slices} column-slice launches per filter step)",
+            "kernel": f"{layer_kernel_name(N, width)}<{width}> ({slices} column-slice launches per filter step)",
             "per": "launch", "algorithmic_bytes": b_step / slices, "algorithmic_bytes_per_step": b_step,
             "traffic_per_step": None if traffic is None else traffic * slices,
             "step_us": step_s * 1e6, "avg_launch_us": avg_launch_s * 1e6, "peak_source": peak_src,

@@ -516,6 +516,308 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// E3' layer_ws_kernel<W>: the same filter step with the row epilogue moved off the gather warps
+// (warp specialisation).  A block has kWsGather gather warps and kWsEpi
+// epilogue warps:
+//  - a gather warp runs layer_kernel's gather pipeline (G rows side by side, W/8 lanes per row,
+//    8 x 256-bit gathers in flight per lane) and, instead of finishing its rows, hands each row
+//    batch's fp64 neighbour sums to an epilogue warp through a one-batch shared-memory slot
+//    (mbarriers full / empty), then starts the next batch at once: no drain of its gathers for
+//    the own-row load, tanh, the store and the statistics;
+//  - an epilogue warp owns W/32 whole columns per lane and finishes the batches of kWsGather /
+//    kWsEpi gather warps: own row (coalesced), Eq. (3) with the deferred ZNorm, tanh, store, and
+//    the exact column sums straight in registers (no staging: the lane already owns its columns).
+// Same arithmetic as layer_kernel in the same order, so the output is bit-identical.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ws_bar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void ws_bar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void ws_bar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WS_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra WS_DONE;\n\t"
+        "bra WS_WAIT;\n\t"
+        "WS_DONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+constexpr int kWsGather = 16;  // gather warps per block (4 warpgroups)
+constexpr int kWsEpi = 4;      // epilogue warps per block (1 warpgroup)
+constexpr int kWsThreads = (kWsGather + kWsEpi) * 32;
+
+template <int W>
+constexpr size_t layer_ws_smem() {
+    // acc_f [NG][W] + slots [kWsGather][G][W] doubles, NG = kWsGather * G, G = 256 / W
+    return sizeof(double) * 2 * (size_t)kWsGather * (256 / W) * W;
+}
+
+// One block of 16 + 4 warps per SM.  The 20 warps leave 96 registers per thread (5 per SM
+// sub-partition), which holds only ~5 gathers in flight per lane; setmaxnreg rebalances them:
+// the gather warpgroups take 104 registers (the full 8-deep batches, checked in the SASS), the
+// epilogue warpgroup 64 (16 x 104 + 4 x 64 = 20 x 96).
+template <int W>
+__global__ void __launch_bounds__(kWsThreads, 1) layer_ws_kernel(const LayerArgs p) {
+    constexpr bool REG = true;
+    static_assert(W >= 32, "epilogue lanes own whole columns");
+    constexpr int LPR = W / 8;
+    constexpr int G = 32 / LPR;
+    constexpr int IPL = kChunk / LPR;
+    constexpr int NG = kWsGather * G;
+    constexpr int C = W / 32;  // columns per epilogue lane
+    __shared__ double2 st[W];  // (mu, 1/sigma) of the previous step
+    __shared__ uint64_t full_bar[kWsGather], empty_bar[kWsGather];
+    __shared__ double red[kWsEpi][2 * W];
+    extern __shared__ double dyn_smem[];
+    double (*acc_f)[W] = reinterpret_cast<double (*)[W]>(dyn_smem);                   // [NG][W]
+    double (*slot)[G][W] = reinterpret_cast<double (*)[G][W]>(dyn_smem + NG * W);     // [kWsGather][G][W]
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (int t = threadIdx.x; t < NG * W; t += kWsThreads) (&acc_f[0][0])[t] = 0.0;
+    if (threadIdx.x < kWsGather) {
+        ws_bar_init(&full_bar[threadIdx.x], 32);
+        ws_bar_init(&empty_bar[threadIdx.x], 32);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t step = (int64_t)gridDim.x * NG;
+
+    if (warp < kWsGather) {
+        if constexpr (REG) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;" ::: "memory");
+        const int q = lane % LPR, g = lane / LPR;
+        const int grp = warp * G + g;
+        const uint64_t* yin = reinterpret_cast<const uint64_t*>(p.yin);
+        const uint64_t pol_idx = evict_first_policy(p.idx_ef);
+        const int32_t amask = p.idx_any ? ~0 : ~3;
+        int64_t base = (int64_t)blockIdx.x * NG + warp * G;
+        int32_t nbeg = 0, nend = 0;
+        int jfirst[IPL];
+        if (base + g < p.n) {
+            nbeg = __ldg(p.rp + base + g);
+            nend = __ldg(p.rp + base + g + 1);
+        }
+        load_idx<IPL>(p.ci, nbeg & amask, nend, q, pol_idx, jfirst, p.idx_any);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        __syncthreads();  // barriers initialised, acc_f zeroed, st written
+        uint32_t phase = 0;
+        double* af = acc_f[grp] + 8 * q;
+        for (; base < p.n; base += step, phase ^= 1u) {
+            const int32_t row = (int32_t)(base + g);
+            const int32_t beg = nbeg, end = nend;
+            nbeg = nend = 0;
+            if (base + step + g < p.n) {
+                nbeg = __ldg(p.rp + base + step + g);
+                nend = __ldg(p.rp + base + step + g + 1);
+            }
+            uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+            int nc = 0;
+            bool folded = false;
+            const int32_t start = beg & amask;
+            const int nch = end > beg ? (end - start + kChunk - 1) / kChunk : 0;
+            const int max_nch = __reduce_max_sync(kFull, nch);
+            int jr[IPL];
+#pragma unroll
+            for (int k = 0; k < IPL; ++k) jr[k] = jfirst[k];
+            if (max_nch == 0) load_idx<IPL>(p.ci, nbeg & amask, nend, q, pol_idx, jfirst, p.idx_any);
+            for (int c = 0; c < max_nch; ++c) {
+                const int32_t e0 = start + c * kChunk, e1 = e0 + kChunk;
+                int jn[IPL];
+                load_idx<IPL>(p.ci, e1, end, q, pol_idx, jn, p.idx_any);
+                const int lo = beg > e0 ? beg - e0 : 0;
+                int hi = end - e0;
+                hi = hi < 0 ? 0 : (hi > kChunk ? kChunk : hi);
+                if (__all_sync(kFull, lo == 0 && hi == kChunk)) {
+#pragma unroll
+                    for (int u0 = 0; u0 < kChunk; u0 += kBatch) {
+                        uint64_t v[kBatch][4];
+#pragma unroll
+                        for (int t = 0; t < kBatch; ++t) {
+                            const int u = u0 + t;
+                            const int j = __shfl_sync(kFull, jr[u % IPL], u / IPL, LPR);
+                            IGP_DASSERT(j >= 0 && j < p.n);
+                            ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
+                        }
+#pragma unroll
+                        for (int t = 0; t < kBatch; ++t)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[t][k]);
+                    }
+                } else {
+#pragma unroll
+                    for (int u0 = 0; u0 < kChunk; u0 += kBatch) {
+                        uint64_t v[kBatch][4];
+#pragma unroll
+                        for (int t = 0; t < kBatch; ++t) {
+                            const int u = u0 + t;
+                            const int j = __shfl_sync(kFull, jr[u % IPL], u / IPL, LPR);
+                            v[t][0] = v[t][1] = v[t][2] = v[t][3] = 0ull;
+                            if (u >= lo && u < hi) {
+                                IGP_DASSERT(j >= 0 && j < p.n);
+                                ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
+                            }
+                        }
+#pragma unroll
+                        for (int t = 0; t < kBatch; ++t)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) acc[k] = fadd2(acc[k], v[t][k]);
+                    }
+                }
+                if (c == 0) {
+                    load_idx<IPL>(p.ci, nbeg & amask, nend, q, pol_idx, jfirst, p.idx_any);
+                    const int32_t lo_e = __shfl_sync(kFull, nbeg, 0);
+                    const int32_t hi_e = __shfl_sync(kFull, nend, 31);
+                    if (lane == 0 && hi_e > lo_e) {
+                        const uint64_t a0 = reinterpret_cast<uint64_t>(p.ci + lo_e) & ~(uint64_t)15;
+                        const uint64_t a1 = (reinterpret_cast<uint64_t>(p.ci + hi_e) + 15) & ~(uint64_t)15;
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
+                                     : "memory");
+                    }
+                }
+                if (++nc == kFoldChunks && e1 < end) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float2 f = unpack2(acc[k]);
+                        af[2 * k] += (double)f.x;
+                        af[2 * k + 1] += (double)f.y;
+                        acc[k] = 0ull;
+                    }
+                    nc = 0;
+                    folded = true;
+                }
+#pragma unroll
+                for (int k = 0; k < IPL; ++k) jr[k] = jn[k];
+            }
+            if (row < p.n) prefetch_l2(yin + ((size_t)row * LPR + q) * 4);  // the epilogue's own row
+            // hand the batch over: wait until the epilogue has consumed the previous one
+            ws_bar_wait(&empty_bar[warp], phase ^ 1u);
+            double* sl = &slot[warp][g][8 * q];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 f = unpack2(acc[k]);
+                double a0 = (double)f.x, a1 = (double)f.y;
+                if (folded) {
+                    a0 += af[2 * k];
+                    a1 += af[2 * k + 1];
+                    af[2 * k] = 0.0;
+                    af[2 * k + 1] = 0.0;
+                }
+                sl[2 * k] = a0;
+                sl[2 * k + 1] = a1;
+            }
+            ws_bar_arrive(&full_bar[warp]);
+        }
+        return;
+    }
+
+    // ---- epilogue warps
+    if constexpr (REG) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;" ::: "memory");
+    const int ew = warp - kWsGather;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int c = threadIdx.x - kWsGather * 32; c < W; c += kWsEpi * 32) {
+        double m = 0.0, is = 1.0;
+        if (p.sums_in) column_stats(p.sums_in, c, W, p.n, p.ddof, m, is);
+        st[c] = make_double2(m, is);
+    }
+    __syncthreads();
+    const uint64_t pol_st = evict_first_policy(p.st_ef);
+    double s1[C], s2[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) s1[k] = s2[k] = 0.0;
+    double2 mc[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) mc[k] = st[lane * C + k];
+    const float* yinf = reinterpret_cast<const float*>(p.yin);
+    float* youtf = reinterpret_cast<float*>(p.yout);
+    uint32_t phase = 0;
+    for (int64_t b0 = (int64_t)blockIdx.x * NG; b0 < p.n; b0 += step, phase ^= 1u) {
+        for (int w = ew; w < kWsGather; w += kWsEpi) {
+            const int64_t base = b0 + w * G;
+            if (base >= p.n) break;
+            ws_bar_wait(&full_bar[w], phase);
+            // all G rows' own values and node parameters first (their latencies overlap), then the math
+            float y[G][C];
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const int64_t r = base + i < p.n ? base + i : p.n - 1;
+                if constexpr (C == 1) {
+                    y[i][0] = __ldg(yinf + r * W + lane);
+                } else if constexpr (C == 2) {
+                    const float2 v = __ldg(reinterpret_cast<const float2*>(yinf + r * W) + lane);
+                    y[i][0] = v.x, y[i][1] = v.y;
+                } else {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(yinf + r * W) + lane);
+                    y[i][0] = v.x, y[i][1] = v.y, y[i][2] = v.z, y[i][3] = v.w;
+                }
+            }
+            // lane i < G holds row i's {s, r} and {c_hi, c_lo}; broadcast by shuffles below
+            float2 my_sr = make_float2(0.f, 0.f), my_cc = make_float2(0.f, 0.f);
+            if (lane < G && base + lane < p.n) {
+                my_sr = __ldg(p.sr + base + lane);
+                if (p.sums_in) my_cc = __ldg(p.cc + base + lane);
+            }
+            float tt[G][C], ys[G];
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const float2 sr2 = make_float2(__shfl_sync(kFull, my_sr.x, i), __shfl_sync(kFull, my_sr.y, i));
+                const float2 cc2 = make_float2(__shfl_sync(kFull, my_cc.x, i), __shfl_sync(kFull, my_cc.y, i));
+                const double si = (double)sr2.x, cc = (double)cc2.x + (double)cc2.y;
+#pragma unroll
+                for (int k = 0; k < C; ++k) {
+                    const double ad = slot[w][i][lane * C + k];
+                    const float tself = y[i][k] * sr2.y;
+                    const double P = ((double)p.theta * (double)tself + (double)p.alpha * si * ad - mc[k].x * cc) *
+                                     mc[k].y;
+                    tt[i][k] = p.linear ? (float)P : tanhf((float)P);
+                }
+                ys[i] = sr2.x;
+            }
+            ws_bar_arrive(&empty_bar[w]);  // this lane has read the slot: the gather warp may refill it
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const int64_t r = base + i;
+                if (r < p.n) {
+                    float yo[C];
+#pragma unroll
+                    for (int k = 0; k < C; ++k) {
+                        yo[k] = ys[i] * tt[i][k];
+                        const double xd = (double)tt[i][k];
+                        s1[k] += grid_round(xd, p.grid_c);
+                        s2[k] += grid_round(xd * xd, p.grid_c);
+                    }
+                    float* dst = youtf + r * W + lane * C;
+                    if constexpr (C == 1) {
+                        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(dst), "f"(yo[0]), "l"(pol_st));
+                    } else if constexpr (C == 2) {
+                        asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;" ::"l"(dst), "f"(yo[0]),
+                                     "f"(yo[1]), "l"(pol_st));
+                    } else {
+                        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(dst),
+                                     "f"(yo[0]), "f"(yo[1]), "f"(yo[2]), "f"(yo[3]), "l"(pol_st));
+                    }
+                }
+            }
+        }
+    }
+    if (p.linear) return;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        red[ew][lane * C + k] = s1[k];
+        red[ew][W + lane * C + k] = s2[k];
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kWsEpi * 32) : "memory");
+    for (int t = threadIdx.x - kWsGather * 32; t < 2 * W; t += kWsEpi * 32) {
+        double v = 0.0;
+#pragma unroll
+        for (int e = 0; e < kWsEpi; ++e) v += red[e][t];
+        atomicAdd(p.sums_out + t, v);
+    }
+}
+
 // Z~ = sigmoid((t - mu)/sigma) of a slice into columns [col0, col0 + W) of out [N][d]
 // (relabelled row i is written to the row of its original id order[i])
 template <int W>
@@ -649,6 +951,28 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     // graphs too small to give every SM a block of 8 warps run 2-warp blocks (4x the blocks)
     const bool small = (n + 8 * (256 / W) - 1) / (8 * (256 / W)) < di.num_sms;
     const int grid = small ? layer_grid<W, MB, 2>(n, di) : layer_grid<W, MB, 8>(n, di);
+    // warp-specialised filter step (layer_ws_kernel) where the gathers are DRAM-bound: a W >= 64
+    // slice beyond 4x the L2 (Large: 1.28 GB; measured -5% per step there, +18% at the L2-sized
+    // headline slice, where its 4 epilogue warps per SM cannot keep up -- DESIGN.md §5).
+    // Development knob IGP_LAYER_WS=0/1 forces it off / on (W >= 32).
+    bool use_ws = false;
+    int ws_grid = 0;
+    if constexpr (W >= 32) {
+        const char* e = getenv("IGP_LAYER_WS");
+        use_ws = !small && (e ? atoi(e) != 0 : (W >= 64 && (double)n * W * 4.0 > 4.0 * (double)di.l2_bytes));
+        if (use_ws) {
+            cudaFuncSetAttribute(layer_ws_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)layer_ws_smem<W>());
+            int o = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, layer_ws_kernel<W>, kWsThreads, layer_ws_smem<W>()) !=
+                    cudaSuccess ||
+                o < 1)
+                o = 1;
+            const int64_t rows_per_block = (int64_t)kWsGather * (256 / W);
+            const int64_t want = (n + rows_per_block - 1) / rows_per_block;
+            const int64_t cap = (int64_t)di.num_sms * o;
+            ws_grid = (int)(want < cap ? want : cap);
+        }
+    }
     const size_t nw = (size_t)n * W;
     // workspace: sr | cc (N + 2 float2 each) | y0 | y1 (N x W each) | sums [slices][L+1][2W]
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -752,8 +1076,21 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 attr[0].val.programmaticStreamSerializationAllowed = 1;
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
-                const cudaError_t le = small ? cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 2>, a)
-                                             : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 8>, a);
+                cudaError_t le;
+                if constexpr (W >= 32) {
+                    if (use_ws) {
+                        cfg.gridDim = dim3(ws_grid);
+                        cfg.blockDim = dim3(kWsThreads);
+                        cfg.dynamicSmemBytes = layer_ws_smem<W>();
+                        le = cudaLaunchKernelEx(&cfg, layer_ws_kernel<W>, a);
+                    } else {
+                        le = small ? cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 2>, a)
+                                   : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 8>, a);
+                    }
+                } else {
+                    le = small ? cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 2>, a)
+                               : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 8>, a);
+                }
                 if ((rc = cuda_status(le, "layer_kernel launch")) != IGP_OK) break;
                 if ((rc = launch_status("layer_kernel")) != IGP_OK) break;
             }

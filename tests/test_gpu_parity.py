@@ -157,6 +157,31 @@ def test_embed_dims_and_ragged_sizes(igp, d, n):
         assert err <= TOL, (mode, d, n)
 
 
+@pytest.mark.parametrize("w", [32, 64, 128])
+@pytest.mark.parametrize("mode", ["full", "linear"])
+def test_layer_ws_kernel_bit_identical(igp, w, mode, monkeypatch):
+    """The warp-specialised filter step (layer_ws_kernel: gather warps hand row sums to epilogue
+    warps; the default for DRAM-bound slices) computes the same arithmetic in the
+    same order as layer_kernel: bit-identical outputs at every slice width, a ragged N (partial
+    last row batch), and within the tolerance of the oracle."""
+    n, d, L = 40961, 128, 8
+    rng = np.random.default_rng(w)
+    edges = rng.integers(0, n, (20 * n, 2)).astype(np.int32)
+    g = gpu_graph(igp, edges, n)
+    monkeypatch.setenv("IGP_SLICE_WIDTH", str(w))
+    outs = []
+    for ws in ("0", "1"):
+        monkeypatch.setenv("IGP_LAYER_WS", ws)
+        outs.append(igp.embed(g, -1.0, d, L, 5, mode=mode))
+    assert torch.equal(outs[0], outs[1])
+    rp, ci, _ = oracle.build_csr(edges, n)
+    omode = oracle.MODE_FULL if mode == "full" else oracle.MODE_LINEAR
+    ref = oracle.embed(rp, ci, n, d, L, -1.0, seed=5, mode=omode, nthreads=NTHREADS)
+    err = row_rel_err(outs[1].cpu().numpy(), ref)
+    record(f"layer_ws_w{w}_{mode}", err)
+    assert err <= TOL
+
+
 @pytest.mark.parametrize("d", [1008, 1024])
 def test_embed_maximum_d(igp, d):
     """The largest d (include/igp.h: a multiple of 16 up to 1024): 1024 = 8 slices of 128 columns,
