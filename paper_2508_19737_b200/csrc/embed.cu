@@ -181,12 +181,20 @@ __device__ __forceinline__ uint64_t evict_first_policy(float frac) {
 __device__ __forceinline__ void ldg256(const void* ptr, uint64_t (&v)[4]) {
     asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(ptr));
 }
+// a neighbour-row gather of layer_kernel: no L1 allocation (the rows are rarely re-read from L1
+// within an SM; the row's own values, prefetched into L1, are not displaced by them)
+__device__ __forceinline__ void ldg256_na(const void* ptr, uint64_t (&v)[4]) {
+    asm("ld.global.nc.L1::no_allocate.v4.b64 {%0,%1,%2,%3}, [%4];"
+        : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
+        : "l"(ptr));
+}
 __device__ __forceinline__ void stg256(void* ptr, const uint64_t (&v)[4], uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.v4.b64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(ptr), "l"(v[0]), "l"(v[1]),
                  "l"(v[2]), "l"(v[3]), "l"(pol)
                  : "memory");
 }
 __device__ __forceinline__ void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); }
+__device__ __forceinline__ void prefetch_l1(const void* ptr) { asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr)); }
 __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
     uint64_t r;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -321,9 +329,15 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
         float t8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         const int32_t beg = nbeg, end = nend;
         const uint64_t* own_ptr = yin + ((size_t)row * LPR + q) * 4;
+        // the row's own values are needed only after its gathers: prefetched into L1 now (the
+        // gathers bypass L1 allocation, so the line stays); its node parameters are loaded now,
+        // their latency hidden behind the gathers (interleaved A/B on one box: -1.5% per launch,
+        // DESIGN.md §5)
+        float2 sr2 = make_float2(0.f, 0.f), cc2 = make_float2(0.f, 0.f);
         if (valid) {
-            prefetch_l2(own_ptr);  // the row's own values are needed only after its gathers
-            prefetch_l2(p.sr + row);
+            prefetch_l1(own_ptr);
+            sr2 = __ldg(p.sr + row);
+            if (p.sums_in) cc2 = __ldg(p.cc + row);
         }
         nbeg = nend = 0;
         if (base + step + g < p.n) {
@@ -363,7 +377,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
                         const int u = u0 + t;
                         const int j = __shfl_sync(kFull, jr[u % IPL], u / IPL, LPR);
                         IGP_DASSERT(j >= 0 && j < p.n);
-                        ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
+                        ldg256_na(yin + ((size_t)j * LPR + q) * 4, v[t]);
                     }
 #pragma unroll
                     for (int t = 0; t < kBatch; ++t)
@@ -381,7 +395,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
                         v[t][0] = v[t][1] = v[t][2] = v[t][3] = 0ull;
                         if (u >= lo && u < hi) {
                             IGP_DASSERT(j >= 0 && j < p.n);
-                            ldg256(yin + ((size_t)j * LPR + q) * 4, v[t]);
+                            ldg256_na(yin + ((size_t)j * LPR + q) * 4, v[t]);
                         }
                     }
 #pragma unroll
@@ -432,8 +446,6 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
                     af[k] = 0.0;
                 }
             }
-            const float2 sr2 = __ldg(p.sr + row);
-            const float2 cc2 = p.sums_in ? __ldg(p.cc + row) : make_float2(0.f, 0.f);
             const float4 nd = make_float4(sr2.x, sr2.y, cc2.x, cc2.y);
             uint64_t own[4];
             ldg256(own_ptr, own);
