@@ -167,7 +167,7 @@ __device__ __forceinline__ double grid_round(double x, double c) { return __dsub
 
 __device__ __forceinline__ int ld_idx1(const int32_t* p, uint64_t pol) {
     int v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
 // L2 policy: a fraction `frac` of the accesses are marked evict_first, the rest unchanged
@@ -213,18 +213,20 @@ __device__ __forceinline__ uint64_t pack2(float a, float b) {
 
 __device__ __forceinline__ int4 ld_idx4h(const int32_t* p, uint64_t pol) {
     int4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+    asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ int2 ld_idx2h(const int32_t* p, uint64_t pol) {
     int2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+    asm volatile("ld.global.nc.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
                  : "=r"(v.x), "=r"(v.y)
                  : "l"(p), "l"(pol));
     return v;
 }
+// (index loads allocate in L1: a row batch's index lines are re-read by its next chunks --
+// interleaved A/B -2.8% per headline launch)
 // indices [e0 + q*IPL, e0 + (q+1)*IPL) of a chunk (vector loads when e0 % 4 == 0 and !any); the col arrays are
 // padded, so a chunk may run past the row (those slots are masked by the caller)
 template <int IPL>
