@@ -50,6 +50,9 @@ constexpr int kFoldChunks = 8;   // fp32 partial sums span at most 128 neighbour
 constexpr int kBatch = 8;       // gathers issued back to back per lane (full chunks)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kDefaultOcc = 2;
+constexpr int kBigNW = 8;
+constexpr int kGrab = 2;
+constexpr bool kDynSchedule = true;  // row batches per atomic grab of layer_kernel's dynamic schedule  // warps per block of layer_kernel (2 for graphs that cannot fill the SMs)
 // index chunks start at each row's first entry (scalar index loads) instead of the 16-byte aligned
 // entry below it: fewer masked gather slots per row batch (round-trip fill 0.87 -> 0.92 on the
 // headline graph); measured headline -1.5%, Large -5% per filter step (profiles/r02/idx_any.txt)
@@ -147,6 +150,7 @@ struct LayerArgs {
     float idx_ef;   // fraction of index-stream loads marked L2 evict_first
     float st_ef;    // fraction of output stores marked L2 evict_first
     int idx_any;    // 1: index chunks start at the row's first entry (scalar index loads), 0: 16-byte aligned
+    int* sched;     // layer_kernel: this launch's row-batch counter (zero at launch; nullptr: static schedule)
 };
 
 // (mu, 1/sigma) of column c from exact sums; std with ddof (0 = population, reading A2; the
@@ -302,11 +306,30 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
 #pragma unroll
     for (int k = 0; k < OC; ++k) s1[k] = s2[k] = 0.0;
 
-    const int64_t step = (int64_t)gridDim.x * NG;
+    // Row-batch schedule: batch b = rows [bG, bG + G) of the relabelled CSR.  Dynamic (p.sched):
+    // every warp takes kGrab consecutive batches at a time (its first grab by index, the rest from
+    // an atomic counter: one same-address atomic per grab -- they serialise at ~5 ns each, so the
+    // host enables this only when every warp gets >= 4 grabs), so the front
+    // still sweeps the rows in order (L2 locality) and no SM idles at the end of the launch
+    // (static striding left the SMs idle 12.6% of the launch on average: ncu sm__cycles_active
+    // 718K of 821K elapsed, min 654K).  The next grab is requested one batch before it is
+    // needed (lane 0 holds it until then).  Static (no counter): warp w takes w, w + warps, ...
+    // The row sums do not depend on the schedule and the column sums are exact: same output.
+    const int64_t nbat = (p.n + G - 1) / G;
+    const bool dyn = p.sched != nullptr;
+    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    int64_t bat;
+    int gi = 0, pend = 0;  // batch within the current grab; lane 0: the grab after it
+    if (dyn) {  // first grab: the warp's own index; the counter hands out the grabs after them
+        if (lane == 0) pend = (int)nwarps + atomicAdd(p.sched, 1);
+        bat = ((int64_t)blockIdx.x * kWarps + warp) * kGrab;
+    } else {
+        bat = (int64_t)blockIdx.x * kWarps + warp;
+    }
     // The row-pointer -> index -> gather chain of a row batch is started one batch ahead:
     // the next batch's row pointers are loaded when a batch begins, and its first index
     // chunk once the batch's first gathers are in flight (nbeg/nend/jfirst).
-    int64_t base = (int64_t)blockIdx.x * NG + warp * G;
+    int64_t base = bat * G;
     int32_t nbeg = 0, nend = 0;
     int jfirst[IPL];
     if (base + g < p.n) {
@@ -325,7 +348,16 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
     __syncthreads();
     // warp-uniform batches of G consecutive rows of the relabelled CSR (degree-sorted, within
     // communities for the community order: neighbouring rows have similar trip counts)
-    for (; base < p.n; base += step) {
+    while (bat < nbat) {
+        base = bat * G;
+        int64_t nxt;  // the batch after this one
+        if (!dyn)
+            nxt = bat + nwarps;
+        else if (gi + 1 < kGrab)
+            nxt = bat + 1;
+        else
+            nxt = (int64_t)__shfl_sync(kFull, pend, 0) * kGrab;
+        const int64_t nbase = nxt * G;
         const int32_t row = (int32_t)(base + g);
         const bool valid = row < p.n;
         float t8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -342,10 +374,17 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
             if (p.sums_in) cc2 = __ldg(p.cc + row);
         }
         nbeg = nend = 0;
-        if (base + step + g < p.n) {
-            nbeg = __ldg(p.rp + base + step + g);
-            nend = __ldg(p.rp + base + step + g + 1);
+        if (nbase + g < p.n) {
+            nbeg = __ldg(p.rp + nbase + g);
+            nend = __ldg(p.rp + nbase + g + 1);
         }
+        if (dyn) {  // entering the next grab after this batch: request the one after it
+            if (++gi == kGrab) {
+                gi = 0;
+                if (lane == 0) pend = (int)nwarps + atomicAdd(p.sched, 1);
+            }
+        }
+        bat = nxt;
         // neighbour sum: packed fp32 within up to kFoldChunks chunks, then folded into
         // fp64 partials in shared memory (only rows longer than 128 neighbours fold).
         // The chunk loop is warp-uniform (the warp's rows have similar degrees), so the
@@ -964,7 +1003,7 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     const int L = o.steps, d = o.d, nslices = d / W;
     // graphs too small to give every SM a block of 8 warps run 2-warp blocks (4x the blocks)
     const bool small = (n + 8 * (256 / W) - 1) / (8 * (256 / W)) < di.num_sms;
-    const int grid = small ? layer_grid<W, MB, 2>(n, di) : layer_grid<W, MB, 8>(n, di);
+    const int grid = small ? layer_grid<W, MB, 2>(n, di) : layer_grid<W, MB, kBigNW>(n, di);
     // warp-specialised filter step (layer_ws_kernel) where the gathers are DRAM-bound: a W >= 64
     // slice beyond 4x the L2 (Large: 1.28 GB; measured -5% per step there, +18% at the L2-sized
     // headline slice, where its 4 epilogue warps per SM cannot keep up -- DESIGN.md §5).
@@ -995,13 +1034,23 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     const size_t off_y0 = al(off_cc + sizeof(float2) * ((size_t)n + 2));
     const size_t off_y1 = al(off_y0 + sizeof(float) * nw);
     const size_t off_sums = al(off_y1 + sizeof(float) * nw);
-    const size_t sums_bytes = sizeof(double) * (size_t)nslices * (L + 1) * 2 * W;
+    // exact column sums [slices][L+1][2W] doubles, then the filter steps' row-batch counters
+    // [slices][L+1] ints: zeroed together once per embed
+    const size_t sums_bytes =
+        sizeof(double) * (size_t)nslices * (L + 1) * 2 * W + sizeof(int) * (size_t)nslices * (L + 1);
     char* ws = nullptr;
     IGP_CUDA(alloc_async((void**)&ws, off_sums + sums_bytes, s), "embed workspace alloc");
     float2* sr = (float2*)(ws + off_sr);
     float2* cc = (float2*)(ws + off_cc);
     float4* ybuf[2] = {(float4*)(ws + off_y0), (float4*)(ws + off_y1)};
     double* sums = (double*)(ws + off_sums);
+    int* sched = (int*)(sums + (size_t)nslices * (L + 1) * 2 * W);
+    bool dyn_sched = kDynSchedule;  // development knob IGP_DYN=0: static row-batch striding
+    if (const char* e = getenv("IGP_DYN")) dyn_sched = atoi(e) != 0;
+    // layer_kernel's dynamic schedule pays off once every warp takes several grabs
+    const int64_t lk_warps = (int64_t)grid * (small ? 2 : kBigNW);
+    const int64_t lk_batches = ((int64_t)n + (256 / W) - 1) / (256 / W);
+    const bool use_dyn = dyn_sched && !small && lk_batches >= 4 * lk_warps * kGrab;
     // stats grid 2^-gexp with N * 2^gexp < 2^51 (|sum t|, sum t^2 <= N)
     int lg = 0;
     while (lg < 62 && ((int64_t)1 << lg) <= (int64_t)n) ++lg;
@@ -1080,10 +1129,11 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 a.idx_ef = idx_ef;
                 a.st_ef = st_ef;
                 a.idx_any = idx_any;
+                a.sched = use_dyn ? sched + (size_t)k * (L + 1) + l : nullptr;
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(grid);
-                cfg.blockDim = dim3(small ? 64 : 256);
-                cfg.dynamicSmemBytes = small ? layer_smem<W, 2>() : layer_smem<W, 8>();
+                cfg.blockDim = dim3(small ? 64 : kBigNW * 32);
+                cfg.dynamicSmemBytes = small ? layer_smem<W, 2>() : layer_smem<W, kBigNW>();
                 cfg.stream = s;
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1099,11 +1149,11 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                         le = cudaLaunchKernelEx(&cfg, layer_ws_kernel<W>, a);
                     } else {
                         le = small ? cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 2>, a)
-                                   : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 8>, a);
+                                   : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, kBigNW>, a);
                     }
                 } else {
                     le = small ? cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 2>, a)
-                               : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, 8>, a);
+                               : cudaLaunchKernelEx(&cfg, layer_kernel<W, MB, kBigNW>, a);
                 }
                 if ((rc = cuda_status(le, "layer_kernel launch")) != IGP_OK) break;
                 if ((rc = launch_status("layer_kernel")) != IGP_OK) break;
