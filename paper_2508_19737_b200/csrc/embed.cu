@@ -50,9 +50,10 @@ constexpr int kFoldChunks = 8;   // fp32 partial sums span at most 128 neighbour
 constexpr int kBatch = 8;       // gathers issued back to back per lane (full chunks)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kDefaultOcc = 2;
-constexpr int kBigNW = 8;
-constexpr int kGrab = 2;
-constexpr bool kDynSchedule = true;  // row batches per atomic grab of layer_kernel's dynamic schedule  // warps per block of layer_kernel (2 for graphs that cannot fill the SMs)
+constexpr int kBigNW = 8;  // warps per block of layer_kernel (2 for graphs that cannot fill the SMs)
+constexpr int kGrab = 1;  // row batches per atomic grab of layer_kernel's dynamic schedule
+constexpr bool kDynSchedule = true;
+constexpr int kCounters = 4;  // row-batch counters per launch (warps spread over them)
 // index chunks start at each row's first entry (scalar index loads) instead of the 16-byte aligned
 // entry below it: fewer masked gather slots per row batch (round-trip fill 0.87 -> 0.92 on the
 // headline graph); measured headline -1.5%, Large -5% per filter step (profiles/r02/idx_any.txt)
@@ -320,9 +321,15 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     int64_t bat;
     int gi = 0, pend = 0;  // batch within the current grab; lane 0: the grab after it
-    if (dyn) {  // first grab: the warp's own index; the counter hands out the grabs after them
-        if (lane == 0) pend = (int)nwarps + atomicAdd(p.sched, 1);
-        bat = ((int64_t)blockIdx.x * kWarps + warp) * kGrab;
+    // kCounters counters: warp w draws from counter c = w mod kCounters, whose tickets t map to
+    // the grabs g = t kCounters + c (fewer same-address atomics per counter)
+    const int64_t wid = (int64_t)blockIdx.x * kWarps + warp;
+    const int cidx = (int)(wid % kCounters);
+    const int tick0 = (int)((nwarps - cidx + kCounters - 1) / kCounters);  // tickets of the static first grabs
+    int* ctr = p.sched + cidx;
+    if (dyn) {  // first grab: the warp's own index; the counters hand out the grabs after them
+        if (lane == 0) pend = (tick0 + atomicAdd(ctr, 1)) * kCounters + cidx;
+        bat = wid * kGrab;
     } else {
         bat = (int64_t)blockIdx.x * kWarps + warp;
     }
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
         if (dyn) {  // entering the next grab after this batch: request the one after it
             if (++gi == kGrab) {
                 gi = 0;
-                if (lane == 0) pend = (int)nwarps + atomicAdd(p.sched, 1);
+                if (lane == 0) pend = (tick0 + atomicAdd(ctr, 1)) * kCounters + cidx;
             }
         }
         bat = nxt;
@@ -1035,9 +1042,9 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     const size_t off_y1 = al(off_y0 + sizeof(float) * nw);
     const size_t off_sums = al(off_y1 + sizeof(float) * nw);
     // exact column sums [slices][L+1][2W] doubles, then the filter steps' row-batch counters
-    // [slices][L+1] ints: zeroed together once per embed
+    // [slices][L+1][kCounters] ints: zeroed together once per embed
     const size_t sums_bytes =
-        sizeof(double) * (size_t)nslices * (L + 1) * 2 * W + sizeof(int) * (size_t)nslices * (L + 1);
+        sizeof(double) * (size_t)nslices * (L + 1) * 2 * W + sizeof(int) * (size_t)nslices * (L + 1) * kCounters;
     char* ws = nullptr;
     IGP_CUDA(alloc_async((void**)&ws, off_sums + sums_bytes, s), "embed workspace alloc");
     float2* sr = (float2*)(ws + off_sr);
@@ -1050,7 +1057,9 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     // layer_kernel's dynamic schedule pays off once every warp takes several grabs
     const int64_t lk_warps = (int64_t)grid * (small ? 2 : kBigNW);
     const int64_t lk_batches = ((int64_t)n + (256 / W) - 1) / (256 / W);
-    const bool use_dyn = dyn_sched && !small && lk_batches >= 4 * lk_warps * kGrab;
+    int dyn_min = 4;  // development knob IGP_DYN_MIN: grabs per warp below which the schedule stays static
+    if (const char* e = getenv("IGP_DYN_MIN")) dyn_min = atoi(e);
+    const bool use_dyn = dyn_sched && !small && lk_batches >= (int64_t)dyn_min * lk_warps * kGrab;
     // stats grid 2^-gexp with N * 2^gexp < 2^51 (|sum t|, sum t^2 <= N)
     int lg = 0;
     while (lg < 62 && ((int64_t)1 << lg) <= (int64_t)n) ++lg;
@@ -1129,7 +1138,7 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
                 a.idx_ef = idx_ef;
                 a.st_ef = st_ef;
                 a.idx_any = idx_any;
-                a.sched = use_dyn ? sched + (size_t)k * (L + 1) + l : nullptr;
+                a.sched = use_dyn ? sched + ((size_t)k * (L + 1) + l) * kCounters : nullptr;
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(grid);
                 cfg.blockDim = dim3(small ? 64 : kBigNW * 32);
