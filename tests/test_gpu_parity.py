@@ -278,6 +278,22 @@ def test_headline_csr_bit_exact(igp, headline):
     check_csr(igp, edges, c.num_nodes)
 
 
+def test_headline_dynamic_schedule_bit_identical(igp, headline, monkeypatch):
+    """layer_kernel's dynamic row-batch schedule (atomic counters; on at the headline size,
+    DESIGN.md §5) changes only which warp finishes which rows: the embedding is bit-identical to
+    the static striding's (IGP_DYN=0), full size, both row orders that use it."""
+    c, edges = headline
+    e = torch.from_numpy(edges).cuda()
+    for order in ("community", "degree"):
+        g = igp.build_graph(e, c.num_nodes, order=order)
+        outs = []
+        for dyn in ("0", "1"):
+            monkeypatch.setenv("IGP_DYN", dyn)
+            outs.append(igp.embed(g, c.tau, c.d, 6, 0))
+        g.close()
+        assert torch.equal(outs[0], outs[1]), order
+
+
 QUICK = os.environ.get("IGP_QUICK") == "1"  # development runs: reduced L at the full sizes
 
 
