@@ -54,6 +54,7 @@ constexpr int kBigNW = 8;  // warps per block of layer_kernel (2 for graphs that
 constexpr int kGrab = 1;  // row batches per atomic grab of layer_kernel's dynamic schedule
 constexpr bool kDynSchedule = true;
 constexpr int kCounters = 4;  // row-batch counters per launch (warps spread over them)
+constexpr int64_t kDynMinEdgesPerWarp = 2048;  // CSR entries per warp below which the schedule stays static
 // index chunks start at each row's first entry (scalar index loads) instead of the 16-byte aligned
 // entry below it: fewer masked gather slots per row batch (round-trip fill 0.87 -> 0.92 on the
 // headline graph); measured headline -1.5%, Large -5% per filter step (profiles/r02/idx_any.txt)
@@ -1059,7 +1060,10 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     const int64_t lk_batches = ((int64_t)n + (256 / W) - 1) / (256 / W);
     int dyn_min = 4;  // development knob IGP_DYN_MIN: grabs per warp below which the schedule stays static
     if (const char* e = getenv("IGP_DYN_MIN")) dyn_min = atoi(e);
-    const bool use_dyn = dyn_sched && !small && lk_batches >= (int64_t)dyn_min * lk_warps * kGrab;
+    // ... and once a warp's share of the edges outlasts the counters' atomics (sparse graphs: the
+    // streaming config's early stages ran 9% slower with it; cap ~ nnz)
+    const bool use_dyn = dyn_sched && !small && lk_batches >= (int64_t)dyn_min * lk_warps * kGrab &&
+                         g.cap >= kDynMinEdgesPerWarp * lk_warps;
     // stats grid 2^-gexp with N * 2^gexp < 2^51 (|sum t|, sum t^2 <= N)
     int lg = 0;
     while (lg < 62 && ((int64_t)1 << lg) <= (int64_t)n) ++lg;
