@@ -157,13 +157,10 @@ KERNEL_SRC = os.path.join(ROOT, "paper_2508_19737_b200", "csrc", "embed.cu")
 
 
 def layer_kernel_name(n, width):
-    """The filter-step kernel embed.cu launches for this slice (run_embed_w's rule): the
-    warp-specialised layer_ws_kernel where a W >= 64 slice exceeds 4x the L2, else layer_kernel."""
-    import torch
-
-    l2 = torch.cuda.get_device_properties(0).L2_cache_size if torch.cuda.is_available() else 0
+    """The filter-step kernel embed.cu launches for this slice (run_embed_w's rule): layer_kernel,
+    or the warp-specialised layer_ws_kernel when IGP_LAYER_WS=1 opts in (W >= 32)."""
     env = os.environ.get("IGP_LAYER_WS")
-    ws = env != "0" if env is not None else (width >= 64 and n * width * 4 > 4 * l2)
+    ws = env is not None and env != "0"
     return "layer_ws_kernel" if ws and width >= 32 else "layer_kernel"
 
 

@@ -1012,15 +1012,16 @@ igp_status run_embed_w(const CsrDevice& g, const igp_embed_opts& o, float* out, 
     // graphs too small to give every SM a block of 8 warps run 2-warp blocks (4x the blocks)
     const bool small = (n + 8 * (256 / W) - 1) / (8 * (256 / W)) < di.num_sms;
     const int grid = small ? layer_grid<W, MB, 2>(n, di) : layer_grid<W, MB, kBigNW>(n, di);
-    // warp-specialised filter step (layer_ws_kernel) where the gathers are DRAM-bound: a W >= 64
-    // slice beyond 4x the L2 (Large: 1.28 GB; measured -5% per step there, +18% at the L2-sized
-    // headline slice, where its 4 epilogue warps per SM cannot keep up -- DESIGN.md §5).
-    // Development knob IGP_LAYER_WS=0/1 forces it off / on (W >= 32).
+    // warp-specialised filter step (layer_ws_kernel): opt-in only (IGP_LAYER_WS=1, W >= 32).  It
+    // beat the statically scheduled layer_kernel where the gathers are DRAM-bound (Large: -5% per
+    // launch) and lost at the L2-sized headline slice (+18%: its 4 epilogue warps per SM cannot
+    // keep up); layer_kernel with the dynamic row-batch schedule beats it on both (Large 5.39 vs
+    // 5.64 ms per launch, interleaved A/B -- DESIGN.md §5).
     bool use_ws = false;
     int ws_grid = 0;
     if constexpr (W >= 32) {
         const char* e = getenv("IGP_LAYER_WS");
-        use_ws = !small && (e ? atoi(e) != 0 : (W >= 64 && (double)n * W * 4.0 > 4.0 * (double)di.l2_bytes));
+        use_ws = !small && e != nullptr && atoi(e) != 0;
         if (use_ws) {
             cudaFuncSetAttribute(layer_ws_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)layer_ws_smem<W>());
             int o = 0;
