@@ -294,6 +294,31 @@ def test_headline_dynamic_schedule_bit_identical(igp, headline, monkeypatch):
         assert torch.equal(outs[0], outs[1]), order
 
 
+def test_dynamic_schedule_ragged_tail(igp, monkeypatch):
+    """The dynamic row-batch schedule where it is on (>= 4 batches and >= 2048 CSR entries per
+    warp) with a ragged N (a partial last batch) and rows of every length: bit-identical to the
+    static striding, and within the tolerance of the oracle."""
+    n, d, L = 300_007, 32, 3
+    rng = np.random.default_rng(11)
+    m = 4_000_000
+    u = rng.integers(0, n, m)
+    v = (u + rng.integers(1, 2000, m)) % n  # banded: neighbours near in id (community-like)
+    hubs = rng.integers(0, 64, 20_000)      # a few long rows (fold path)
+    edges = np.concatenate([np.stack([u, v], 1), np.stack([hubs, rng.integers(0, n, hubs.size)], 1)])
+    edges = edges.astype(np.int32)
+    g = gpu_graph(igp, edges, n)
+    outs = []
+    for dyn in ("0", "1"):
+        monkeypatch.setenv("IGP_DYN", dyn)
+        outs.append(igp.embed(g, -1.0, d, L, 9))
+    assert torch.equal(outs[0], outs[1])
+    rp, ci, _ = oracle.build_csr(edges, n)
+    ref = oracle.embed(rp, ci, n, d, L, -1.0, seed=9, mode=oracle.MODE_FULL, nthreads=NTHREADS)
+    err = row_rel_err(outs[1].cpu().numpy(), ref)
+    record("dyn_schedule_ragged", err)
+    assert err <= TOL
+
+
 QUICK = os.environ.get("IGP_QUICK") == "1"  # development runs: reduced L at the full sizes
 
 
