@@ -309,21 +309,21 @@ __global__ void __launch_bounds__(NW * 32, MB) layer_kernel(const LayerArgs p) {
     for (int k = 0; k < OC; ++k) s1[k] = s2[k] = 0.0;
 
     // Row-batch schedule: batch b = rows [bG, bG + G) of the relabelled CSR.  Dynamic (p.sched):
-    // every warp takes kGrab consecutive batches at a time (its first grab by index, the rest from
-    // an atomic counter: one same-address atomic per grab -- they serialise at ~5 ns each, so the
-    // host enables this only when every warp gets >= 4 grabs), so the front
-    // still sweeps the rows in order (L2 locality) and no SM idles at the end of the launch
-    // (static striding left the SMs idle 12.6% of the launch on average: ncu sm__cycles_active
-    // 718K of 821K elapsed, min 654K).  The next grab is requested one batch before it is
-    // needed (lane 0 holds it until then).  Static (no counter): warp w takes w, w + warps, ...
-    // The row sums do not depend on the schedule and the column sums are exact: same output.
+    // a warp's first grab of kGrab batches is its own index, every later one a ticket from one of
+    // kCounters atomic counters (warp w -> counter c = w mod kCounters, ticket t -> grab
+    // t kCounters + c), requested one batch before it is needed (lane 0 holds it until then).  The
+    // rows in flight stay one narrow front sweeping the CSR in order -- the in-community gathers
+    // hit L2 before it turns over (8-batch grabs, a 4x wider front, were 47% slower) -- and no SM
+    // idles at the end (static striding: SMs active 718K of 821K cycles, min 654K; dynamic: 95%).
+    // Same-address atomics serialise (~5 ns each), so the host enables it only when every warp gets
+    // >= 4 batches and >= 2048 CSR entries.  Static (no counter): warp w takes
+    // batches w, w + warps, ...  The row sums do not depend on the schedule and the column sums
+    // are exact: the output is bit-identical either way.
     const int64_t nbat = (p.n + G - 1) / G;
     const bool dyn = p.sched != nullptr;
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     int64_t bat;
     int gi = 0, pend = 0;  // batch within the current grab; lane 0: the grab after it
-    // kCounters counters: warp w draws from counter c = w mod kCounters, whose tickets t map to
-    // the grabs g = t kCounters + c (fewer same-address atomics per counter)
     const int64_t wid = (int64_t)blockIdx.x * kWarps + warp;
     const int cidx = (int)(wid % kCounters);
     const int tick0 = (int)((nwarps - cidx + kCounters - 1) / kCounters);  // tickets of the static first grabs
