@@ -26,6 +26,8 @@ re-launches itself under torch.distributed.run with N processes.
 --config streaming: one step = the 10 cumulative stages of BASELINE.json config 4
 (stage 0 build, stages 1-9 igp_graph_add_edges merges, each followed by a re-embed
 with Philox subsequence t, Alg. 2 l.1-7); per-stage merge / embed ms are reported.
+The default headline run also reports the streaming config's per-stage merge / re-embed ms
+("streaming_stages", measured after the timed region; --no-side skips it).
 After the timed region the downstream BIRCH (Alg. 1 l.7) is timed once on the step's
 embedding and reported beside the FFP ("birch"), with the oracle's BIRCH time.
 """
@@ -461,6 +463,56 @@ def streaming_alg2_leg(args, igp, batches, N, d, L, tau, seed, stream, dev):
 
 
 # ---------------------------------------------------------------- GPU arm
+def streaming_side_leg(igp, dev, stream, reps=3):
+    """BASELINE.json config 4 (Alg. 2 l.1-7) measured inside the default headline
+    run, after its timed region, so a driver-run line carries per-stage merge / re-embed times:
+    stage 0 build, stages 1-9 igp_graph_add_edges merges, each followed by a re-embed with
+    Philox subsequence t.  Medians over `reps` runs after one warm-up; CUDA events on `stream`."""
+    import torch
+    cfg = CONFIGS["streaming"]
+    edges_np, _ = generate(cfg, seed=cfg.seed)
+    batches = [torch.from_numpy(b).to(dev) for b in stream_batches(edges_np, 10)]
+    N, d, L, tau = cfg.num_nodes, cfg.d, cfg.steps, cfg.tau
+    out = torch.empty((N, d), dtype=torch.float32, device=dev)
+    runs = []
+    for r in range(reps + 1):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g = igp.build_graph(batches[0], N, stream=stream, async_build=True)
+        for t in range(10):
+            if t > 0:
+                g.add_edges(batches[t], stream=stream)
+            ev[t][0].record(stream)
+            igp.embed(g, tau, d, L, cfg.seed, out=out, stream=stream, subsequence=t)
+            ev[t][1].record(stream)
+        torch.cuda.synchronize(dev)
+        nnz = g.nnz
+        g.close()
+        starts = [e0] + [ev[t - 1][1] for t in range(1, 10)]
+        if r > 0:  # r == 0 warms up
+            runs.append(([starts[t].elapsed_time(ev[t][0]) for t in range(10)],
+                         [a.elapsed_time(b) for a, b in ev], e0.elapsed_time(ev[9][1])))
+    fb = []
+    all_edges = torch.cat(batches)
+    for _ in range(reps + 1):
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        gf = igp.build_graph(all_edges, N, stream=stream, async_build=True)
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        gf.close()
+        fb.append(f0.elapsed_time(f1))
+    med = lambda xs: float(np.median(xs))  # noqa: E731
+    merge = [med([r[0][t] for r in runs]) for t in range(10)]
+    emb = [med([r[1][t] for r in runs]) for t in range(10)]
+    fresh = med(fb[1:])
+    return {"workload": "streaming (BASELINE.json config 4): N=200,000, 10 cumulative stages",
+            "final_nnz": int(nnz), "d": d, "L": L, "tau": tau, "reps": reps,
+            "build_or_merge_ms": merge, "embed_ms": emb, "ten_stage_ms": med([r[2] for r in runs]),
+            "fresh_build_of_final_graph_ms": fresh, "merge_stage9_vs_fresh_build": merge[9] / fresh}
+
+
 def run_gpu(args, cfg):
     import torch
     rank, world, local = dist_env()
@@ -678,6 +730,14 @@ def run_gpu(args, cfg):
         except Exception as exc:  # noqa: BLE001
             line["birch"] = {"error": f"{type(exc).__name__}: {exc}"}
 
+    # the streaming config's per-stage merge / re-embed times beside the headline (not part of
+    # the headline step or its value)
+    if rank == 0 and world == 1 and cfg.name == "headline" and not args.no_side:
+        try:
+            line["streaming_stages"] = streaming_side_leg(igp, dev, stream)
+        except Exception as exc:  # noqa: BLE001
+            line["streaming_stages"] = {"error": f"{type(exc).__name__}: {exc}"}
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = cpu_cores()
         secs, onnz = oracle_sample(cfg, edges_np if not streaming else np.concatenate(stream_batches(edges_np, 10)),
@@ -707,6 +767,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-birch", action="store_true")
+    ap.add_argument("--no-side", action="store_true", help="skip the streaming per-stage leg of the headline run")
     ap.add_argument("--birch-threshold", type=float, default=1.0)  # reading B1
     ap.add_argument("--birch-branching", type=int, default=50)
     ap.add_argument("--birch-oracle-rows", type=int, default=200_000)
