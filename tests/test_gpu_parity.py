@@ -320,14 +320,20 @@ def test_dynamic_schedule_ragged_tail(igp, monkeypatch):
 
 
 QUICK = os.environ.get("IGP_QUICK") == "1"  # development runs: reduced L at the full sizes
+# The oracle's fp32 twin at the full headline size and L = 60 costs ~150 s of host time and gates
+# nothing (it is a reported floor): opt-in.  The recorded value (4.0e-6, beside the GPU's 4.1e-6)
+# is in profiles/r02/parity_gpu_full_suite.json and profiles/r02/final_s4/.
+FULL_FLOORS = os.environ.get("IGP_FULL_FLOORS") == "1"
 
 
 def test_headline_parity_full_steps(igp, headline):
     """The bench workload itself: full N / nnz / d / L = 60, the same kernels and grid as
-    bench.py, element by element against the fp64 oracle (IGP_QUICK=1: L = 3)."""
+    bench.py, element by element against the fp64 oracle (IGP_QUICK=1: L = 3;
+    IGP_FULL_FLOORS=1 also runs the oracle's fp32 twin and records its drift)."""
     c, edges = headline
     L = 3 if QUICK else c.steps
-    z, ref = run_parity(igp, edges, c.num_nodes, c.d, L, c.tau, floor=f"headline_L{L}")
+    z, ref = run_parity(igp, edges, c.num_nodes, c.d, L, c.tau,
+                        floor=f"headline_L{L}" if (FULL_FLOORS or QUICK) else None)
     err = row_rel_err(z, ref)
     record(f"headline_L{L}", err)
     assert err <= TOL
